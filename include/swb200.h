@@ -1,0 +1,213 @@
+/* swb200.h -- C-ABI of the B200-native SW#db scoring path (libswb200.so).
+ *
+ * This is the drop-in boundary for the reference's database-search hot path.  Plain pointers and
+ * sizes only; no C++/torch types; no exception ever crosses it.  Every function returns an
+ * swb_status; swb_last_error() gives the message for the calling thread.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj/include/swsearch):
+ *
+ *   swb_db_create / _flat     partition_database          scheduler.hpp:56-65   (length routing)
+ *                             + the per-chunk pointer gather  scheduler.hpp:156-160
+ *                             (here: one-off length-sorted, interleaved packing, resident in HBM)
+ *   swb_search                run_search, lines           scheduler.hpp:188-244
+ *                             (profile -> partition -> both kernels -> merge_results), i.e. the
+ *                             region SPEC.md:403 times; traceback (scheduler.hpp:246-249) stays host C++
+ *   swb_search_keys           the same, returning packed sort keys for the multi-GPU merge
+ *   swb_merge_keys            merge_results               scheduler.hpp:106-117  (across shards)
+ *   swb_score_all             "sequential scalar scan"    scheduler.hpp:179-183  (all N scores)
+ *   swb_score_batch           sw_score_batch              align.hpp:91-159
+ *   swb_score_pair            sw_score_wavefront          align.hpp:166-229
+ *   swb_mdb_*                 run_search over several GPUs of one box in one process
+ *                             (no reference equivalent: SPEC.md:342 lists device offload as a non-goal)
+ *
+ * Semantics common to all scoring entry points: residue codes are 0..23 in the order of
+ * alphabet.hpp:60 ("ARNDCQEGHILKMFPSTWYVBZX*"); `matrix` is the 24x24 row-major int32 table of
+ * scoring.hpp:32,42 indexed [subject_code*24 + query_code] exactly like align.hpp:34,74;
+ * gaps are positive magnitudes with open >= extend >= 0 (scoring.hpp:50-53); a score is the int32
+ * value of align.hpp:42-64 -- bit-exact, whichever kernel (packed int16 DPX, int32 re-run,
+ * intra-task) produced it.  Hits are ordered score descending, then db_index ascending
+ * (scheduler.hpp:111-114) and every database sequence, including empty ones, is a candidate
+ * (scheduler.hpp:163,171).
+ *
+ * There is no CPU fallback: without a usable CUDA device every compute entry point fails with
+ * SWB_ERR_CUDA.
+ */
+#ifndef SWB200_H
+#define SWB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum swb_status {
+    SWB_OK = 0,
+    SWB_ERR_INVALID = 1,     /* bad argument: maps to std::invalid_argument in the C++ shim      */
+    SWB_ERR_RANGE = 2,       /* residue / query code >= 24: std::out_of_range (scoring.hpp:203)   */
+    SWB_ERR_CUDA = 3,        /* CUDA runtime / driver failure, or no device                       */
+    SWB_ERR_NCCL = 4,        /* NCCL failure in the multi-GPU merge                               */
+    SWB_ERR_UNSUPPORTED = 5, /* scores would leave the exact int32 range this build guarantees    */
+    SWB_ERR_INTERNAL = 6
+} swb_status;
+
+typedef struct swb_db swb_db;   /* one packed database shard resident on one GPU */
+typedef struct swb_mdb swb_mdb; /* a database sharded over several GPUs of one process */
+
+typedef struct swb_hit {
+    uint32_t db_index; /* position in the caller's database (Hit::db_index, scheduler.hpp:88) */
+    int32_t score;     /* Hit::score.value */
+} swb_hit;
+
+/* Execution report.  The first three fields are SearchStats (scheduler.hpp:120-124). */
+typedef struct swb_stats {
+    uint64_t lane_scored;      /* sequences scored by the inter-task kernel                       */
+    uint64_t wavefront_scored; /* sequences scored by the intra-task kernel                       */
+    uint64_t chunks_claimed;   /* work units launched: interleaved groups + long sequences        */
+    uint64_t rescored_i32;     /* sequences flagged by the int16 pass and re-run in int32         */
+    uint64_t cells;            /* query_len x residues of this shard (GCUPS numerator)*/
+    uint64_t padded_cells;     /* cells executed including row/column padding                     */
+    uint32_t kernel_launches;  /* launches of this library's kernels during the call              */
+    uint32_t reserved;
+    float ms_total;            /* device time of the call (CUDA events on the search stream)      */
+    float ms_inter;            /* inter-task int16 kernel                                         */
+    float ms_intra;            /* intra-task kernel                                               */
+    float ms_rescore;          /* int32 re-run                                                    */
+    float ms_topk;             /* key build + top-k select                                        */
+    float ms_h2d_d2h;          /* query/profile upload + result download                          */
+} swb_stats;
+
+typedef struct swb_db_info {
+    uint32_t n_total;          /* sequences in the whole database                                 */
+    uint32_t n_local;          /* sequences held by this shard                                    */
+    uint32_t n_short;          /* ... routed to the inter-task kernel (length < threshold)        */
+    uint32_t n_long;           /* ... routed to the intra-task kernel                             */
+    uint32_t n_groups;         /* interleaved groups of 64 short sequences                        */
+    uint32_t max_length;       /* longest sequence in this shard                                  */
+    uint32_t shard_rank;
+    uint32_t shard_count;
+    uint64_t residues;         /* real residues in this shard                                     */
+    uint64_t padded_residues;  /* residues stored including padding                               */
+    uint64_t device_bytes;     /* HBM held by this handle (database + work buffers)               */
+    uint64_t length_threshold;
+    int32_t device;
+    int32_t reserved;
+} swb_db_info;
+
+const char* swb_last_error(void);
+const char* swb_version(void);
+swb_status swb_device_count(int32_t* count);
+
+/* Pack the caller's database and make it resident on `device`.
+ *   seqs[i]/lens[i]   residue codes of sequence i (EncodedSequence::codes, sequence.hpp:22);
+ *                     seqs[i] may be NULL when lens[i] == 0.
+ *   length_threshold  SearchConfig::length_threshold (scheduler.hpp:24): length < threshold goes
+ *                     to the inter-task kernel, the rest to the intra-task kernel.
+ *   shard_rank/count  this handle keeps only its residue-balanced share of the database
+ *                     (count = 1: everything).  db_index values stay global.
+ * The input is not referenced after the call returns. */
+swb_status swb_db_create(const uint8_t* const* seqs, const uint32_t* lens, uint32_t n,
+                         uint64_t length_threshold, int32_t device, uint32_t shard_rank,
+                         uint32_t shard_count, swb_db** out);
+
+/* Same, from concatenated codes and n+1 offsets. */
+swb_status swb_db_create_flat(const uint8_t* codes, const uint64_t* offsets, uint32_t n,
+                              uint64_t length_threshold, int32_t device, uint32_t shard_rank,
+                              uint32_t shard_count, swb_db** out);
+
+void swb_db_destroy(swb_db* db);
+swb_status swb_db_info_get(const swb_db* db, swb_db_info* info);
+
+/* Use an externally owned cudaStream_t (passed as an integer/pointer value, e.g.
+ * torch.cuda.current_stream().cuda_stream) for all work of this handle; 0 restores the
+ * handle's own stream. */
+swb_status swb_db_set_stream(swb_db* db, void* cuda_stream);
+
+/* One query against the shard: scores every sequence, selects the top_k hits.
+ *   hits      room for top_k entries;  *n_hits = min(top_k, n_local)
+ *   stats     optional
+ * Host buffers in, host buffers out; synchronous. */
+swb_status swb_search(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
+                      int32_t gap_open, int32_t gap_extend, uint32_t top_k, swb_hit* hits,
+                      uint32_t* n_hits, swb_stats* stats);
+
+/* As swb_search, but returns the shard's top_k as packed 64-bit keys
+ *   key = (uint64(score) << 32) | (0xFFFFFFFF - db_index)
+ * in descending key order, padded with 0 up to top_k entries (0 is never a valid key).  A plain
+ * descending sort of the union of all shards' keys reproduces scheduler.hpp:111-114.
+ *   host_keys    optional host buffer of top_k entries
+ *   device_keys  optional: receives a device pointer (valid until the next call on this handle)
+ *                to the same top_k keys, for a collective without a host round trip. */
+swb_status swb_search_keys(swb_db* db, const uint8_t* query, uint32_t query_len,
+                           const int32_t* matrix, int32_t gap_open, int32_t gap_extend,
+                           uint32_t top_k, uint64_t* host_keys, void** device_keys,
+                           swb_stats* stats);
+
+/* Top-k select over n packed keys on `device` (the cross-shard merge; zeros are ignored).
+ * keys is a host pointer unless keys_on_device != 0. */
+swb_status swb_merge_keys(const uint64_t* keys, uint64_t n, int32_t keys_on_device, int32_t device,
+                          uint32_t top_k, swb_hit* hits, uint32_t* n_hits);
+
+/* Scores of every sequence of the whole database in db_index order (n_total entries); entries
+ * belonging to other shards are left untouched. */
+swb_status swb_score_all(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
+                         int32_t gap_open, int32_t gap_extend, int32_t* scores, swb_stats* stats);
+
+/* sw_score_batch (align.hpp:91-159): up to lane_width subjects, NULL = padding lane; out has
+ * lane_width entries, padding lanes 0.  Runs the inter-task kernel (packed int16 + int32 re-run)
+ * on a transient packed batch whatever the subject lengths. */
+swb_status swb_score_batch(const uint8_t* query, uint32_t query_len, const uint8_t* const* subjects,
+                           const uint32_t* lens, uint32_t count, uint32_t lane_width,
+                           const int32_t* matrix, int32_t gap_open, int32_t gap_extend,
+                           int32_t device, int32_t* out);
+
+/* sw_score_wavefront (align.hpp:166-229): one pair on the intra-task kernel. chunk_width is
+ * validated (>= 1, align.hpp:169) and otherwise result-invisible. */
+swb_status swb_score_pair(const uint8_t* query, uint32_t query_len, const uint8_t* subject,
+                          uint32_t subject_len, const int32_t* matrix, int32_t gap_open,
+                          int32_t gap_extend, uint64_t chunk_width, int32_t device, int32_t* score);
+
+/* ---- several GPUs, one process (the C++ drop-in's multi-GPU mode) ------------------------------
+ * The database is dealt by residue count over `n_devices` GPUs; each search runs all shards
+ * concurrently, then the per-shard top-k keys are exchanged with one ncclAllGather and merged.
+ * With n_devices == 1 no NCCL is loaded. */
+swb_status swb_mdb_create_flat(const uint8_t* codes, const uint64_t* offsets, uint32_t n,
+                               uint64_t length_threshold, const int32_t* devices,
+                               uint32_t n_devices, swb_mdb** out);
+swb_status swb_mdb_create(const uint8_t* const* seqs, const uint32_t* lens, uint32_t n,
+                          uint64_t length_threshold, const int32_t* devices, uint32_t n_devices,
+                          swb_mdb** out);
+void swb_mdb_destroy(swb_mdb* mdb);
+swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len,
+                          const int32_t* matrix, int32_t gap_open, int32_t gap_extend,
+                          uint32_t top_k, swb_hit* hits, uint32_t* n_hits, swb_stats* stats);
+uint32_t swb_mdb_shard_count(const swb_mdb* mdb);
+swb_db* swb_mdb_shard(swb_mdb* mdb, uint32_t i);
+
+/* ---- measurement ----------------------------------------------------------------------------
+ * Sustained thread-level instruction rate of the DPX / integer pipes on `device`, measured with
+ * independent chains on every SM for about `seconds`.  Rates are in 1e9 thread-instructions/s. */
+typedef struct swb_pipe_rates {
+    double viaddmnmx_s16x2; /* VIADDMNMX.S16x2  (__viaddmax_s16x2)   -- P_dpx of SURVEY 8(d)      */
+    double vimnmx3_s16x2;   /* VIMNMX3.S16x2    (__vimax3_s16x2_relu)                             */
+    double viadd_16x2;      /* VIADD.16x2       (__vadd2)                                         */
+    double viaddmnmx_s32;   /* VIADDMNMX        (__viaddmax_s32)                                  */
+    double prmt;            /* PRMT                                                               */
+    double imad;            /* IMAD (fma pipe)                                                    */
+    double mix_alu_fma;     /* VIADDMNMX.S16x2 + IMAD issued 1:1, counted as both                 */
+    double sm_clock_mhz;    /* average SM clock during the run (clock64 / wall)                   */
+    int32_t sm_count;
+    int32_t reserved;
+} swb_pipe_rates;
+swb_status swb_measure_pipe_rates(int32_t device, double seconds, swb_pipe_rates* out);
+
+/* Deterministic sharding rule used by swb_db_create (exposed for tests and for hosts that
+ * shard themselves): shard_of[i] for every sequence, given the lengths. */
+swb_status swb_shard_assignment(const uint32_t* lens, uint32_t n, uint64_t length_threshold,
+                                uint32_t shard_count, uint32_t* shard_of);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWB200_H */

@@ -1,0 +1,951 @@
+// cabi.cu -- the C-ABI of include/swb200.h: handles, orchestration, launches.
+//
+// Host flow of one search (replaces scheduler.hpp:188-244):
+//   validate -> upload query + matrix -> build_profile_kernel -> intra-task kernel (long pool)
+//   -> inter-task int16 kernel (short pool) -> int32 re-run of flagged lanes -> key build ->
+//   top-k select -> download k hits.
+// Everything runs on one stream per handle; no host synchronisation happens between the upload and
+// the final download.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/swb200.h"
+#include "kernels.cuh"
+#include "pack.hpp"
+#include "pipe_rates.cuh"
+
+using namespace swb;
+
+namespace {
+
+thread_local std::string g_error;
+
+swb_status fail(swb_status st, const std::string& msg) {
+    g_error = msg;
+    return st;
+}
+
+#define SWB_CUDA(expr)                                                                           \
+    do {                                                                                         \
+        cudaError_t e__ = (expr);                                                                \
+        if (e__ != cudaSuccess)                                                                  \
+            return fail(SWB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__));      \
+    } while (0)
+
+template <class T>
+swb_status dev_alloc(T** ptr, size_t count, uint64_t* tally) {
+    *ptr = nullptr;
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    SWB_CUDA(cudaMalloc(reinterpret_cast<void**>(ptr), bytes));
+    if (tally) *tally += bytes;
+    return SWB_OK;
+}
+
+inline uint32_t pack16(int32_t v) {
+    const uint32_t h = static_cast<uint32_t>(v) & 0xffffu;
+    return h | (h << 16);
+}
+
+enum { EV_START = 0, EV_UP, EV_INTRA, EV_INTER, EV_RESCORE, EV_TOPK, EV_END, EV_COUNT };
+
+struct QueryPlan {
+    bool wide = false;        // int32 everywhere (matrix + open outside int8, or huge gaps)
+    bool may_overflow = true; // a score above `limit` is possible at all
+    int32_t limit = 0;
+    int32_t open = 0, ext = 0;
+    uint32_t m = 0;
+    uint32_t pstride = 0;       // inter profile row stride
+    uint32_t intra_t = 8, n_lane_tiles = 0, intra_w = 1, intra_passes = 0;
+};
+
+}  // namespace
+
+struct swb_db {
+    int device = 0;
+    cudaStream_t own_stream = nullptr, stream = nullptr;
+    int sm_count = 0;
+    size_t smem_optin = 0;
+    std::mutex mu;
+    uint64_t device_bytes = 0;
+
+    // database (metadata stays on the host, bulk arrays live on the device only)
+    PackedDb meta;
+    uint32_t n_slots = 0;
+    uint32_t max_short_rows = 0;
+    uint64_t long_rows = 0;     // bytes of the long pool == border rows
+    uint8_t* d_short_codes = nullptr;
+    GroupDesc* d_groups = nullptr;
+    uint32_t* d_slot_index = nullptr;
+    uint32_t* d_slot_len = nullptr;
+    uint8_t* d_long_codes = nullptr;
+    LongDesc* d_longs = nullptr;
+
+    // work buffers
+    uint2 *d_border0 = nullptr, *d_border1 = nullptr;      // inter int16, database-shaped
+    uint2 *d_lborder0 = nullptr, *d_lborder1 = nullptr;    // intra, long-pool-shaped
+    uint2 *d_wborder0 = nullptr, *d_wborder1 = nullptr;    // int32 re-run, [rows][threads]
+    uint32_t wide_threads = 0;
+    int32_t* d_slot_scores = nullptr;
+    int32_t* d_long_scores = nullptr;
+    uint32_t* d_flag_list = nullptr;
+    uint32_t* d_counters = nullptr;   // [0] work counter, [1] flag count
+    uint64_t* d_keys = nullptr;
+    uint64_t* d_sel[2] = {nullptr, nullptr};
+    size_t sel_cap = 0;
+    uint64_t* d_sort = nullptr;
+    size_t sort_cap = 0;
+    int32_t* d_all_scores = nullptr;
+
+    // query side
+    uint32_t query_cap = 0;
+    uint8_t* d_query = nullptr;
+    int32_t* d_matrix = nullptr;
+    int8_t *d_prof8 = nullptr, *d_prof8i = nullptr;
+    int32_t *d_prof32 = nullptr, *d_prof32i = nullptr;
+    size_t prof8_cap = 0, prof8i_cap = 0, prof32_cap = 0, prof32i_cap = 0;
+
+    uint8_t* h_stage = nullptr;   // pinned: query + matrix up, keys down
+    size_t stage_cap = 0;
+    uint32_t* h_counters = nullptr;   // pinned copy of d_counters
+    cudaEvent_t ev[EV_COUNT] = {};
+    uint32_t launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+swb_status ensure_stage(swb_db* db, size_t bytes) {
+    if (bytes <= db->stage_cap) return SWB_OK;
+    if (db->h_stage) cudaFreeHost(db->h_stage);
+    db->h_stage = nullptr;
+    db->stage_cap = 0;
+    const size_t cap = std::max<size_t>(bytes * 2, 1 << 16);
+    SWB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&db->h_stage), cap));
+    db->stage_cap = cap;
+    return SWB_OK;
+}
+
+template <class T>
+swb_status ensure_dev(T** ptr, size_t* cap, size_t need, uint64_t* tally) {
+    if (need <= *cap) return SWB_OK;
+    if (*ptr) {
+        cudaFree(*ptr);
+        *tally -= *cap * sizeof(T);
+    }
+    *ptr = nullptr;
+    *cap = 0;
+    const size_t want = need + need / 4 + 256;
+    swb_status st = dev_alloc(ptr, want, tally);
+    if (st != SWB_OK) return st;
+    *cap = want;
+    return SWB_OK;
+}
+
+swb_status check_scoring_args(const uint8_t* query, uint32_t m, const int32_t* matrix, int32_t open,
+                              int32_t ext) {
+    if (!matrix) return fail(SWB_ERR_INVALID, "matrix is null");
+    if (m && !query) return fail(SWB_ERR_INVALID, "query is null");
+    // GapModel's invariant and message (scoring.hpp:50-53)
+    if (ext < 0 || open < ext) return fail(SWB_ERR_INVALID, "gap model requires open >= extend >= 0");
+    // QueryProfile's check and message (scoring.hpp:203-205)
+    for (uint32_t j = 0; j < m; ++j)
+        if (query[j] >= kAlphabet) return fail(SWB_ERR_RANGE, "query code outside matrix alphabet");
+    int32_t lo = matrix[0], hi = matrix[0];
+    for (int i = 1; i < 576; ++i) lo = std::min(lo, matrix[i]), hi = std::max(hi, matrix[i]);
+    if (lo < -(1 << 20) || hi > (1 << 20) || open > (1 << 28))
+        return fail(SWB_ERR_UNSUPPORTED, "matrix entries beyond +-2^20 or gap open beyond 2^28");
+    return SWB_OK;
+}
+
+QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext) {
+    QueryPlan pl;
+    pl.m = m;
+    pl.open = open;
+    pl.ext = ext;
+    int32_t lo = matrix[0], hi = matrix[0];
+    for (int i = 1; i < 576; ++i) lo = std::min(lo, matrix[i]), hi = std::max(hi, matrix[i]);
+    const bool fits8 = (lo + open >= -128) && (hi + open <= 127) && (open <= 127);
+    pl.wide = !fits8;
+    const int32_t top = std::max(hi, 0);
+    pl.limit = 32767 - top;
+    const uint64_t reach = static_cast<uint64_t>(top) * std::min<uint64_t>(m, db->max_short_rows);
+    pl.may_overflow = reach > static_cast<uint64_t>(pl.limit);
+
+    // inter profile stride: columns padded to the 32-column tile, then to 16 (mod 128) bytes
+    const uint32_t mpad = std::max<uint32_t>(32, (m + 31) / 32 * 32);
+    pl.pstride = mpad + ((16 + 128 - (mpad % 128)) % 128);
+
+    // intra-task geometry: T columns per lane (4..8), W warps per CTA, passes
+    uint64_t best_cols = ~0ull;
+    for (uint32_t t = 4; t <= 8; ++t) {
+        const uint32_t tiles = (std::max<uint32_t>(m, 1) + t - 1) / t;
+        const uint32_t w = std::min<uint32_t>(kIntraMaxWarps, (tiles + 31) / 32);
+        const uint32_t passes = (tiles + 32 * w - 1) / (32 * w);
+        const uint64_t cols = static_cast<uint64_t>(passes) * w * 32 * t;
+        if (cols <= best_cols) {
+            best_cols = cols;
+            pl.intra_t = t;
+            pl.n_lane_tiles = tiles;
+            pl.intra_w = w;
+            pl.intra_passes = passes;
+        }
+    }
+    return pl;
+}
+
+template <int T, typename PT>
+void launch_intra(const IntraParams& ip, uint32_t warps, cudaStream_t s) {
+    intra_s32_kernel<T, PT><<<ip.n_long, warps * 32, 0, s>>>(ip);
+}
+
+template <typename PT>
+void launch_intra_t(uint32_t t, const IntraParams& ip, uint32_t warps, cudaStream_t s) {
+    switch (t) {
+        case 4: launch_intra<4, PT>(ip, warps, s); break;
+        case 5: launch_intra<5, PT>(ip, warps, s); break;
+        case 6: launch_intra<6, PT>(ip, warps, s); break;
+        case 7: launch_intra<7, PT>(ip, warps, s); break;
+        default: launch_intra<8, PT>(ip, warps, s); break;
+    }
+}
+
+// Scores every local sequence; results land in d_slot_scores / d_long_scores.  Asynchronous.
+swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_t* matrix, int32_t open,
+                      int32_t ext, swb_stats* stats) {
+    cudaStream_t s = db->stream;
+    const QueryPlan pl = make_plan(db, m, matrix, open, ext);
+    db->launches = 0;
+    SWB_CUDA(cudaEventRecord(db->ev[EV_START], s));
+
+    if (m == 0 || db->meta.n_local == 0) {
+        // empty query: every score is 0 (align.hpp:45,100,172)
+        SWB_CUDA(cudaMemsetAsync(db->d_slot_scores, 0, std::max<size_t>(db->n_slots, 1) * sizeof(int32_t), s));
+        SWB_CUDA(cudaMemsetAsync(db->d_long_scores, 0, std::max<size_t>(db->meta.n_long, 1) * sizeof(int32_t), s));
+        for (int e = EV_UP; e <= EV_RESCORE; ++e) SWB_CUDA(cudaEventRecord(db->ev[e], s));
+        return SWB_OK;
+    }
+
+    // ---- upload query + matrix, build profiles -------------------------------------------------
+    swb_status st = ensure_stage(db, m + 576 * sizeof(int32_t) + 64);
+    if (st != SWB_OK) return st;
+    if (m > db->query_cap) {
+        if (db->d_query) cudaFree(db->d_query);
+        db->d_query = nullptr;
+        st = dev_alloc(&db->d_query, static_cast<size_t>(m) * 2, &db->device_bytes);
+        if (st != SWB_OK) return st;
+        db->query_cap = m * 2;
+    }
+    std::memcpy(db->h_stage, matrix, 576 * sizeof(int32_t));
+    std::memcpy(db->h_stage + 576 * sizeof(int32_t), query, m);
+    SWB_CUDA(cudaMemcpyAsync(db->d_matrix, db->h_stage, 576 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_query, db->h_stage + 576 * sizeof(int32_t), m, cudaMemcpyHostToDevice, s));
+
+    const size_t prof_elems = static_cast<size_t>(kProfRows) * pl.pstride;
+    const size_t profi_elems = static_cast<size_t>(kProfRows) * pl.n_lane_tiles * 8;
+    ProfileParams pp{};
+    pp.query = db->d_query;
+    pp.matrix = db->d_matrix;
+    pp.m = m;
+    pp.open = open;
+    pp.pstride = pl.pstride;
+    pp.intra_t = pl.intra_t;
+    pp.n_lane_tiles = pl.n_lane_tiles;
+    if (!pl.wide) {
+        if ((st = ensure_dev(&db->d_prof8, &db->prof8_cap, prof_elems, &db->device_bytes)) != SWB_OK) return st;
+        if ((st = ensure_dev(&db->d_prof8i, &db->prof8i_cap, profi_elems, &db->device_bytes)) != SWB_OK) return st;
+        pp.prof8 = db->d_prof8;
+        pp.prof8i = db->d_prof8i;
+    } else {
+        if ((st = ensure_dev(&db->d_prof32, &db->prof32_cap, prof_elems, &db->device_bytes)) != SWB_OK) return st;
+        if ((st = ensure_dev(&db->d_prof32i, &db->prof32i_cap, profi_elems, &db->device_bytes)) != SWB_OK) return st;
+        pp.prof32 = db->d_prof32;
+        pp.prof32i = db->d_prof32i;
+    }
+    build_profile_kernel<<<64, 256, 0, s>>>(pp);
+    ++db->launches;
+    SWB_CUDA(cudaMemsetAsync(db->d_counters, 0, 4 * sizeof(uint32_t), s));
+    SWB_CUDA(cudaEventRecord(db->ev[EV_UP], s));
+
+    // ---- long pool: intra-task kernel ------------------------------------------------------------
+    if (db->meta.n_long) {
+        IntraParams ip{};
+        ip.codes = db->d_long_codes;
+        ip.longs = db->d_longs;
+        ip.n_long = db->meta.n_long;
+        ip.profi = pl.wide ? static_cast<const void*>(db->d_prof32i) : static_cast<const void*>(db->d_prof8i);
+        ip.n_lane_tiles = pl.n_lane_tiles;
+        ip.n_passes = pl.intra_passes;
+        ip.border0 = db->d_lborder0;
+        ip.border1 = db->d_lborder1;
+        ip.long_scores = db->d_long_scores;
+        ip.open = open;
+        ip.ext = ext;
+        if (pl.wide) launch_intra_t<int32_t>(pl.intra_t, ip, pl.intra_w, s);
+        else launch_intra_t<int8_t>(pl.intra_t, ip, pl.intra_w, s);
+        ++db->launches;
+    }
+    SWB_CUDA(cudaEventRecord(db->ev[EV_INTRA], s));
+
+    // ---- short pool: inter-task kernels ------------------------------------------------------------
+    const uint32_t n_groups = static_cast<uint32_t>(db->meta.groups.size());
+    bool need_wide_pass = false;
+    if (n_groups && !pl.wide) {
+        InterParams ip{};
+        ip.codes = reinterpret_cast<const uint4*>(db->d_short_codes);
+        ip.groups = db->d_groups;
+        ip.n_groups = n_groups;
+        ip.prof8 = db->d_prof8;
+        ip.pstride = pl.pstride;
+        ip.n_tiles = (m + kInterTile - 1) / kInterTile;
+        ip.border0 = db->d_border0;
+        ip.border1 = db->d_border1;
+        ip.slot_scores = db->d_slot_scores;
+        ip.flag_list = db->d_flag_list;
+        ip.flag_count = db->d_counters + 1;
+        ip.work_counter = db->d_counters;
+        ip.neg_open2 = pack16(-open);
+        ip.neg_ext2 = pack16(-ext);
+        ip.limit = pl.limit;
+        const size_t smem = prof_elems;
+        const uint32_t warps_per_cta = kInterThreads / 32;
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(db->sm_count, (n_groups + warps_per_cta - 1) / warps_per_cta));
+        if (smem <= db->smem_optin) {
+            SWB_CUDA(cudaFuncSetAttribute(inter_s16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+            inter_s16_kernel<true><<<grid, kInterThreads, smem, s>>>(ip);
+        } else {
+            inter_s16_kernel<false><<<grid, kInterThreads, 0, s>>>(ip);
+        }
+        ++db->launches;
+        need_wide_pass = pl.may_overflow;
+    }
+    SWB_CUDA(cudaEventRecord(db->ev[EV_INTER], s));
+
+    if (n_groups && (pl.wide || need_wide_pass)) {
+        if (!db->d_wborder0) {
+            const uint64_t rows = std::max<uint32_t>(db->max_short_rows, 1);
+            uint64_t threads = (256ull << 20) / (rows * 16);
+            threads = std::min<uint64_t>(8192, std::max<uint64_t>(128, threads / 128 * 128));
+            db->wide_threads = static_cast<uint32_t>(threads);
+            if ((st = dev_alloc(&db->d_wborder0, rows * threads, &db->device_bytes)) != SWB_OK) return st;
+            if ((st = dev_alloc(&db->d_wborder1, rows * threads, &db->device_bytes)) != SWB_OK) return st;
+        }
+        WideParams wp{};
+        wp.codes = db->d_short_codes;
+        wp.groups = db->d_groups;
+        wp.slot_len = db->d_slot_len;
+        wp.list = pl.wide ? nullptr : db->d_flag_list;
+        wp.list_count = db->d_counters + 1;
+        wp.n_slots = db->n_slots;
+        wp.prof = pl.wide ? static_cast<const void*>(db->d_prof32) : static_cast<const void*>(db->d_prof8);
+        wp.pstride = pl.pstride;
+        wp.n_tiles = (m + kWideTile - 1) / kWideTile;
+        wp.border0 = db->d_wborder0;
+        wp.border1 = db->d_wborder1;
+        wp.slot_scores = db->d_slot_scores;
+        wp.open = open;
+        wp.ext = ext;
+        const uint32_t blocks = db->wide_threads / 128;
+        if (pl.wide) inter_s32_kernel<int32_t><<<blocks, 128, 0, s>>>(wp);
+        else inter_s32_kernel<int8_t><<<blocks, 128, 0, s>>>(wp);
+        ++db->launches;
+    }
+    SWB_CUDA(cudaEventRecord(db->ev[EV_RESCORE], s));
+    SWB_CUDA(cudaGetLastError());
+    (void)stats;
+    return SWB_OK;
+}
+
+// Descending top-k of n device keys; result pointer (k entries, zero padded) in *out.
+swb_status select_topk(swb_db* db, const uint64_t* d_in, uint64_t n, uint32_t k, const uint64_t** out) {
+    cudaStream_t s = db->stream;
+    swb_status st;
+    if (k <= kSelectMaxK) {
+        const uint64_t first_blocks = std::max<uint64_t>(1, (n + kSelectSlice - 1) / kSelectSlice);
+        const size_t need = static_cast<size_t>(first_blocks) * k;
+        if (need > db->sel_cap) {
+            for (auto& p : db->d_sel) {
+                if (p) cudaFree(p);
+                p = nullptr;
+            }
+            for (auto& p : db->d_sel)
+                if ((st = dev_alloc(&p, need, &db->device_bytes)) != SWB_OK) return st;
+            db->sel_cap = need;
+        }
+        const uint64_t* in = d_in;
+        int which = 0;
+        for (;;) {
+            const uint64_t blocks = std::max<uint64_t>(1, (n + kSelectSlice - 1) / kSelectSlice);
+            select_topk_kernel<<<static_cast<unsigned>(blocks), kSelectThreads, 0, s>>>(in, n, k, db->d_sel[which]);
+            ++db->launches;
+            in = db->d_sel[which];
+            n = blocks * k;
+            which ^= 1;
+            if (blocks == 1) break;
+        }
+        *out = in;
+        return SWB_OK;
+    }
+    // k > 1024: full bitonic sort of the zero-padded key array
+    uint64_t pow2 = 2;
+    while (pow2 < n) pow2 <<= 1;
+    if (pow2 > db->sort_cap) {
+        if (db->d_sort) cudaFree(db->d_sort);
+        db->d_sort = nullptr;
+        if ((st = dev_alloc(&db->d_sort, pow2, &db->device_bytes)) != SWB_OK) return st;
+        db->sort_cap = pow2;
+    }
+    SWB_CUDA(cudaMemsetAsync(db->d_sort, 0, pow2 * sizeof(uint64_t), s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_sort, d_in, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(4096, std::max<uint64_t>(1, pow2 / 2 / 256)));
+    for (uint64_t size = 2; size <= pow2; size <<= 1)
+        for (uint64_t stride = size >> 1; stride > 0; stride >>= 1) {
+            bitonic_step_kernel<<<grid, 256, 0, s>>>(db->d_sort, pow2, size, stride);
+            ++db->launches;
+        }
+    *out = db->d_sort;
+    return SWB_OK;
+}
+
+void fill_stats(swb_db* db, uint32_t m, swb_stats* st) {
+    if (!st) return;
+    std::memset(st, 0, sizeof(*st));
+    st->lane_scored = db->meta.n_short;
+    st->wavefront_scored = db->meta.n_long;
+    st->chunks_claimed = db->meta.groups.size() + db->meta.n_long;
+    st->cells = static_cast<uint64_t>(m) * db->meta.residues;
+    const uint64_t mpad = (static_cast<uint64_t>(m) + kInterTile - 1) / kInterTile * kInterTile;
+    st->padded_cells = mpad * db->meta.padded_rows * kGroupSeqs + static_cast<uint64_t>(m) * (db->meta.residues - db->meta.short_residues);
+    st->kernel_launches = db->launches;
+    st->rescored_i32 = db->h_counters ? db->h_counters[1] : 0;
+    auto span = [&](int a, int b) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, db->ev[a], db->ev[b]);
+        return ms;
+    };
+    st->ms_h2d_d2h = span(EV_START, EV_UP);
+    st->ms_intra = span(EV_UP, EV_INTRA);
+    st->ms_inter = span(EV_INTRA, EV_INTER);
+    st->ms_rescore = span(EV_INTER, EV_RESCORE);
+    st->ms_topk = span(EV_RESCORE, EV_TOPK);
+    st->ms_total = span(EV_START, EV_END);
+}
+
+swb_status upload_db(swb_db* db) {
+    PackedDb& m = db->meta;
+    db->n_slots = static_cast<uint32_t>(m.groups.size() * kGroupSeqs);
+    db->max_short_rows = m.groups.empty() ? 0 : m.groups[0].n_chunks * kRowsPerChunk;
+    db->long_rows = m.long_codes.size();
+    uint64_t* tally = &db->device_bytes;
+    swb_status st;
+#define ALLOC_COPY(dptr, vec)                                                                        \
+    if ((st = dev_alloc(&(dptr), (vec).size(), tally)) != SWB_OK) return st;                         \
+    if (!(vec).empty())                                                                              \
+        SWB_CUDA(cudaMemcpy((dptr), (vec).data(), (vec).size() * sizeof((vec)[0]), cudaMemcpyHostToDevice));
+    ALLOC_COPY(db->d_short_codes, m.short_codes);
+    ALLOC_COPY(db->d_groups, m.groups);
+    ALLOC_COPY(db->d_slot_index, m.short_index);
+    ALLOC_COPY(db->d_slot_len, m.short_len);
+    ALLOC_COPY(db->d_long_codes, m.long_codes);
+    ALLOC_COPY(db->d_longs, m.longs);
+#undef ALLOC_COPY
+    const size_t brows = static_cast<size_t>(m.total_chunks) * kRowsPerChunk * 32 + 64;
+    if ((st = dev_alloc(&db->d_border0, brows, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_border1, brows, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_lborder0, db->long_rows + 16, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_lborder1, db->long_rows + 16, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_slot_scores, db->n_slots, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_long_scores, m.n_long, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_flag_list, db->n_slots, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_counters, 4, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_keys, static_cast<size_t>(db->n_slots) + m.n_long, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_matrix, 576, tally)) != SWB_OK) return st;
+    SWB_CUDA(cudaMemset(db->d_slot_scores, 0, std::max<size_t>(db->n_slots, 1) * sizeof(int32_t)));
+    // the bulk host copies are no longer needed
+    std::vector<uint8_t>().swap(m.short_codes);
+    std::vector<uint8_t>().swap(m.long_codes);
+    return SWB_OK;
+}
+
+swb_status create_from(const SeqSource& src, uint64_t threshold, int32_t device, uint32_t rank,
+                       uint32_t count, swb_db** out) {
+    if (!out) return fail(SWB_ERR_INVALID, "out is null");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(SWB_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(SWB_ERR_INVALID, "device index out of range");
+    auto* db = new swb_db();
+    db->device = device;
+    bool bad = false;
+    const std::string err = pack_database(src, threshold, rank, count, db->meta, &bad);
+    if (!err.empty()) {
+        delete db;
+        return fail(bad ? SWB_ERR_RANGE : SWB_ERR_INVALID, err);
+    }
+    DeviceGuard guard(device);
+    cudaDeviceProp prop{};
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) {
+        delete db;
+        return fail(SWB_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (prop.major < 10) {
+        delete db;
+        return fail(SWB_ERR_CUDA, "device is not sm_100-class; this library is built for sm_100a only");
+    }
+    db->sm_count = prop.multiProcessorCount;
+    db->smem_optin = prop.sharedMemPerBlockOptin;
+    swb_status st = SWB_OK;
+    do {
+        if (cudaStreamCreateWithFlags(&db->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+            st = fail(SWB_ERR_CUDA, "cudaStreamCreate failed");
+            break;
+        }
+        db->stream = db->own_stream;
+        for (auto& ev : db->ev)
+            if (cudaEventCreate(&ev) != cudaSuccess) st = fail(SWB_ERR_CUDA, "cudaEventCreate failed");
+        if (st != SWB_OK) break;
+        if (cudaMallocHost(reinterpret_cast<void**>(&db->h_counters), 4 * sizeof(uint32_t)) != cudaSuccess) {
+            st = fail(SWB_ERR_CUDA, "cudaMallocHost failed");
+            break;
+        }
+        std::memset(db->h_counters, 0, 4 * sizeof(uint32_t));
+        st = upload_db(db);
+    } while (false);
+    if (st != SWB_OK) {
+        const std::string keep = g_error;
+        swb_db_destroy(db);
+        g_error = keep;
+        return st;
+    }
+    *out = db;
+    return SWB_OK;
+}
+
+swb_status search_keys_locked(swb_db* db, const uint8_t* query, uint32_t m, const int32_t* matrix,
+                              int32_t open, int32_t ext, uint32_t top_k, const uint64_t** d_out,
+                              swb_stats* stats) {
+    swb_status st = score_core(db, query, m, matrix, open, ext, stats);
+    if (st != SWB_OK) return st;
+    cudaStream_t s = db->stream;
+    const uint32_t n_keys = db->n_slots + db->meta.n_long;
+    if (n_keys) {
+        build_keys_kernel<<<std::max(1u, std::min(1024u, (n_keys + 255) / 256)), 256, 0, s>>>(
+            db->d_slot_scores, db->d_slot_index, db->n_slots, db->d_long_scores, db->d_longs, db->meta.n_long,
+            db->d_keys);
+        ++db->launches;
+    }
+    st = select_topk(db, db->d_keys, n_keys, top_k, d_out);
+    if (st != SWB_OK) return st;
+    SWB_CUDA(cudaEventRecord(db->ev[EV_TOPK], s));
+    return SWB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* swb_last_error(void) { return g_error.c_str(); }
+const char* swb_version(void) { return "swb200 0.1 (sm_100a)"; }
+
+swb_status swb_device_count(int32_t* count) {
+    if (!count) return fail(SWB_ERR_INVALID, "count is null");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        *count = 0;
+        return fail(SWB_ERR_CUDA, "cudaGetDeviceCount failed");
+    }
+    *count = n;
+    return SWB_OK;
+}
+
+swb_status swb_db_create(const uint8_t* const* seqs, const uint32_t* lens, uint32_t n, uint64_t length_threshold,
+                         int32_t device, uint32_t shard_rank, uint32_t shard_count, swb_db** out) {
+    if (n && (!seqs || !lens)) return fail(SWB_ERR_INVALID, "seqs/lens are null");
+    SeqSource src;
+    static const uint8_t* const kNoPtrs[1] = {nullptr};
+    static const uint32_t kNoLens[1] = {0};
+    src.ptrs = n ? seqs : kNoPtrs;
+    src.lens = n ? lens : kNoLens;
+    src.n = n;
+    return create_from(src, length_threshold, device, shard_rank, shard_count, out);
+}
+
+swb_status swb_db_create_flat(const uint8_t* codes, const uint64_t* offsets, uint32_t n, uint64_t length_threshold,
+                              int32_t device, uint32_t shard_rank, uint32_t shard_count, swb_db** out) {
+    if (!offsets) return fail(SWB_ERR_INVALID, "offsets is null");
+    if (n && offsets[n] && !codes) return fail(SWB_ERR_INVALID, "codes is null");
+    for (uint32_t i = 0; i < n; ++i)
+        if (offsets[i + 1] < offsets[i]) return fail(SWB_ERR_INVALID, "offsets must be non-decreasing");
+    SeqSource src;
+    src.flat = codes;
+    src.offsets = offsets;
+    src.n = n;
+    return create_from(src, length_threshold, device, shard_rank, shard_count, out);
+}
+
+void swb_db_destroy(swb_db* db) {
+    if (!db) return;
+    {
+        DeviceGuard guard(db->device);
+        if (db->own_stream) cudaStreamSynchronize(db->own_stream);
+        void* ptrs[] = {db->d_short_codes, db->d_groups,      db->d_slot_index, db->d_slot_len,  db->d_long_codes,
+                        db->d_longs,       db->d_border0,     db->d_border1,    db->d_lborder0,  db->d_lborder1,
+                        db->d_wborder0,    db->d_wborder1,    db->d_slot_scores, db->d_long_scores, db->d_flag_list,
+                        db->d_counters,    db->d_keys,        db->d_sel[0],     db->d_sel[1],    db->d_sort,
+                        db->d_all_scores,  db->d_query,       db->d_matrix,     db->d_prof8,     db->d_prof8i,
+                        db->d_prof32,      db->d_prof32i};
+        for (void* p : ptrs)
+            if (p) cudaFree(p);
+        if (db->h_stage) cudaFreeHost(db->h_stage);
+        if (db->h_counters) cudaFreeHost(db->h_counters);
+        for (auto& ev : db->ev)
+            if (ev) cudaEventDestroy(ev);
+        if (db->own_stream) cudaStreamDestroy(db->own_stream);
+    }
+    delete db;
+}
+
+swb_status swb_db_info_get(const swb_db* db, swb_db_info* info) {
+    if (!db || !info) return fail(SWB_ERR_INVALID, "null argument");
+    std::memset(info, 0, sizeof(*info));
+    info->n_total = db->meta.n_total;
+    info->n_local = db->meta.n_local;
+    info->n_short = db->meta.n_short;
+    info->n_long = db->meta.n_long;
+    info->n_groups = static_cast<uint32_t>(db->meta.groups.size());
+    info->max_length = db->meta.max_length;
+    info->shard_rank = db->meta.shard_rank;
+    info->shard_count = db->meta.shard_count;
+    info->residues = db->meta.residues;
+    info->padded_residues = db->meta.padded_rows * kGroupSeqs + db->long_rows;
+    info->device_bytes = db->device_bytes;
+    info->length_threshold = db->meta.length_threshold;
+    info->device = db->device;
+    return SWB_OK;
+}
+
+swb_status swb_db_set_stream(swb_db* db, void* cuda_stream) {
+    if (!db) return fail(SWB_ERR_INVALID, "db is null");
+    std::lock_guard<std::mutex> lock(db->mu);
+    db->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : db->own_stream;
+    return SWB_OK;
+}
+
+swb_status swb_search_keys(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
+                           int32_t gap_open, int32_t gap_extend, uint32_t top_k, uint64_t* host_keys,
+                           void** device_keys, swb_stats* stats) {
+    if (!db) return fail(SWB_ERR_INVALID, "db is null");
+    // SearchConfig::validate's message (scheduler.hpp:34)
+    if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
+    swb_status st = check_scoring_args(query, query_len, matrix, gap_open, gap_extend);
+    if (st != SWB_OK) return st;
+    std::lock_guard<std::mutex> lock(db->mu);
+    DeviceGuard guard(db->device);
+    // never select more than the shard holds (plus zero padding up to top_k on the host side)
+    const uint64_t n_keys = static_cast<uint64_t>(db->n_slots) + db->meta.n_long;
+    const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint64_t>(n_keys, 1)));
+    const uint64_t* d_top = nullptr;
+    st = search_keys_locked(db, query, query_len, matrix, gap_open, gap_extend, k_eff, &d_top, stats);
+    if (st != SWB_OK) return st;
+    cudaStream_t s = db->stream;
+    if (host_keys) {
+        st = ensure_stage(db, static_cast<size_t>(k_eff) * sizeof(uint64_t));
+        if (st != SWB_OK) return st;
+        SWB_CUDA(cudaMemcpyAsync(db->h_stage, d_top, static_cast<size_t>(k_eff) * sizeof(uint64_t),
+                                 cudaMemcpyDeviceToHost, s));
+    }
+    SWB_CUDA(cudaMemcpyAsync(db->h_counters, db->d_counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SWB_CUDA(cudaEventRecord(db->ev[EV_END], s));
+    SWB_CUDA(cudaStreamSynchronize(s));
+    if (host_keys) {
+        std::memcpy(host_keys, db->h_stage, static_cast<size_t>(k_eff) * sizeof(uint64_t));
+        for (uint32_t i = k_eff; i < top_k; ++i) host_keys[i] = 0;
+    }
+    if (device_keys) *device_keys = (k_eff == top_k) ? const_cast<uint64_t*>(d_top) : nullptr;
+    fill_stats(db, query_len, stats);
+    return SWB_OK;
+}
+
+swb_status swb_search(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix, int32_t gap_open,
+                      int32_t gap_extend, uint32_t top_k, swb_hit* hits, uint32_t* n_hits, swb_stats* stats) {
+    if (!hits || !n_hits) return fail(SWB_ERR_INVALID, "hits/n_hits are null");
+    if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
+    if (!db) return fail(SWB_ERR_INVALID, "db is null");
+    const uint64_t n_keys = static_cast<uint64_t>(db->n_slots) + db->meta.n_long;
+    const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint64_t>(n_keys, 1)));
+    std::vector<uint64_t> keys(k_eff);
+    swb_status st = swb_search_keys(db, query, query_len, matrix, gap_open, gap_extend, k_eff, keys.data(), nullptr, stats);
+    if (st != SWB_OK) return st;
+    uint32_t cnt = 0;
+    for (uint32_t i = 0; i < k_eff; ++i) {
+        if (!keys[i]) break;
+        hits[cnt].db_index = 0xFFFFFFFFu - static_cast<uint32_t>(keys[i] & 0xFFFFFFFFu);
+        hits[cnt].score = static_cast<int32_t>(keys[i] >> 32);
+        ++cnt;
+    }
+    *n_hits = cnt;
+    return SWB_OK;
+}
+
+swb_status swb_score_all(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix, int32_t gap_open,
+                         int32_t gap_extend, int32_t* scores, swb_stats* stats) {
+    if (!db || !scores) return fail(SWB_ERR_INVALID, "null argument");
+    swb_status st = check_scoring_args(query, query_len, matrix, gap_open, gap_extend);
+    if (st != SWB_OK) return st;
+    std::lock_guard<std::mutex> lock(db->mu);
+    DeviceGuard guard(db->device);
+    st = score_core(db, query, query_len, matrix, gap_open, gap_extend, stats);
+    if (st != SWB_OK) return st;
+    cudaStream_t s = db->stream;
+    const uint32_t n_total = db->meta.n_total;
+    if (!db->d_all_scores)
+        if ((st = dev_alloc(&db->d_all_scores, n_total, &db->device_bytes)) != SWB_OK) return st;
+    // entries of other shards must stay untouched: stage the caller's values first
+    SWB_CUDA(cudaMemcpyAsync(db->d_all_scores, scores, static_cast<size_t>(n_total) * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, s));
+    const uint32_t total = db->n_slots + db->meta.n_long;
+    if (total) {
+        scatter_scores_kernel<<<std::max(1u, std::min(1024u, (total + 255) / 256)), 256, 0, s>>>(
+            db->d_slot_scores, db->d_slot_index, db->n_slots, db->d_long_scores, db->d_longs, db->meta.n_long,
+            db->d_all_scores);
+        ++db->launches;
+    }
+    SWB_CUDA(cudaEventRecord(db->ev[EV_TOPK], s));
+    SWB_CUDA(cudaMemcpyAsync(scores, db->d_all_scores, static_cast<size_t>(n_total) * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, s));
+    SWB_CUDA(cudaMemcpyAsync(db->h_counters, db->d_counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SWB_CUDA(cudaEventRecord(db->ev[EV_END], s));
+    SWB_CUDA(cudaStreamSynchronize(s));
+    fill_stats(db, query_len, stats);
+    return SWB_OK;
+}
+
+swb_status swb_merge_keys(const uint64_t* keys, uint64_t n, int32_t keys_on_device, int32_t device, uint32_t top_k,
+                          swb_hit* hits, uint32_t* n_hits) {
+    if (!hits || !n_hits) return fail(SWB_ERR_INVALID, "hits/n_hits are null");
+    if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
+    if (n && !keys) return fail(SWB_ERR_INVALID, "keys is null");
+    *n_hits = 0;
+    if (n == 0) return SWB_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(SWB_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(SWB_ERR_INVALID, "device index out of range");
+    DeviceGuard guard(device);
+    // a scratch handle gives select_topk its buffers and stream
+    swb_db tmp;
+    tmp.device = device;
+    SWB_CUDA(cudaStreamCreateWithFlags(&tmp.own_stream, cudaStreamNonBlocking));
+    tmp.stream = tmp.own_stream;
+    uint64_t* d_in = nullptr;
+    swb_status st = SWB_OK;
+    std::vector<uint64_t> top;
+    const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, n));
+    do {
+        const uint64_t* src = keys;
+        if (!keys_on_device) {
+            if ((st = dev_alloc(&d_in, n, &tmp.device_bytes)) != SWB_OK) break;
+            if (cudaMemcpyAsync(d_in, keys, n * sizeof(uint64_t), cudaMemcpyHostToDevice, tmp.stream) != cudaSuccess) {
+                st = fail(SWB_ERR_CUDA, "cudaMemcpyAsync failed");
+                break;
+            }
+            src = d_in;
+        }
+        const uint64_t* d_top = nullptr;
+        if ((st = select_topk(&tmp, src, n, k_eff, &d_top)) != SWB_OK) break;
+        top.resize(k_eff);
+        if (cudaMemcpyAsync(top.data(), d_top, k_eff * sizeof(uint64_t), cudaMemcpyDeviceToHost, tmp.stream) != cudaSuccess ||
+            cudaStreamSynchronize(tmp.stream) != cudaSuccess) {
+            st = fail(SWB_ERR_CUDA, std::string("merge: ") + cudaGetErrorString(cudaGetLastError()));
+            break;
+        }
+    } while (false);
+    if (d_in) cudaFree(d_in);
+    for (auto& p : tmp.d_sel)
+        if (p) cudaFree(p);
+    if (tmp.d_sort) cudaFree(tmp.d_sort);
+    cudaStreamDestroy(tmp.own_stream);
+    tmp.own_stream = nullptr;
+    if (st != SWB_OK) return st;
+    uint32_t cnt = 0;
+    for (uint32_t i = 0; i < k_eff; ++i) {
+        if (!top[i]) break;
+        hits[cnt].db_index = 0xFFFFFFFFu - static_cast<uint32_t>(top[i] & 0xFFFFFFFFu);
+        hits[cnt].score = static_cast<int32_t>(top[i] >> 32);
+        ++cnt;
+    }
+    *n_hits = cnt;
+    return SWB_OK;
+}
+
+swb_status swb_score_batch(const uint8_t* query, uint32_t query_len, const uint8_t* const* subjects,
+                           const uint32_t* lens, uint32_t count, uint32_t lane_width, const int32_t* matrix,
+                           int32_t gap_open, int32_t gap_extend, int32_t device, int32_t* out) {
+    // align.hpp:93-95, same messages
+    if (lane_width < 1) return fail(SWB_ERR_INVALID, "lane_width must be >= 1");
+    if (count > lane_width) return fail(SWB_ERR_INVALID, "more subjects than lanes");
+    if (!out) return fail(SWB_ERR_INVALID, "out is null");
+    if (count && (!subjects || !lens)) return fail(SWB_ERR_INVALID, "subjects/lens are null");
+    swb_status st = check_scoring_args(query, query_len, matrix, gap_open, gap_extend);
+    if (st != SWB_OK) return st;
+    for (uint32_t l = 0; l < lane_width; ++l) out[l] = 0;
+    // Null lanes are padding (align.hpp:126,148): they are packed as empty sequences and their
+    // score (0) is simply not reported back.
+    std::vector<const uint8_t*> ptrs(count);
+    std::vector<uint32_t> ls(count);
+    for (uint32_t i = 0; i < count; ++i) {
+        ptrs[i] = subjects[i];
+        ls[i] = subjects[i] ? lens[i] : 0;
+    }
+    if (count == 0 || query_len == 0) return SWB_OK;
+    swb_db* db = nullptr;
+    // threshold = infinity: every lane goes through the inter-task kernel, whatever its length
+    st = swb_db_create(ptrs.data(), ls.data(), count, ~0ull, device, 0, 1, &db);
+    if (st != SWB_OK) return st;
+    std::vector<int32_t> scores(count, 0);
+    st = swb_score_all(db, query, query_len, matrix, gap_open, gap_extend, scores.data(), nullptr);
+    const std::string keep = g_error;
+    swb_db_destroy(db);
+    g_error = keep;
+    if (st != SWB_OK) return st;
+    for (uint32_t i = 0; i < count; ++i) out[i] = subjects[i] ? scores[i] : 0;
+    return SWB_OK;
+}
+
+swb_status swb_score_pair(const uint8_t* query, uint32_t query_len, const uint8_t* subject, uint32_t subject_len,
+                          const int32_t* matrix, int32_t gap_open, int32_t gap_extend, uint64_t chunk_width,
+                          int32_t device, int32_t* score) {
+    // align.hpp:169, same message
+    if (chunk_width < 1) return fail(SWB_ERR_INVALID, "chunk_width must be >= 1");
+    if (!score) return fail(SWB_ERR_INVALID, "score is null");
+    if (subject_len && !subject) return fail(SWB_ERR_INVALID, "subject is null");
+    swb_status st = check_scoring_args(query, query_len, matrix, gap_open, gap_extend);
+    if (st != SWB_OK) return st;
+    *score = 0;
+    if (query_len == 0 || subject_len == 0) return SWB_OK;
+    swb_db* db = nullptr;
+    const uint8_t* ptrs[1] = {subject};
+    const uint32_t ls[1] = {subject_len};
+    // threshold = 0: the sequence is routed to the intra-task kernel (scheduler.hpp:59-62)
+    st = swb_db_create(ptrs, ls, 1, 0, device, 0, 1, &db);
+    if (st != SWB_OK) return st;
+    int32_t out[1] = {0};
+    st = swb_score_all(db, query, query_len, matrix, gap_open, gap_extend, out, nullptr);
+    const std::string keep = g_error;
+    swb_db_destroy(db);
+    g_error = keep;
+    if (st != SWB_OK) return st;
+    *score = out[0];
+    return SWB_OK;
+}
+
+swb_status swb_shard_assignment(const uint32_t* lens, uint32_t n, uint64_t length_threshold, uint32_t shard_count,
+                                uint32_t* shard_of) {
+    if (n && (!lens || !shard_of)) return fail(SWB_ERR_INVALID, "null argument");
+    if (shard_count < 1) return fail(SWB_ERR_INVALID, "shard_count must be >= 1");
+    std::vector<const uint8_t*> ptrs(std::max<uint32_t>(n, 1), nullptr);
+    SeqSource src;
+    src.ptrs = ptrs.data();
+    src.lens = lens;
+    src.n = n;
+    std::vector<uint32_t> result;
+    shard_assignment(src, length_threshold, shard_count, result);
+    for (uint32_t i = 0; i < n; ++i) shard_of[i] = result[i];
+    return SWB_OK;
+}
+
+}  // extern "C"
+
+// ---- pipe-rate microbenchmark -------------------------------------------------------------------
+template <int OP>
+static swb_status run_pipe(int sm_count, double seconds, double* rate_ginst, double* clock_mhz) {
+    uint32_t* sink = nullptr;
+    unsigned long long* cyc = nullptr;
+    SWB_CUDA(cudaMalloc(&sink, 64));
+    SWB_CUDA(cudaMalloc(&cyc, sizeof(unsigned long long)));
+    cudaEvent_t a, b;
+    SWB_CUDA(cudaEventCreate(&a));
+    SWB_CUDA(cudaEventCreate(&b));
+    const int grid = sm_count * 2, block = 512;
+    int iters = 2000;
+    double ms = 0;
+    for (int attempt = 0; attempt < 6; ++attempt) {
+        SWB_CUDA(cudaMemset(cyc, 0, sizeof(unsigned long long)));
+        pipe_rate_kernel<OP><<<grid, block>>>(sink, cyc, 0xfffefffeu, 0x00030003u, iters);   // warm-up
+        SWB_CUDA(cudaMemset(cyc, 0, sizeof(unsigned long long)));
+        SWB_CUDA(cudaEventRecord(a));
+        pipe_rate_kernel<OP><<<grid, block>>>(sink, cyc, 0xfffefffeu, 0x00030003u, iters);
+        SWB_CUDA(cudaEventRecord(b));
+        SWB_CUDA(cudaEventSynchronize(b));
+        float fms = 0;
+        SWB_CUDA(cudaEventElapsedTime(&fms, a, b));
+        ms = fms;
+        if (ms >= seconds * 1000.0 * 0.5 || iters > (1 << 28)) break;
+        const double scale = std::min(64.0, std::max(2.0, seconds * 1000.0 / std::max(ms, 1e-3)));
+        iters = static_cast<int>(iters * scale);
+    }
+    unsigned long long cycles = 0;
+    SWB_CUDA(cudaMemcpy(&cycles, cyc, sizeof(cycles), cudaMemcpyDeviceToHost));
+    const double inst = static_cast<double>(grid) * block * static_cast<double>(iters) * kPipeChains * kPipeUnroll;
+    *rate_ginst = inst / (ms * 1e-3) / 1e9;
+    *clock_mhz = static_cast<double>(cycles) / (ms * 1e-3) / 1e6;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    cudaFree(cyc);
+    return SWB_OK;
+}
+
+extern "C" {
+
+swb_status swb_measure_pipe_rates(int32_t device, double seconds, swb_pipe_rates* out) {
+    if (!out) return fail(SWB_ERR_INVALID, "out is null");
+    std::memset(out, 0, sizeof(*out));
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(SWB_ERR_CUDA, "no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(SWB_ERR_INVALID, "device index out of range");
+    DeviceGuard guard(device);
+    cudaDeviceProp prop{};
+    SWB_CUDA(cudaGetDeviceProperties(&prop, device));
+    out->sm_count = prop.multiProcessorCount;
+    const double each = std::max(0.02, seconds / kOpCount);
+    double clk = 0, clk_sum = 0;
+    swb_status st;
+    if ((st = run_pipe<kOpViaddmnmx16>(prop.multiProcessorCount, each, &out->viaddmnmx_s16x2, &clk)) != SWB_OK) return st;
+    clk_sum += clk;
+    if ((st = run_pipe<kOpVimnmx3_16>(prop.multiProcessorCount, each, &out->vimnmx3_s16x2, &clk)) != SWB_OK) return st;
+    if ((st = run_pipe<kOpViadd16>(prop.multiProcessorCount, each, &out->viadd_16x2, &clk)) != SWB_OK) return st;
+    if ((st = run_pipe<kOpViaddmnmx32>(prop.multiProcessorCount, each, &out->viaddmnmx_s32, &clk)) != SWB_OK) return st;
+    if ((st = run_pipe<kOpPrmt>(prop.multiProcessorCount, each, &out->prmt, &clk)) != SWB_OK) return st;
+    if ((st = run_pipe<kOpImad>(prop.multiProcessorCount, each, &out->imad, &clk)) != SWB_OK) return st;
+    if ((st = run_pipe<kOpMixAluFma>(prop.multiProcessorCount, each, &out->mix_alu_fma, &clk)) != SWB_OK) return st;
+    out->sm_clock_mhz = clk_sum;
+    return SWB_OK;
+}
+
+}  // extern "C"
+
+#include "multi.inl"

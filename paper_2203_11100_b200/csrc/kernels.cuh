@@ -1,0 +1,547 @@
+// kernels.cuh -- hand-written sm_100a kernels of the SW#db scoring path.
+//
+// All kernels compute the recurrence of the reference's detail::local_score_rows
+// (align.hpp:42-64) in a shifted but algebraically identical form:
+//
+//   stored per cell:  Hm = H - open            (so both uses of "H - open" are free)
+//   profile entries:  sub' = M[s][q] + open    (so diag + sub = Hm_diag + sub')
+//   E (reference gap_h, along the query), F (reference gap_v, along the subject), and the
+//   boundaries H = 0, gap = -inf become Hm = -open, E = F = -open: the first real cell then gets
+//   max(0 - open, -open - extend) = -open, the value the reference's -inf sentinel yields
+//   (align.hpp:51-55).  Nothing can drop below -open - extend, so nothing wraps on the low side.
+//
+//   per cell:   E  = max(E - ext, Hm_left)            VIADDMNMX        (__viaddmax)
+//               F  = max(F - ext, Hm_up)              VIADDMNMX
+//               H  = max(0, Hm_diag + sub', E, F)     VIADDMNMX.RELU + VIMNMX.RELU
+//               Hm = H - open                         VIADD
+//               best = max(best, H)                   VIMNMX3 per two cells
+//
+// Padding (rows past a sequence's end, columns past the query's end, lanes with no sequence) uses
+// substitution score 0: every padded cell is bounded by an earlier real cell, so `best` is
+// unaffected, and a pad row applied to the initial state leaves it unchanged.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pack.hpp"
+
+namespace swb {
+
+constexpr int kProfRows = 25;        // 24 symbols + the pad row
+constexpr int kInterTile = 32;       // query columns held in registers per pass (inter-task)
+constexpr int kInterThreads = 512;   // persistent CTA: 16 warps, one per SMSP x4
+constexpr int kWideTile = 16;        // query columns per pass in the int32 re-run kernel
+constexpr int kIntraDelta = 64;      // step offset between neighbouring warps of an intra-task CTA
+constexpr int kIntraRing = 128;      // rows of border ring buffer between neighbouring warps
+constexpr int kIntraMaxWarps = 8;
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Query profile (scoring.hpp:199-215 restated for the device layouts).
+//   prof8  [25][pstride]            int8   sub' for the inter-task kernels, column-contiguous
+//   prof8i [25][n_lane_tiles][8]    int8   the same, re-tiled so that an intra-task lane's T<=8
+//                                          columns are one aligned 8-byte word
+//   prof32 / prof32i                int32  the wide variants (matrices that do not fit int8)
+// ------------------------------------------------------------------------------------------------
+struct ProfileParams {
+    const uint8_t* query;    // m codes
+    const int32_t* matrix;   // 24x24, [subject*24 + query]
+    uint32_t m;
+    int32_t open;
+    uint32_t pstride;        // bytes (int8) / elements (int32) per row of the column-contiguous form
+    uint32_t intra_t;        // columns per lane in the intra-task kernel (<= 8)
+    uint32_t n_lane_tiles;   // number of 8-slot words per row of the re-tiled form
+    int8_t* prof8;
+    int8_t* prof8i;
+    int32_t* prof32;
+    int32_t* prof32i;
+};
+
+__global__ void build_profile_kernel(ProfileParams p) {
+    const uint32_t per_row = p.pstride;
+    const uint32_t total = kProfRows * per_row;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t s = i / per_row, j = i % per_row;
+        int32_t v = p.open;  // pad row / pad column: substitution 0
+        if (s < kAlphabet && j < p.m) v = p.matrix[s * kAlphabet + p.query[j]] + p.open;
+        if (p.prof8) p.prof8[i] = static_cast<int8_t>(v);
+        if (p.prof32) p.prof32[i] = v;
+    }
+    const uint32_t per_row_i = p.n_lane_tiles * 8;
+    const uint32_t total_i = kProfRows * per_row_i;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total_i; i += gridDim.x * blockDim.x) {
+        const uint32_t s = i / per_row_i, rem = i % per_row_i;
+        const uint32_t tile = rem / 8, k = rem % 8;
+        const uint32_t j = tile * p.intra_t + k;
+        int32_t v = p.open;
+        if (s < kAlphabet && k < p.intra_t && j < p.m) v = p.matrix[s * kAlphabet + p.query[j]] + p.open;
+        if (p.prof8i) p.prof8i[i] = static_cast<int8_t>(v);
+        if (p.prof32i) p.prof32i[i] = v;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Inter-task kernel, packed int16 (the hot kernel).
+//
+// One warp owns one interleaved group of 64 sequences at a time (claimed from a global counter in
+// descending-length order); each thread carries two sequences in the two int16 halves of every
+// DPX word.  The query is swept in tiles of 32 columns held in registers (Hm, F per column);
+// between tiles the last column (Hm, E) of every row goes through a database-shaped border array
+// in HBM/L2 (8 bytes per row per thread, coalesced, double-buffered).  The int8 profile lives in
+// shared memory with a row stride of 16 (mod 128) bytes so that the 25 rows spread over the banks.
+//
+// Exactness: additions wrap (VIADD.16x2 / VIADDMNMX have no saturation), so a lane is trusted only
+// if its best never exceeded limit = 32767 - max(matrix); H grows by at most max(matrix) per
+// step, hence no wrap can precede a value above the limit.  Lanes above the limit are appended to
+// flag_list and re-run by the int32 kernel: the reference's contract for saturated lanes
+// (align.hpp:149-153).
+// ------------------------------------------------------------------------------------------------
+struct InterParams {
+    const uint4* codes;
+    const GroupDesc* groups;
+    uint32_t n_groups;
+    const int8_t* prof8;
+    uint32_t pstride;
+    uint32_t n_tiles;        // ceil(m / 32)
+    uint2* border0;
+    uint2* border1;
+    int32_t* slot_scores;    // [n_groups*64]
+    uint32_t* flag_list;
+    uint32_t* flag_count;
+    uint32_t* work_counter;
+    uint32_t neg_open2;      // (-open, -open) packed
+    uint32_t neg_ext2;       // (-extend, -extend) packed
+    int32_t limit;
+    int32_t prof_in_smem;
+};
+
+template <bool kSmemProfile>
+__global__ void __launch_bounds__(kInterThreads, 1) inter_s16_kernel(InterParams p) {
+    constexpr int T = kInterTile;
+    extern __shared__ __align__(16) uint8_t smem_prof[];
+
+    const int8_t* prof;
+    if (kSmemProfile) {
+        const uint32_t n16 = kProfRows * p.pstride / 16;
+        const uint4* src = reinterpret_cast<const uint4*>(p.prof8);
+        uint4* dst = reinterpret_cast<uint4*>(smem_prof);
+        for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
+        prof = reinterpret_cast<const int8_t*>(smem_prof);
+    } else {
+        prof = p.prof8;
+    }
+
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
+
+    for (;;) {
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(p.work_counter, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= p.n_groups) break;
+        const GroupDesc gd = p.groups[g];
+        const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
+        const size_t brow0 = static_cast<size_t>(gd.chunk_base) * kRowsPerChunk * 32 + lane;
+        uint32_t best = 0;
+
+        for (uint32_t tile = 0; tile < p.n_tiles; ++tile) {
+            const int8_t* ptile = prof + tile * T;
+            const bool first = tile == 0, last = tile + 1 == p.n_tiles;
+            const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + brow0;
+            uint2* bout = ((tile & 1) ? p.border1 : p.border0) + brow0;
+
+            uint32_t Hm[T], F[T];
+#pragma unroll
+            for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
+            uint32_t diag_in = NO;
+
+            uint4 cw = gd.n_chunks ? gcodes[0] : make_uint4(0, 0, 0, 0);
+            uint2 bnext = make_uint2(NO, NO);
+            if (!first && gd.n_chunks) bnext = bin[0];
+
+            for (uint32_t chunk = 0; chunk < gd.n_chunks; ++chunk) {
+                const uint4 cur = cw;
+                if (chunk + 1 < gd.n_chunks) cw = gcodes[static_cast<size_t>(chunk + 1) * 32];
+#pragma unroll
+                for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
+                    const uint32_t wa = r < 4 ? cur.x : cur.y;
+                    const uint32_t wb = r < 4 ? cur.z : cur.w;
+                    const uint32_t a1 = (wa >> (8 * (r & 3))) & 0xffu;
+                    const uint32_t a2 = (wb >> (8 * (r & 3))) & 0xffu;
+                    const uint4* pa = reinterpret_cast<const uint4*>(ptile + a1 * p.pstride);
+                    const uint4* pb = reinterpret_cast<const uint4*>(ptile + a2 * p.pstride);
+                    uint32_t wA[T / 4], wB[T / 4];
+#pragma unroll
+                    for (int i = 0; i < T / 16; ++i) {
+                        const uint4 va = pa[i], vb = pb[i];
+                        wA[4 * i] = va.x, wA[4 * i + 1] = va.y, wA[4 * i + 2] = va.z, wA[4 * i + 3] = va.w;
+                        wB[4 * i] = vb.x, wB[4 * i + 1] = vb.y, wB[4 * i + 2] = vb.z, wB[4 * i + 3] = vb.w;
+                    }
+                    const size_t row = static_cast<size_t>(chunk) * kRowsPerChunk + r;
+                    const uint2 bi = bnext;
+                    if (!first) {
+                        // prefetch the next row's inbound border (rows are padded to whole chunks,
+                        // one extra row is read only inside the group's own region or the slack)
+                        const size_t nrow = row + 1;
+                        if (nrow < static_cast<size_t>(gd.n_chunks) * kRowsPerChunk) bnext = bin[nrow * 32];
+                    }
+                    uint32_t hl = bi.x;   // Hm of the column left of the tile, this row
+                    uint32_t E = bi.y;
+                    uint32_t diag = diag_in;
+                    diag_in = hl;
+#pragma unroll
+                    for (int k = 0; k < T; k += 2) {
+                        const uint32_t s0 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xC480u : 0xE6A2u);
+                        const uint32_t s1 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xD591u : 0xF7B3u);
+                        // cell k
+                        E = __viaddmax_s16x2(E, NE, hl);
+                        F[k] = __viaddmax_s16x2(F[k], NE, Hm[k]);
+                        uint32_t h0 = __vimax3_s16x2_relu(__vadd2(diag, s0), E, F[k]);
+                        diag = Hm[k];
+                        hl = __vadd2(h0, NO);
+                        Hm[k] = hl;
+                        // cell k+1
+                        E = __viaddmax_s16x2(E, NE, hl);
+                        F[k + 1] = __viaddmax_s16x2(F[k + 1], NE, Hm[k + 1]);
+                        uint32_t h1 = __vimax3_s16x2_relu(__vadd2(diag, s1), E, F[k + 1]);
+                        diag = Hm[k + 1];
+                        hl = __vadd2(h1, NO);
+                        Hm[k + 1] = hl;
+                        best = __vimax3_s16x2(best, h0, h1);
+                    }
+                    if (!last) bout[row * 32] = make_uint2(hl, E);
+                }
+            }
+        }
+
+        // Epilogue: halves -> slots (lane, lane+32); above the limit -> int32 re-run list.
+        const int32_t sa = static_cast<int32_t>(best & 0xffffu);
+        const int32_t sb = static_cast<int32_t>(best >> 16);
+        const uint32_t slot_a = gd.first_slot + lane, slot_b = slot_a + 32;
+        if (sa > p.limit) p.flag_list[atomicAdd(p.flag_count, 1u)] = slot_a;
+        else p.slot_scores[slot_a] = sa;
+        if (sb > p.limit) p.flag_list[atomicAdd(p.flag_count, 1u)] = slot_b;
+        else p.slot_scores[slot_b] = sb;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Inter-task kernel, int32: the exact re-run of flagged lanes (align.hpp:149-153 -> :42-64), and
+// the only inter-task kernel in "wide" mode (matrix + open outside int8).  One thread per
+// sequence, 16 query columns per pass, thread-private border rows laid out [row][thread].
+// PT = int8_t (prof8) or int32_t (prof32).
+// ------------------------------------------------------------------------------------------------
+struct WideParams {
+    const uint8_t* codes;       // interleaved short pool, as bytes
+    const GroupDesc* groups;
+    const uint32_t* slot_len;
+    const uint32_t* list;       // slots to score; nullptr = every slot 0..n_slots-1
+    const uint32_t* list_count; // device count for `list`
+    uint32_t n_slots;
+    const void* prof;
+    uint32_t pstride;
+    uint32_t n_tiles;           // ceil(m / 16)
+    uint2* border0;             // [max_rows][n_threads]
+    uint2* border1;
+    int32_t* slot_scores;
+    int32_t open, ext;
+};
+
+template <typename PT>
+__global__ void __launch_bounds__(128) inter_s32_kernel(WideParams p) {
+    constexpr int T = kWideTile;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t n_threads = gridDim.x * blockDim.x;
+    const uint32_t count = p.list ? *p.list_count : p.n_slots;
+    const int32_t NO = -p.open, NE = -p.ext;
+    const PT* prof = static_cast<const PT*>(p.prof);
+
+    for (uint32_t item = tid; item < count; item += n_threads) {
+        const uint32_t slot = p.list ? p.list[item] : item;
+        const uint32_t len = p.slot_len[slot];
+        const GroupDesc gd = p.groups[slot / kGroupSeqs];
+        const uint32_t s = slot % kGroupSeqs, lane = s & 31, half = s >> 5;
+        const uint8_t* seq = p.codes + (static_cast<size_t>(gd.chunk_base) * 32 + lane) * 16 + half * 8;
+        int32_t best = 0;
+        for (uint32_t tile = 0; tile < p.n_tiles; ++tile) {
+            const PT* ptile = prof + tile * T;
+            const bool first = tile == 0, last = tile + 1 == p.n_tiles;
+            const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + tid;
+            uint2* bout = ((tile & 1) ? p.border1 : p.border0) + tid;
+            int32_t Hm[T], F[T];
+#pragma unroll
+            for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
+            int32_t diag_in = NO;
+            for (uint32_t row = 0; row < len; ++row) {
+                const uint32_t a = seq[static_cast<size_t>(row / kRowsPerChunk) * 512 + (row % kRowsPerChunk)];
+                int32_t sub[T];
+                if (sizeof(PT) == 1) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(ptile + a * p.pstride);
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int k = 0; k < T; ++k)
+                        sub[k] = static_cast<int32_t>(static_cast<int8_t>((w[k / 4] >> (8 * (k & 3))) & 0xff));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < T / 4; ++i) {
+                        const int4 v = *reinterpret_cast<const int4*>(ptile + a * p.pstride + 4 * i);
+                        sub[4 * i] = v.x, sub[4 * i + 1] = v.y, sub[4 * i + 2] = v.z, sub[4 * i + 3] = v.w;
+                    }
+                }
+                int32_t hl = NO, E = NO;
+                if (!first) {
+                    const uint2 bi = bin[static_cast<size_t>(row) * n_threads];
+                    hl = static_cast<int32_t>(bi.x), E = static_cast<int32_t>(bi.y);
+                }
+                int32_t diag = diag_in;
+                diag_in = hl;
+#pragma unroll
+                for (int k = 0; k < T; ++k) {
+                    E = __viaddmax_s32(E, NE, hl);
+                    F[k] = __viaddmax_s32(F[k], NE, Hm[k]);
+                    const int32_t h = __vimax3_s32_relu(diag + sub[k], E, F[k]);
+                    diag = Hm[k];
+                    hl = h + NO;
+                    Hm[k] = hl;
+                    best = max(best, h);
+                }
+                if (!last) bout[static_cast<size_t>(row) * n_threads] = make_uint2(hl, E);
+            }
+        }
+        p.slot_scores[slot] = best;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Intra-task kernel (int32): one CTA per long sequence (align.hpp:166-229 re-designed).
+//
+// The query is striped over lanes, T (<= 8) columns per lane, 32*T per warp, W warps side by side
+// (W*32*T columns per pass).  Lane l of warp w handles subject row  d - w*Delta - l  at step d:
+// an anti-diagonal wavefront.  The (Hm, E) border of a lane's last column moves to its right
+// neighbour with one __shfl_up per step; between warps it goes through a shared-memory ring
+// (written by lane 31, read by the next warp's lane 0 >= 33 steps later, one __syncthreads every
+// 32 steps); between passes it goes through a per-sequence border row in global memory.
+// The diagonal seed is the previous step's inbound Hm, exactly the reference's diag_seed
+// (align.hpp:223).  Rows outside [0, n) are pad rows: before the start they leave the initial
+// state untouched, after the end they cannot raise `best`.
+// ------------------------------------------------------------------------------------------------
+struct IntraParams {
+    const uint8_t* codes;     // long pool
+    const LongDesc* longs;
+    uint32_t n_long;
+    const void* profi;        // prof8i or prof32i
+    uint32_t n_lane_tiles;    // 8-slot words per profile row
+    uint32_t n_passes;
+    uint2* border0;           // [long pool rows] (indexed by LongDesc::offset + row)
+    uint2* border1;
+    int32_t* long_scores;     // [n_long]
+    int32_t open, ext;
+};
+
+template <int T, typename PT>
+__global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraParams p) {
+    __shared__ uint2 ring[kIntraMaxWarps][kIntraRing];
+    __shared__ int32_t warp_best[kIntraMaxWarps];
+
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const LongDesc ld = p.longs[blockIdx.x];
+    const int64_t n = ld.length;
+    const uint8_t* seq = p.codes + ld.offset;
+    const int32_t NO = -p.open, NE = -p.ext;
+    const PT* prof = static_cast<const PT*>(p.profi);
+    const uint32_t row_words = p.n_lane_tiles * 8;
+
+    int32_t best = 0;
+    const int64_t steps = n + 31 + static_cast<int64_t>(kIntraDelta) * (W - 1);
+
+    for (uint32_t pass = 0; pass < p.n_passes; ++pass) {
+        const uint32_t lane_tile = (pass * W + w) * 32 + lane;   // which T-column stripe this lane owns
+        const bool tile_valid = lane_tile < p.n_lane_tiles;
+        const PT* ptile = prof + static_cast<size_t>(tile_valid ? lane_tile : 0) * 8;
+        const bool first = pass == 0, last = pass + 1 == p.n_passes;
+        const uint2* bin = ((pass & 1) ? p.border0 : p.border1) + ld.offset;
+        uint2* bout = ((pass & 1) ? p.border1 : p.border0) + ld.offset;
+
+        int32_t Hm[T], F[T];
+#pragma unroll
+        for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
+        int32_t diag_in = NO, out_h = NO, out_e = NO;
+
+        if (W > 1) __syncthreads();   // ring reuse across passes
+
+        for (int64_t d = 0; d < steps; ++d) {
+            const int64_t r = d - static_cast<int64_t>(w) * kIntraDelta - lane;
+            const bool in_range = r >= 0 && r < n;
+            const uint32_t a = (in_range && tile_valid) ? seq[r] : kPadCode;
+
+            // inbound border: from the left lane (previous step), the left warp's ring, the
+            // previous pass's global row, or the matrix edge
+            int32_t in_h = __shfl_up_sync(0xffffffffu, out_h, 1);
+            int32_t in_e = __shfl_up_sync(0xffffffffu, out_e, 1);
+            if (lane == 0) {
+                in_h = NO, in_e = NO;
+                if (in_range) {
+                    if (w > 0) {
+                        const uint2 v = ring[w][r & (kIntraRing - 1)];
+                        in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
+                    } else if (!first) {
+                        const uint2 v = bin[r];
+                        in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
+                    }
+                }
+            }
+
+            int32_t sub[T];
+            if (sizeof(PT) == 1) {
+                const uint2 v = *reinterpret_cast<const uint2*>(ptile + static_cast<size_t>(a) * row_words);
+#pragma unroll
+                for (int k = 0; k < T; ++k) {
+                    const uint32_t word = k < 4 ? v.x : v.y;
+                    const uint32_t sel = (k & 3) == 0 ? 0x8880u : (k & 3) == 1 ? 0x9991u : (k & 3) == 2 ? 0xAAA2u : 0xBBB3u;
+                    sub[k] = static_cast<int32_t>(prmt(word, 0, sel));
+                }
+            } else {
+                const int4* q = reinterpret_cast<const int4*>(ptile + static_cast<size_t>(a) * row_words);
+                const int4 v0 = q[0];
+                const int4 v1 = T > 4 ? q[1] : make_int4(0, 0, 0, 0);
+                const int32_t all[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (int k = 0; k < T; ++k) sub[k] = all[k];
+            }
+
+            int32_t hl = in_h, E = in_e;
+            int32_t diag = diag_in;
+            diag_in = in_h;
+#pragma unroll
+            for (int k = 0; k < T; ++k) {
+                E = __viaddmax_s32(E, NE, hl);
+                F[k] = __viaddmax_s32(F[k], NE, Hm[k]);
+                const int32_t h = __vimax3_s32_relu(diag + sub[k], E, F[k]);
+                diag = Hm[k];
+                hl = h + NO;
+                Hm[k] = hl;
+                best = max(best, h);
+            }
+            out_h = hl, out_e = E;
+
+            if (lane == 31 && in_range) {
+                if (w + 1 < W) ring[w + 1][r & (kIntraRing - 1)] = make_uint2(hl, E);
+                else if (!last) bout[r] = make_uint2(hl, E);
+            }
+            if (W > 1 && (d & 31) == 31) __syncthreads();
+        }
+    }
+
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) warp_best[w] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 1; i < W; ++i) best = max(best, warp_best[i]);
+        p.long_scores[blockIdx.x] = best;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Score gather (merge_results, scheduler.hpp:106-117, without the full sort).
+//   key = (score << 32) | (0xFFFFFFFF - db_index): descending key order == (score desc, index asc).
+//   0 is never a valid key (db_index < 2^32 - 1), so it pads.
+// select: every block bitonic-sorts a slice of 4096 keys in shared memory and emits its top k;
+// rounds repeat until one block remains.  k <= 1024 here; larger k takes the full bitonic sort.
+// ------------------------------------------------------------------------------------------------
+constexpr int kSelectSlice = 4096;
+constexpr int kSelectThreads = 1024;
+constexpr uint32_t kSelectMaxK = 1024;
+
+__global__ void build_keys_kernel(const int32_t* slot_scores, const uint32_t* slot_index, uint32_t n_slots,
+                                  const int32_t* long_scores, const LongDesc* longs, uint32_t n_long,
+                                  uint64_t* keys) {
+    const uint32_t total = n_slots + n_long;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        uint64_t key = 0;
+        if (i < n_slots) {
+            const uint32_t idx = slot_index[i];
+            if (idx != kNoSequence)
+                key = (static_cast<uint64_t>(static_cast<uint32_t>(slot_scores[i])) << 32) | (0xFFFFFFFFu - idx);
+        } else {
+            const uint32_t pidx = i - n_slots;
+            key = (static_cast<uint64_t>(static_cast<uint32_t>(long_scores[pidx])) << 32) |
+                  (0xFFFFFFFFu - longs[pidx].db_index);
+        }
+        keys[i] = key;
+    }
+}
+
+__global__ void scatter_scores_kernel(const int32_t* slot_scores, const uint32_t* slot_index, uint32_t n_slots,
+                                      const int32_t* long_scores, const LongDesc* longs, uint32_t n_long,
+                                      int32_t* out) {
+    const uint32_t total = n_slots + n_long;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        if (i < n_slots) {
+            const uint32_t idx = slot_index[i];
+            if (idx != kNoSequence) out[idx] = slot_scores[i];
+        } else {
+            out[longs[i - n_slots].db_index] = long_scores[i - n_slots];
+        }
+    }
+}
+
+// Sort `s` (kSelectSlice keys in shared memory) descending.
+__device__ __forceinline__ void bitonic_sort_desc(uint64_t* s) {
+    for (uint32_t size = 2; size <= kSelectSlice; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            __syncthreads();
+            for (uint32_t t = threadIdx.x; t < kSelectSlice / 2; t += blockDim.x) {
+                const uint32_t lo = 2 * t - (t & (stride - 1));
+                const uint32_t hi = lo + stride;
+                const bool desc = (lo & size) == 0;
+                const uint64_t a = s[lo], b = s[hi];
+                if ((a < b) == desc) s[lo] = b, s[hi] = a;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSelectThreads) select_topk_kernel(const uint64_t* in, uint64_t n, uint32_t k,
+                                                                      uint64_t* out) {
+    __shared__ uint64_t s[kSelectSlice];
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kSelectSlice;
+    for (uint32_t i = threadIdx.x; i < kSelectSlice; i += blockDim.x) s[i] = base + i < n ? in[base + i] : 0ull;
+    bitonic_sort_desc(s);
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) out[static_cast<uint64_t>(blockIdx.x) * k + i] = s[i];
+}
+
+// Full descending bitonic sort in global memory for k > kSelectMaxK (n padded to a power of two).
+__global__ void bitonic_step_kernel(uint64_t* keys, uint64_t n_pow2, uint64_t size, uint64_t stride) {
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < n_pow2 / 2;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t lo = 2 * t - (t & (stride - 1));
+        const uint64_t hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const uint64_t a = keys[lo], b = keys[hi];
+        if ((a < b) == desc) keys[lo] = b, keys[hi] = a;
+    }
+}
+
+__global__ void keys_to_hits_kernel(const uint64_t* keys, uint32_t k, uint32_t* out_index, int32_t* out_score,
+                                    uint32_t* out_count) {
+    uint32_t cnt = 0;
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        const uint64_t key = keys[i];
+        if (key) {
+            out_index[i] = 0xFFFFFFFFu - static_cast<uint32_t>(key & 0xFFFFFFFFu);
+            out_score[i] = static_cast<int32_t>(key >> 32);
+            ++cnt;
+        }
+    }
+    if (cnt) atomicAdd(out_count, cnt);
+}
+
+}  // namespace swb

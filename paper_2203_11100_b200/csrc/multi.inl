@@ -1,0 +1,273 @@
+// multi.inl -- several GPUs of one box driven from one process (included by cabi.cu).
+//
+// The database is dealt over the devices by residue count (pack.hpp: snake deal of the
+// length-sorted pools).  A search runs every shard concurrently (one host thread per shard, each
+// on its shard's own stream), each producing its top-k as packed keys on its device.  The only
+// exchange is k x 8 bytes per shard: one ncclAllGather over NVLink (ncclCommInitAll communicator,
+// grouped call), after which shard 0 selects the global top-k from the G x k gathered keys.
+// NCCL is loaded with dlopen only when two or more distinct devices are used, so a single-GPU
+// process never needs it.  Shards that share a device (used to exercise the sharding logic on a
+// one-GPU box) cannot form an NCCL communicator (NCCL rejects duplicate devices), so their keys
+// are gathered with device-to-device copies on that device instead.
+
+namespace {
+
+struct NcclApi {
+    void* handle = nullptr;
+    int (*CommInitAll)(void**, int, const int*) = nullptr;
+    int (*CommDestroy)(void*) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+
+    bool load(std::string* why) {
+        if (handle) return true;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            handle = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+            if (handle) break;
+        }
+        if (!handle) {
+            *why = std::string("cannot load libnccl: ") + dlerror();
+            return false;
+        }
+        CommInitAll = reinterpret_cast<decltype(CommInitAll)>(dlsym(handle, "ncclCommInitAll"));
+        CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(handle, "ncclCommDestroy"));
+        GroupStart = reinterpret_cast<decltype(GroupStart)>(dlsym(handle, "ncclGroupStart"));
+        GroupEnd = reinterpret_cast<decltype(GroupEnd)>(dlsym(handle, "ncclGroupEnd"));
+        AllGather = reinterpret_cast<decltype(AllGather)>(dlsym(handle, "ncclAllGather"));
+        GetErrorString = reinterpret_cast<decltype(GetErrorString)>(dlsym(handle, "ncclGetErrorString"));
+        if (!CommInitAll || !CommDestroy || !GroupStart || !GroupEnd || !AllGather || !GetErrorString) {
+            *why = "libnccl is missing a required symbol";
+            return false;
+        }
+        return true;
+    }
+};
+
+constexpr int kNcclUint64 = 5;   // ncclUint64 (nccl.h)
+
+}  // namespace
+
+struct swb_mdb {
+    std::vector<swb_db*> shards;
+    std::vector<int> devices;
+    bool distinct = true;
+    NcclApi nccl;
+    std::vector<void*> comms;
+    std::vector<uint64_t*> d_gather;   // per shard: G * k_cap keys on that shard's device
+    std::vector<uint64_t*> d_send;     // per shard: k_cap keys
+    uint32_t k_cap = 0;
+    std::mutex mu;
+};
+
+namespace {
+
+swb_status mdb_build(const SeqSource& src, uint64_t threshold, const int32_t* devices, uint32_t n_devices,
+                     swb_mdb** out) {
+    if (!out) return fail(SWB_ERR_INVALID, "out is null");
+    *out = nullptr;
+    if (n_devices < 1 || !devices) return fail(SWB_ERR_INVALID, "at least one device is required");
+    auto* mdb = new swb_mdb();
+    mdb->devices.assign(devices, devices + n_devices);
+    std::vector<int> sorted(mdb->devices);
+    std::sort(sorted.begin(), sorted.end());
+    mdb->distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+    mdb->shards.assign(n_devices, nullptr);
+
+    // pack + upload the shards concurrently (each on its own device)
+    std::vector<swb_status> sts(n_devices, SWB_OK);
+    std::vector<std::string> errs(n_devices);
+    std::vector<std::thread> pool;
+    for (uint32_t r = 0; r < n_devices; ++r)
+        pool.emplace_back([&, r] {
+            sts[r] = create_from(src, threshold, devices[r], r, n_devices, &mdb->shards[r]);
+            if (sts[r] != SWB_OK) errs[r] = g_error;
+        });
+    for (auto& t : pool) t.join();
+    for (uint32_t r = 0; r < n_devices; ++r)
+        if (sts[r] != SWB_OK) {
+            const swb_status st = sts[r];
+            const std::string msg = errs[r];
+            swb_mdb_destroy(mdb);
+            return fail(st, msg);
+        }
+
+    if (n_devices > 1 && mdb->distinct) {
+        std::string why;
+        if (!mdb->nccl.load(&why)) {
+            swb_mdb_destroy(mdb);
+            return fail(SWB_ERR_NCCL, why);
+        }
+        mdb->comms.assign(n_devices, nullptr);
+        const int rc = mdb->nccl.CommInitAll(mdb->comms.data(), static_cast<int>(n_devices), mdb->devices.data());
+        if (rc != 0) {
+            const std::string msg = std::string("ncclCommInitAll: ") + mdb->nccl.GetErrorString(rc);
+            mdb->comms.clear();
+            swb_mdb_destroy(mdb);
+            return fail(SWB_ERR_NCCL, msg);
+        }
+    }
+    *out = mdb;
+    return SWB_OK;
+}
+
+swb_status mdb_ensure_buffers(swb_mdb* mdb, uint32_t k) {
+    if (k <= mdb->k_cap) return SWB_OK;
+    const size_t G = mdb->shards.size();
+    for (size_t r = 0; r < mdb->d_gather.size(); ++r) {
+        DeviceGuard guard(mdb->devices[r]);
+        if (mdb->d_gather[r]) cudaFree(mdb->d_gather[r]);
+        if (mdb->d_send[r]) cudaFree(mdb->d_send[r]);
+    }
+    mdb->d_gather.assign(G, nullptr);
+    mdb->d_send.assign(G, nullptr);
+    mdb->k_cap = 0;
+    for (size_t r = 0; r < G; ++r) {
+        DeviceGuard guard(mdb->devices[r]);
+        SWB_CUDA(cudaMalloc(reinterpret_cast<void**>(&mdb->d_gather[r]), G * k * sizeof(uint64_t)));
+        SWB_CUDA(cudaMalloc(reinterpret_cast<void**>(&mdb->d_send[r]), static_cast<size_t>(k) * sizeof(uint64_t)));
+    }
+    mdb->k_cap = k;
+    return SWB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+swb_status swb_mdb_create_flat(const uint8_t* codes, const uint64_t* offsets, uint32_t n, uint64_t length_threshold,
+                               const int32_t* devices, uint32_t n_devices, swb_mdb** out) {
+    if (!offsets) return fail(SWB_ERR_INVALID, "offsets is null");
+    for (uint32_t i = 0; i < n; ++i)
+        if (offsets[i + 1] < offsets[i]) return fail(SWB_ERR_INVALID, "offsets must be non-decreasing");
+    SeqSource src;
+    src.flat = codes;
+    src.offsets = offsets;
+    src.n = n;
+    return mdb_build(src, length_threshold, devices, n_devices, out);
+}
+
+swb_status swb_mdb_create(const uint8_t* const* seqs, const uint32_t* lens, uint32_t n, uint64_t length_threshold,
+                          const int32_t* devices, uint32_t n_devices, swb_mdb** out) {
+    if (n && (!seqs || !lens)) return fail(SWB_ERR_INVALID, "seqs/lens are null");
+    static const uint8_t* const kNoPtrs[1] = {nullptr};
+    static const uint32_t kNoLens[1] = {0};
+    SeqSource src;
+    src.ptrs = n ? seqs : kNoPtrs;
+    src.lens = n ? lens : kNoLens;
+    src.n = n;
+    return mdb_build(src, length_threshold, devices, n_devices, out);
+}
+
+void swb_mdb_destroy(swb_mdb* mdb) {
+    if (!mdb) return;
+    for (size_t r = 0; r < mdb->comms.size(); ++r)
+        if (mdb->comms[r]) mdb->nccl.CommDestroy(mdb->comms[r]);
+    for (size_t r = 0; r < mdb->d_gather.size(); ++r) {
+        DeviceGuard guard(mdb->devices[r]);
+        if (mdb->d_gather[r]) cudaFree(mdb->d_gather[r]);
+        if (mdb->d_send[r]) cudaFree(mdb->d_send[r]);
+    }
+    for (swb_db* db : mdb->shards) swb_db_destroy(db);
+    delete mdb;
+}
+
+uint32_t swb_mdb_shard_count(const swb_mdb* mdb) { return mdb ? static_cast<uint32_t>(mdb->shards.size()) : 0; }
+
+swb_db* swb_mdb_shard(swb_mdb* mdb, uint32_t i) {
+    return (mdb && i < mdb->shards.size()) ? mdb->shards[i] : nullptr;
+}
+
+swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
+                          int32_t gap_open, int32_t gap_extend, uint32_t top_k, swb_hit* hits, uint32_t* n_hits,
+                          swb_stats* stats) {
+    if (!mdb) return fail(SWB_ERR_INVALID, "mdb is null");
+    if (!hits || !n_hits) return fail(SWB_ERR_INVALID, "hits/n_hits are null");
+    if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
+    const size_t G = mdb->shards.size();
+    if (G == 1) return swb_search(mdb->shards[0], query, query_len, matrix, gap_open, gap_extend, top_k, hits, n_hits, stats);
+    swb_status st = check_scoring_args(query, query_len, matrix, gap_open, gap_extend);
+    if (st != SWB_OK) return st;
+
+    std::lock_guard<std::mutex> lock(mdb->mu);
+    // no shard can contribute more than the whole database holds
+    const uint32_t n_total = mdb->shards[0]->meta.n_total;
+    const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint32_t>(n_total, 1)));
+    if ((st = mdb_ensure_buffers(mdb, k)) != SWB_OK) return st;
+
+    // 1. every shard scores and selects concurrently; its keys stay on its device
+    std::vector<swb_status> sts(G, SWB_OK);
+    std::vector<std::string> errs(G);
+    std::vector<swb_stats> sstats(G);
+    std::vector<std::thread> pool;
+    for (size_t r = 0; r < G; ++r)
+        pool.emplace_back([&, r] {
+            swb_db* db = mdb->shards[r];
+            std::vector<uint64_t> host(k);
+            void* dkeys = nullptr;
+            sts[r] = swb_search_keys(db, query, query_len, matrix, gap_open, gap_extend, k, host.data(), &dkeys, &sstats[r]);
+            if (sts[r] != SWB_OK) {
+                errs[r] = g_error;
+                return;
+            }
+            DeviceGuard guard(db->device);
+            // zero-padded send buffer (a shard may hold fewer than k sequences)
+            cudaError_t e = cudaMemcpyAsync(mdb->d_send[r], host.data(), k * sizeof(uint64_t), cudaMemcpyHostToDevice, db->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(db->stream);
+            if (e != cudaSuccess) {
+                sts[r] = SWB_ERR_CUDA;
+                errs[r] = cudaGetErrorString(e);
+            }
+        });
+    for (auto& t : pool) t.join();
+    for (size_t r = 0; r < G; ++r)
+        if (sts[r] != SWB_OK) return fail(sts[r], errs[r]);
+
+    // 2. exchange: k keys per shard
+    if (mdb->distinct) {
+        int rc = mdb->nccl.GroupStart();
+        for (size_t r = 0; r < G && rc == 0; ++r) {
+            DeviceGuard guard(mdb->devices[r]);
+            rc = mdb->nccl.AllGather(mdb->d_send[r], mdb->d_gather[r], k, kNcclUint64, mdb->comms[r], mdb->shards[r]->stream);
+        }
+        const int rc_end = mdb->nccl.GroupEnd();
+        if (rc == 0) rc = rc_end;
+        if (rc != 0) return fail(SWB_ERR_NCCL, std::string("ncclAllGather: ") + mdb->nccl.GetErrorString(rc));
+        for (size_t r = 0; r < G; ++r) {
+            DeviceGuard guard(mdb->devices[r]);
+            SWB_CUDA(cudaStreamSynchronize(mdb->shards[r]->stream));
+        }
+    } else {
+        DeviceGuard guard(mdb->devices[0]);
+        for (size_t r = 0; r < G; ++r)
+            SWB_CUDA(cudaMemcpyPeerAsync(mdb->d_gather[0] + r * k, mdb->devices[0], mdb->d_send[r], mdb->devices[r],
+                                         k * sizeof(uint64_t), mdb->shards[0]->stream));
+        SWB_CUDA(cudaStreamSynchronize(mdb->shards[0]->stream));
+    }
+
+    // 3. global select on shard 0's device
+    st = swb_merge_keys(mdb->d_gather[0], G * k, 1, mdb->devices[0], top_k, hits, n_hits);
+    if (st != SWB_OK) return st;
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        for (size_t r = 0; r < G; ++r) {
+            stats->lane_scored += sstats[r].lane_scored;
+            stats->wavefront_scored += sstats[r].wavefront_scored;
+            stats->chunks_claimed += sstats[r].chunks_claimed;
+            stats->rescored_i32 += sstats[r].rescored_i32;
+            stats->cells += sstats[r].cells;
+            stats->padded_cells += sstats[r].padded_cells;
+            stats->kernel_launches += sstats[r].kernel_launches;
+            stats->ms_total = std::max(stats->ms_total, sstats[r].ms_total);
+            stats->ms_inter = std::max(stats->ms_inter, sstats[r].ms_inter);
+            stats->ms_intra = std::max(stats->ms_intra, sstats[r].ms_intra);
+            stats->ms_rescore = std::max(stats->ms_rescore, sstats[r].ms_rescore);
+            stats->ms_topk = std::max(stats->ms_topk, sstats[r].ms_topk);
+            stats->ms_h2d_d2h = std::max(stats->ms_h2d_d2h, sstats[r].ms_h2d_d2h);
+        }
+    }
+    return SWB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+"""One process per GPU (torchrun): database sharded by residue count, per-shard top-k merged with one
+all-gather of k packed 64-bit keys per rank (NCCL over NVLink on GPUs; gloo in the CPU tests).
+
+The data path has no other collective: every (query, subject) score is independent
+(align.hpp:80-82) and the (score desc, index asc) order is a strict total order
+(scheduler.hpp:111-114), so top-k of the union == top-k of the per-shard top-k's.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def exchange_keys(local_keys: np.ndarray, device: torch.device | None = None, group=None) -> np.ndarray:
+    """All-gather this rank's top_k packed keys (zero padded to a common length).
+
+    Returns the concatenation over ranks, shape (world * k,).  uint64 keys travel as int64 bit
+    patterns (NCCL/gloo have no uint64 tensor type in torch)."""
+    world = dist.get_world_size(group)
+    send = torch.from_numpy(np.ascontiguousarray(local_keys, dtype=np.uint64).view(np.int64).copy())
+    if device is not None and device.type == "cuda":
+        send = send.to(device, non_blocking=True)
+    recv = torch.empty(world * send.numel(), dtype=torch.int64, device=send.device)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    return recv.cpu().numpy().view(np.uint64)
+
+
+class ShardedSearch:
+    """This rank's shard of the database plus the cross-rank merge."""
+
+    def __init__(self, codes, offsets, length_threshold: int = 3000, device_index: int = 0, group=None):
+        from .search import Database
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.device_index = device_index
+        self.db = Database(codes, offsets, length_threshold=length_threshold, device=device_index,
+                           shard_rank=self.rank, shard_count=self.world)
+
+    def search(self, query, matrix, gaps, top_k: int = 10):
+        """-> (db_index, score, local stats).  Every rank returns the same global list."""
+        from .search import decode_keys, merge_keys
+        keys, _, stats = self.db.search_keys(query, matrix, gaps, top_k)
+        if self.world == 1:
+            idx, sc = decode_keys(keys)
+            return idx, sc, stats
+        gathered = exchange_keys(keys, torch.device("cuda", self.device_index), self.group)
+        idx, sc = merge_keys(gathered, top_k, device=self.device_index)
+        return idx, sc, stats
+
+    def close(self):
+        self.db.close()

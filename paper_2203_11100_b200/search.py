@@ -1,0 +1,291 @@
+"""Python host side above the C-ABI: the reference's search interface, names and error behaviour
+(scheduler.hpp:20-36, 86-124, 184-251), driving libswb200.so through ctypes.
+
+This is what bench.py and the parity tests call; the C++ drop-in lives in include/swsearch/.
+Nothing here computes scores on the CPU: every call goes to the CUDA library or raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _cabi
+
+_u8p, _i32p, _u32p, _u64p = _cabi.u8p, _cabi.i32p, _cabi.u32p, _cabi.u64p
+
+
+class SwbError(RuntimeError):
+    """CUDA / NCCL / internal failure reported by the library."""
+
+
+def _raise(lib, rc: int):
+    if rc == _cabi.SWB_OK:
+        return
+    msg = lib.swb_last_error().decode()
+    if rc == _cabi.SWB_ERR_INVALID:
+        raise ValueError(msg)          # std::invalid_argument in the reference
+    if rc == _cabi.SWB_ERR_RANGE:
+        raise IndexError(msg)          # std::out_of_range (scoring.hpp:203-205)
+    raise SwbError(f"[{rc}] {msg}")
+
+
+def _u8(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint8))
+
+
+def _mat(matrix) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(matrix, dtype=np.int32).reshape(576))
+
+
+def _ptr(arr, typ):
+    return arr.ctypes.data_as(typ)
+
+
+@dataclass
+class SearchConfig:
+    """scheduler.hpp:20-36.  worker_count / lane_width / chunk_width / cpu_pool_threads are
+    validated but result-invisible (scheduler.hpp:18-19); the GPU path ignores them."""
+    worker_count: int = 1
+    lane_width: int = 8
+    chunk_width: int = 64
+    length_threshold: int = 3000
+    top_k: int = 10
+    cpu_pool_threads: int = 1
+
+    def validate(self):
+        if self.worker_count < 1:
+            raise ValueError("worker_count must be >= 1")
+        if self.lane_width < 1:
+            raise ValueError("lane_width must be >= 1")
+        if self.chunk_width < 1:
+            raise ValueError("chunk_width must be >= 1")
+        if self.top_k < 1:
+            raise ValueError("top_k must be >= 1")
+
+
+@dataclass
+class GapModel:
+    """scoring.hpp:48-61."""
+    open: int = 10
+    extend: int = 2
+
+    def __post_init__(self):
+        if self.extend < 0 or self.open < self.extend:
+            raise ValueError("gap model requires open >= extend >= 0")
+
+
+class Database:
+    """One packed shard resident on one GPU (swb_db)."""
+
+    def __init__(self, codes, offsets, length_threshold: int = 3000, device: int = 0, shard_rank: int = 0,
+                 shard_count: int = 1):
+        self._lib = _cabi.load()
+        self._h = C.c_void_p()
+        codes = _u8(codes)
+        offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+        self.n_total = len(offsets) - 1
+        keep = codes if len(codes) else np.zeros(1, np.uint8)
+        rc = self._lib.swb_db_create_flat(_ptr(keep, _u8p), _ptr(offsets, _u64p), self.n_total,
+                                          int(length_threshold) & (2 ** 64 - 1), device, shard_rank, shard_count,
+                                          C.byref(self._h))
+        _raise(self._lib, rc)
+        self.device = device
+
+    @classmethod
+    def from_sequences(cls, seqs, **kw):
+        lens = np.array([len(s) for s in seqs], dtype=np.uint64)
+        offsets = np.zeros(len(seqs) + 1, dtype=np.uint64)
+        np.cumsum(lens, out=offsets[1:])
+        codes = np.concatenate([_u8(s) for s in seqs]) if len(seqs) and offsets[-1] else np.zeros(0, np.uint8)
+        return cls(codes, offsets, **kw)
+
+    def close(self):
+        if self._h:
+            self._lib.swb_db_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def info(self) -> dict:
+        info = _cabi.SwbDbInfo()
+        _raise(self._lib, self._lib.swb_db_info_get(self._h, C.byref(info)))
+        return info.as_dict()
+
+    def set_stream(self, cuda_stream: int):
+        _raise(self._lib, self._lib.swb_db_set_stream(self._h, C.c_void_p(cuda_stream)))
+
+    def search(self, query, matrix, gaps: GapModel, top_k: int = 10):
+        """-> (db_index[uint32], score[int32], stats dict), at most top_k hits, final order."""
+        q, mat = _u8(query), _mat(matrix)
+        hits = (_cabi.SwbHit * max(1, top_k))()
+        n = C.c_uint32(0)
+        st = _cabi.SwbStats()
+        rc = self._lib.swb_search(self._h, _ptr(q, _u8p), len(q), _ptr(mat, _i32p), gaps.open, gaps.extend,
+                                  top_k, hits, C.byref(n), C.byref(st))
+        _raise(self._lib, rc)
+        idx = np.array([hits[i].db_index for i in range(n.value)], dtype=np.uint32)
+        sc = np.array([hits[i].score for i in range(n.value)], dtype=np.int32)
+        return idx, sc, st.as_dict()
+
+    def search_keys(self, query, matrix, gaps: GapModel, top_k: int = 10):
+        """-> (keys[uint64, top_k] zero padded, device pointer or None, stats)."""
+        q, mat = _u8(query), _mat(matrix)
+        keys = np.zeros(max(1, top_k), dtype=np.uint64)
+        dptr = C.c_void_p()
+        st = _cabi.SwbStats()
+        rc = self._lib.swb_search_keys(self._h, _ptr(q, _u8p), len(q), _ptr(mat, _i32p), gaps.open, gaps.extend,
+                                       top_k, _ptr(keys, _u64p), C.byref(dptr), C.byref(st))
+        _raise(self._lib, rc)
+        return keys[:top_k], dptr.value, st.as_dict()
+
+    def score_all(self, query, matrix, gaps: GapModel, out: np.ndarray | None = None):
+        """Scores of all n_total sequences in db order (other shards' entries untouched)."""
+        q, mat = _u8(query), _mat(matrix)
+        if out is None:
+            out = np.zeros(max(1, self.n_total), dtype=np.int32)
+        st = _cabi.SwbStats()
+        rc = self._lib.swb_score_all(self._h, _ptr(q, _u8p), len(q), _ptr(mat, _i32p), gaps.open, gaps.extend,
+                                     _ptr(out, _i32p), C.byref(st))
+        _raise(self._lib, rc)
+        return out[:self.n_total], st.as_dict()
+
+
+def merge_keys(keys, top_k: int, device: int = 0):
+    """Cross-shard merge on the GPU (merge_results, scheduler.hpp:106-117)."""
+    lib = _cabi.load()
+    keys = np.ascontiguousarray(np.asarray(keys, dtype=np.uint64).reshape(-1))
+    hits = (_cabi.SwbHit * max(1, top_k))()
+    n = C.c_uint32(0)
+    rc = lib.swb_merge_keys(keys.ctypes.data_as(C.c_void_p), len(keys), 0, device, top_k, hits, C.byref(n))
+    _raise(lib, rc)
+    idx = np.array([hits[i].db_index for i in range(n.value)], dtype=np.uint32)
+    sc = np.array([hits[i].score for i in range(n.value)], dtype=np.int32)
+    return idx, sc
+
+
+def decode_keys(keys):
+    """Packed keys -> (db_index, score) for the non-zero entries, order preserved."""
+    keys = np.asarray(keys, dtype=np.uint64).reshape(-1)
+    keys = keys[keys != 0]
+    idx = (np.uint64(0xFFFFFFFF) - (keys & np.uint64(0xFFFFFFFF))).astype(np.uint32)
+    sc = (keys >> np.uint64(32)).astype(np.int64).astype(np.int32)
+    return idx, sc
+
+
+def encode_keys(index, score):
+    index = np.asarray(index, dtype=np.uint64)
+    score = np.asarray(score, dtype=np.int64).astype(np.uint64)
+    return (score << np.uint64(32)) | (np.uint64(0xFFFFFFFF) - index)
+
+
+def run_search(query, db: Database, matrix, gaps: GapModel, config: SearchConfig | None = None):
+    """run_search (scheduler.hpp:184-251) with compute_alignments=false: the timed region of
+    SPEC.md:403.  length_threshold was fixed when `db` was packed."""
+    config = config or SearchConfig()
+    config.validate()
+    idx, sc, st = db.search(query, matrix, gaps, config.top_k)
+    stats = {"lane_scored": st["lane_scored"], "wavefront_scored": st["wavefront_scored"],
+             "chunks_claimed": st["chunks_claimed"]}
+    return idx, sc, stats, st
+
+
+def score_batch(query, subjects, lane_width: int, matrix, gaps: GapModel, device: int = 0):
+    """sw_score_batch (align.hpp:91-159): subjects may contain None (padding lanes)."""
+    lib = _cabi.load()
+    q, mat = _u8(query), _mat(matrix)
+    keep = [None if s is None else _u8(s) for s in subjects]
+    ptrs = (_u8p * max(1, len(keep)))()
+    lens = np.zeros(max(1, len(keep)), dtype=np.uint32)
+    dummy = np.zeros(1, np.uint8)
+    for i, s in enumerate(keep):
+        if s is None:
+            ptrs[i] = None
+        else:
+            ptrs[i] = _ptr(s if len(s) else dummy, _u8p)
+            lens[i] = len(s)
+    out = np.zeros(max(1, lane_width), dtype=np.int32)
+    rc = lib.swb_score_batch(_ptr(q, _u8p), len(q), ptrs, _ptr(lens, _u32p), len(keep), lane_width,
+                             _ptr(mat, _i32p), gaps.open, gaps.extend, device, _ptr(out, _i32p))
+    _raise(lib, rc)
+    return out[:lane_width].copy()
+
+
+def score_wavefront(query, subject, matrix, gaps: GapModel, chunk_width: int = 64, device: int = 0) -> int:
+    """sw_score_wavefront (align.hpp:166-229) on the intra-task kernel."""
+    lib = _cabi.load()
+    q, s, mat = _u8(query), _u8(subject), _mat(matrix)
+    out = C.c_int32(0)
+    dummy = np.zeros(1, np.uint8)
+    rc = lib.swb_score_pair(_ptr(q if len(q) else dummy, _u8p), len(q), _ptr(s if len(s) else dummy, _u8p), len(s),
+                            _ptr(mat, _i32p), gaps.open, gaps.extend, max(0, chunk_width), device, C.byref(out))
+    _raise(lib, rc)
+    return out.value
+
+
+def shard_assignment(lengths, length_threshold: int, shard_count: int) -> np.ndarray:
+    """The deterministic residue-balanced deal used by swb_db_create (host only, no GPU needed)."""
+    lib = _cabi.load()
+    lens = np.ascontiguousarray(np.asarray(lengths, dtype=np.uint32))
+    out = np.zeros(max(1, len(lens)), dtype=np.uint32)
+    rc = lib.swb_shard_assignment(_ptr(lens, _u32p), len(lens), int(length_threshold) & (2 ** 64 - 1), shard_count,
+                                  _ptr(out, _u32p))
+    _raise(lib, rc)
+    return out[:len(lens)]
+
+
+def measure_pipe_rates(device: int = 0, seconds: float = 1.0) -> dict:
+    lib = _cabi.load()
+    r = _cabi.SwbPipeRates()
+    _raise(lib, lib.swb_measure_pipe_rates(device, seconds, C.byref(r)))
+    return r.as_dict()
+
+
+class MultiGpuDatabase:
+    """One process, several GPUs (swb_mdb): shards + NCCL all-gather of the per-shard top-k."""
+
+    def __init__(self, codes, offsets, devices, length_threshold: int = 3000):
+        self._lib = _cabi.load()
+        self._h = C.c_void_p()
+        codes = _u8(codes)
+        offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+        devs = np.ascontiguousarray(np.asarray(devices, dtype=np.int32))
+        keep = codes if len(codes) else np.zeros(1, np.uint8)
+        rc = self._lib.swb_mdb_create_flat(_ptr(keep, _u8p), _ptr(offsets, _u64p), len(offsets) - 1,
+                                           int(length_threshold) & (2 ** 64 - 1), _ptr(devs, _i32p), len(devs),
+                                           C.byref(self._h))
+        _raise(self._lib, rc)
+
+    def close(self):
+        if self._h:
+            self._lib.swb_mdb_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search(self, query, matrix, gaps: GapModel, top_k: int = 10):
+        q, mat = _u8(query), _mat(matrix)
+        hits = (_cabi.SwbHit * max(1, top_k))()
+        n = C.c_uint32(0)
+        st = _cabi.SwbStats()
+        rc = self._lib.swb_mdb_search(self._h, _ptr(q, _u8p), len(q), _ptr(mat, _i32p), gaps.open, gaps.extend,
+                                      top_k, hits, C.byref(n), C.byref(st))
+        _raise(self._lib, rc)
+        idx = np.array([hits[i].db_index for i in range(n.value)], dtype=np.uint32)
+        sc = np.array([hits[i].score for i in range(n.value)], dtype=np.int32)
+        return idx, sc, st.as_dict()
