@@ -62,20 +62,20 @@ typedef struct swb_hit {
 
 /* Execution report.  The first three fields are SearchStats (scheduler.hpp:120-124). */
 typedef struct swb_stats {
-    uint64_t lane_scored;      /* sequences scored by the inter-task kernel                       */
-    uint64_t wavefront_scored; /* sequences scored by the intra-task kernel                       */
-    uint64_t chunks_claimed;   /* work units launched: interleaved groups + long sequences        */
+    uint64_t lane_scored;      /* sequences below the length threshold (inter-task pool)          */
+    uint64_t wavefront_scored; /* sequences at or above it (intra-task pool)                      */
+    uint64_t chunks_claimed;   /* work units handed out by the ticket counter                     */
     uint64_t rescored_i32;     /* sequences flagged by the int16 pass and re-run in int32         */
     uint64_t cells;            /* query_len x residues of this shard (GCUPS numerator)*/
     uint64_t padded_cells;     /* cells executed including row/column padding                     */
     uint32_t kernel_launches;  /* launches of this library's kernels during the call              */
     uint32_t reserved;
     float ms_total;            /* device time of the call (CUDA events on the search stream)      */
-    float ms_inter;            /* inter-task int16 kernel                                         */
-    float ms_intra;            /* intra-task kernel                                               */
-    float ms_rescore;          /* int32 re-run                                                    */
-    float ms_topk;             /* key build + top-k select                                        */
-    float ms_h2d_d2h;          /* query/profile upload + result download                          */
+    float ms_setup;            /* query/matrix upload, profile build, buffer clears               */
+    float ms_scan;             /* the packed-int16 tile-wavefront kernel over all groups          */
+    float ms_rescore;          /* flag collection + int32 re-run (or the whole scan in wide mode) */
+    float ms_topk;             /* key build + top-k select (or the score scatter)                 */
+    float ms_reserved;
 } swb_stats;
 
 typedef struct swb_db_info {

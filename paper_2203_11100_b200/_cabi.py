@@ -27,12 +27,12 @@ class SwbStats(C.Structure):
         ("lane_scored", C.c_uint64), ("wavefront_scored", C.c_uint64), ("chunks_claimed", C.c_uint64),
         ("rescored_i32", C.c_uint64), ("cells", C.c_uint64), ("padded_cells", C.c_uint64),
         ("kernel_launches", C.c_uint32), ("reserved", C.c_uint32),
-        ("ms_total", C.c_float), ("ms_inter", C.c_float), ("ms_intra", C.c_float),
-        ("ms_rescore", C.c_float), ("ms_topk", C.c_float), ("ms_h2d_d2h", C.c_float),
+        ("ms_total", C.c_float), ("ms_setup", C.c_float), ("ms_scan", C.c_float),
+        ("ms_rescore", C.c_float), ("ms_topk", C.c_float), ("ms_reserved", C.c_float),
     ]
 
     def as_dict(self):
-        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+        return {name: getattr(self, name) for name, _ in self._fields_ if "reserved" not in name}
 
 
 class SwbDbInfo(C.Structure):
@@ -45,7 +45,7 @@ class SwbDbInfo(C.Structure):
     ]
 
     def as_dict(self):
-        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+        return {name: getattr(self, name) for name, _ in self._fields_ if "reserved" not in name}
 
 
 class SwbPipeRates(C.Structure):
@@ -57,7 +57,7 @@ class SwbPipeRates(C.Structure):
     ]
 
     def as_dict(self):
-        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+        return {name: getattr(self, name) for name, _ in self._fields_ if "reserved" not in name}
 
 
 # name -> (restype, argtypes); every symbol include/swb200.h declares

@@ -1,9 +1,9 @@
 // cabi.cu -- the C-ABI of include/swb200.h: handles, orchestration, launches.
 //
 // Host flow of one search (replaces scheduler.hpp:188-244):
-//   validate -> upload query + matrix -> build_profile_kernel -> intra-task kernel (long pool)
-//   -> inter-task int16 kernel (short pool) -> int32 re-run of flagged lanes -> key build ->
-//   top-k select -> download k hits.
+//   validate -> upload query + matrix + unit table -> build_profile_kernel -> packed-int16
+//   tile-wavefront kernel over all groups -> collect + int32 re-run of lanes above the trust limit
+//   -> key build -> top-k select -> download k hits.
 // Everything runs on one stream per handle; no host synchronisation happens between the upload and
 // the final download.
 #include <cuda_runtime.h>
@@ -56,7 +56,7 @@ inline uint32_t pack16(int32_t v) {
     return h | (h << 16);
 }
 
-enum { EV_START = 0, EV_UP, EV_INTRA, EV_INTER, EV_RESCORE, EV_TOPK, EV_END, EV_COUNT };
+enum { EV_START = 0, EV_UP, EV_SCAN, EV_RESCORE, EV_TOPK, EV_END, EV_COUNT };
 
 struct QueryPlan {
     bool wide = false;        // int32 everywhere (matrix + open outside int8, or huge gaps)
@@ -77,28 +77,27 @@ struct swb_db {
     size_t smem_optin = 0;
     std::mutex mu;
     uint64_t device_bytes = 0;
+    bool force_intra = false;   // swb_score_pair: score with the intra-task kernel only
 
     // database (metadata stays on the host, bulk arrays live on the device only)
     PackedDb meta;
     uint32_t n_slots = 0;
-    uint32_t max_short_rows = 0;
-    uint64_t long_rows = 0;     // bytes of the long pool == border rows
-    uint8_t* d_short_codes = nullptr;
+    uint32_t max_rows = 0;      // padded rows of the longest group
+    uint8_t* d_codes = nullptr;
     GroupDesc* d_groups = nullptr;
     uint32_t* d_slot_index = nullptr;
     uint32_t* d_slot_len = nullptr;
-    uint8_t* d_long_codes = nullptr;
-    LongDesc* d_longs = nullptr;
 
     // work buffers
-    uint2 *d_border0 = nullptr, *d_border1 = nullptr;      // inter int16, database-shaped
-    uint2 *d_lborder0 = nullptr, *d_lborder1 = nullptr;    // intra, long-pool-shaped
-    uint2 *d_wborder0 = nullptr, *d_wborder1 = nullptr;    // int32 re-run, [rows][threads]
-    uint32_t wide_threads = 0;
+    uint2 *d_border0 = nullptr, *d_border1 = nullptr;      // wavefront kernel, database-shaped
+    uint2 *d_iborder0 = nullptr, *d_iborder1 = nullptr;    // intra kernel, [ctas][max_rows]
+    uint32_t intra_ctas = 0;
     int32_t* d_slot_scores = nullptr;
-    int32_t* d_long_scores = nullptr;
     uint32_t* d_flag_list = nullptr;
-    uint32_t* d_counters = nullptr;   // [0] work counter, [1] flag count
+    uint32_t* d_counters = nullptr;   // [0] ticket, [1] flag count
+    uint32_t* d_unit_start = nullptr;
+    uint32_t* d_progress = nullptr;
+    size_t progress_cap = 0;
     uint64_t* d_keys = nullptr;
     uint64_t* d_sel[2] = {nullptr, nullptr};
     size_t sel_cap = 0;
@@ -111,14 +110,16 @@ struct swb_db {
     uint8_t* d_query = nullptr;
     int32_t* d_matrix = nullptr;
     int8_t *d_prof8 = nullptr, *d_prof8i = nullptr;
-    int32_t *d_prof32 = nullptr, *d_prof32i = nullptr;
-    size_t prof8_cap = 0, prof8i_cap = 0, prof32_cap = 0, prof32i_cap = 0;
+    int32_t* d_prof32i = nullptr;
+    size_t prof8_cap = 0, prof8i_cap = 0, prof32i_cap = 0;
 
-    uint8_t* h_stage = nullptr;   // pinned: query + matrix up, keys down
+    uint8_t* h_stage = nullptr;   // pinned: matrix + query + unit table up, keys down
     size_t stage_cap = 0;
     uint32_t* h_counters = nullptr;   // pinned copy of d_counters
     cudaEvent_t ev[EV_COUNT] = {};
     uint32_t launches = 0;
+    uint32_t last_units = 0;
+    bool smem_attr_set = false;
 };
 
 namespace {
@@ -177,6 +178,16 @@ swb_status check_scoring_args(const uint8_t* query, uint32_t m, const int32_t* m
     return SWB_OK;
 }
 
+// Fraction of a warp's fair share of the search above which a group is split into a wavefront.
+double unit_budget_fraction() {
+    static const double f = [] {
+        const char* e = std::getenv("SWB200_UNIT_BUDGET");
+        const double v = e ? std::atof(e) : 0.0;
+        return v > 0.0 ? v : 0.75;
+    }();
+    return f;
+}
+
 QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext) {
     QueryPlan pl;
     pl.m = m;
@@ -184,14 +195,15 @@ QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t
     pl.ext = ext;
     int32_t lo = matrix[0], hi = matrix[0];
     for (int i = 1; i < 576; ++i) lo = std::min(lo, matrix[i]), hi = std::max(hi, matrix[i]);
+    // packed path: profile entries (matrix + open, and the pad entry `open`) must fit int8
     const bool fits8 = (lo + open >= -128) && (hi + open <= 127) && (open <= 127);
     pl.wide = !fits8;
     const int32_t top = std::max(hi, 0);
     pl.limit = 32767 - top;
-    const uint64_t reach = static_cast<uint64_t>(top) * std::min<uint64_t>(m, db->max_short_rows);
+    const uint64_t reach = static_cast<uint64_t>(top) * std::min<uint64_t>(m, db->meta.max_length);
     pl.may_overflow = reach > static_cast<uint64_t>(pl.limit);
 
-    // inter profile stride: columns padded to the 32-column tile, then to 16 (mod 128) bytes
+    // wavefront profile stride: columns padded to the 32-column tile, then to 16 (mod 128) bytes
     const uint32_t mpad = std::max<uint32_t>(32, (m + 31) / 32 * 32);
     pl.pstride = mpad + ((16 + 128 - (mpad % 128)) % 128);
 
@@ -214,39 +226,82 @@ QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t
 }
 
 template <int T, typename PT>
-void launch_intra(const IntraParams& ip, uint32_t warps, cudaStream_t s) {
-    intra_s32_kernel<T, PT><<<ip.n_long, warps * 32, 0, s>>>(ip);
+void launch_intra(const IntraParams& ip, uint32_t ctas, uint32_t warps, cudaStream_t s) {
+    intra_s32_kernel<T, PT><<<ctas, warps * 32, 0, s>>>(ip);
 }
 
 template <typename PT>
-void launch_intra_t(uint32_t t, const IntraParams& ip, uint32_t warps, cudaStream_t s) {
+void launch_intra_t(uint32_t t, const IntraParams& ip, uint32_t ctas, uint32_t warps, cudaStream_t s) {
     switch (t) {
-        case 4: launch_intra<4, PT>(ip, warps, s); break;
-        case 5: launch_intra<5, PT>(ip, warps, s); break;
-        case 6: launch_intra<6, PT>(ip, warps, s); break;
-        case 7: launch_intra<7, PT>(ip, warps, s); break;
-        default: launch_intra<8, PT>(ip, warps, s); break;
+        case 4: launch_intra<4, PT>(ip, ctas, warps, s); break;
+        case 5: launch_intra<5, PT>(ip, ctas, warps, s); break;
+        case 6: launch_intra<6, PT>(ip, ctas, warps, s); break;
+        case 7: launch_intra<7, PT>(ip, ctas, warps, s); break;
+        default: launch_intra<8, PT>(ip, ctas, warps, s); break;
     }
 }
 
-// Scores every local sequence; results land in d_slot_scores / d_long_scores.  Asynchronous.
+// Launch the int32 intra-task kernel over `list` (nullptr = every slot).
+swb_status run_intra(swb_db* db, const QueryPlan& pl, const uint32_t* list, cudaStream_t s) {
+    swb_status st;
+    if (!db->intra_ctas) {
+        // per-CTA border rows are only touched when the query needs more than one pass, but the
+        // allocation is sized once for the worst case
+        const uint64_t rows = std::max<uint32_t>(db->max_rows, 1);
+        uint64_t ctas = (512ull << 20) / (rows * 16);
+        ctas = std::min<uint64_t>(static_cast<uint64_t>(db->sm_count) * 8, std::max<uint64_t>(8, ctas));
+        ctas = std::min<uint64_t>(ctas, std::max<uint32_t>(db->n_slots, 1));
+        if ((st = dev_alloc(&db->d_iborder0, rows * ctas, &db->device_bytes)) != SWB_OK) return st;
+        if ((st = dev_alloc(&db->d_iborder1, rows * ctas, &db->device_bytes)) != SWB_OK) return st;
+        db->intra_ctas = static_cast<uint32_t>(ctas);
+    }
+    IntraParams ip{};
+    ip.codes = db->d_codes;
+    ip.groups = db->d_groups;
+    ip.slot_len = db->d_slot_len;
+    ip.list = list;
+    ip.list_count = db->d_counters + 1;
+    ip.n_slots = db->n_slots;
+    ip.profi = pl.wide ? static_cast<const void*>(db->d_prof32i) : static_cast<const void*>(db->d_prof8i);
+    ip.n_lane_tiles = pl.n_lane_tiles;
+    ip.n_passes = pl.intra_passes;
+    ip.border0 = db->d_iborder0;
+    ip.border1 = db->d_iborder1;
+    ip.border_rows = std::max<uint32_t>(db->max_rows, 1);
+    ip.slot_scores = db->d_slot_scores;
+    ip.open = pl.open;
+    ip.ext = pl.ext;
+    if (pl.wide) launch_intra_t<int32_t>(pl.intra_t, ip, db->intra_ctas, pl.intra_w, s);
+    else launch_intra_t<int8_t>(pl.intra_t, ip, db->intra_ctas, pl.intra_w, s);
+    ++db->launches;
+    return SWB_OK;
+}
+
+// Scores every local sequence; results land in d_slot_scores.  Asynchronous on db->stream.
 swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_t* matrix, int32_t open,
-                      int32_t ext, swb_stats* stats) {
+                      int32_t ext) {
     cudaStream_t s = db->stream;
     const QueryPlan pl = make_plan(db, m, matrix, open, ext);
     db->launches = 0;
+    db->last_units = 0;
     SWB_CUDA(cudaEventRecord(db->ev[EV_START], s));
+    SWB_CUDA(cudaMemsetAsync(db->d_slot_scores, 0, std::max<size_t>(db->n_slots, 1) * sizeof(int32_t), s));
+    SWB_CUDA(cudaMemsetAsync(db->d_counters, 0, 4 * sizeof(uint32_t), s));
 
     if (m == 0 || db->meta.n_local == 0) {
         // empty query: every score is 0 (align.hpp:45,100,172)
-        SWB_CUDA(cudaMemsetAsync(db->d_slot_scores, 0, std::max<size_t>(db->n_slots, 1) * sizeof(int32_t), s));
-        SWB_CUDA(cudaMemsetAsync(db->d_long_scores, 0, std::max<size_t>(db->meta.n_long, 1) * sizeof(int32_t), s));
         for (int e = EV_UP; e <= EV_RESCORE; ++e) SWB_CUDA(cudaEventRecord(db->ev[e], s));
         return SWB_OK;
     }
 
-    // ---- upload query + matrix, build profiles -------------------------------------------------
-    swb_status st = ensure_stage(db, m + 576 * sizeof(int32_t) + 64);
+    const uint32_t n_groups = static_cast<uint32_t>(db->meta.groups.size());
+    const bool packed = !pl.wide && !db->force_intra;
+
+    // ---- stage matrix + query (+ the unit table of the wavefront kernel) and upload -----------------
+    const size_t off_query = 576 * sizeof(int32_t);
+    const size_t off_units = (off_query + m + 15) & ~size_t(15);
+    const size_t stage_bytes = off_units + (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t);
+    swb_status st = ensure_stage(db, stage_bytes);
     if (st != SWB_OK) return st;
     if (m > db->query_cap) {
         if (db->d_query) cudaFree(db->d_query);
@@ -255,10 +310,32 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         if (st != SWB_OK) return st;
         db->query_cap = m * 2;
     }
-    std::memcpy(db->h_stage, matrix, 576 * sizeof(int32_t));
-    std::memcpy(db->h_stage + 576 * sizeof(int32_t), query, m);
-    SWB_CUDA(cudaMemcpyAsync(db->d_matrix, db->h_stage, 576 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    SWB_CUDA(cudaMemcpyAsync(db->d_query, db->h_stage + 576 * sizeof(int32_t), m, cudaMemcpyHostToDevice, s));
+    std::memcpy(db->h_stage, matrix, off_query);
+    std::memcpy(db->h_stage + off_query, query, m);
+    const uint32_t n_tiles = (m + kInterTile - 1) / kInterTile;
+    uint32_t n_units = 0;
+    if (packed) {
+        // Unit policy: a group whose whole (rows x tiles) sweep exceeds the budget -- a fraction of one
+        // warp's fair share of the search -- is split into one unit per tile (a wavefront of warps);
+        // everything else is a single unit scored end to end by one warp.
+        uint32_t* us = reinterpret_cast<uint32_t*>(db->h_stage + off_units);
+        const uint64_t total_row_tiles = db->meta.padded_rows * n_tiles;
+        const uint64_t warps = static_cast<uint64_t>(db->sm_count) * (kInterThreads / 32);
+        const uint64_t budget = std::max<uint64_t>(4096, static_cast<uint64_t>(unit_budget_fraction() * total_row_tiles / warps));
+        for (uint32_t g = 0; g < n_groups; ++g) {
+            us[g] = n_units;
+            const uint64_t work = static_cast<uint64_t>(db->meta.groups[g].n_chunks) * kRowsPerChunk * n_tiles;
+            n_units += (work > budget && n_tiles > 1) ? n_tiles : 1;
+        }
+        us[n_groups] = n_units;
+        SWB_CUDA(cudaMemcpyAsync(db->d_unit_start, us, (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, s));
+        if ((st = ensure_dev(&db->d_progress, &db->progress_cap, n_units, &db->device_bytes)) != SWB_OK) return st;
+        SWB_CUDA(cudaMemsetAsync(db->d_progress, 0, static_cast<size_t>(n_units) * sizeof(uint32_t), s));
+        db->last_units = n_units;
+    }
+    SWB_CUDA(cudaMemcpyAsync(db->d_matrix, db->h_stage, off_query, cudaMemcpyHostToDevice, s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_query, db->h_stage + off_query, m, cudaMemcpyHostToDevice, s));
 
     const size_t prof_elems = static_cast<size_t>(kProfRows) * pl.pstride;
     const size_t profi_elems = static_cast<size_t>(kProfRows) * pl.n_lane_tiles * 8;
@@ -276,103 +353,59 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         pp.prof8 = db->d_prof8;
         pp.prof8i = db->d_prof8i;
     } else {
-        if ((st = ensure_dev(&db->d_prof32, &db->prof32_cap, prof_elems, &db->device_bytes)) != SWB_OK) return st;
         if ((st = ensure_dev(&db->d_prof32i, &db->prof32i_cap, profi_elems, &db->device_bytes)) != SWB_OK) return st;
-        pp.prof32 = db->d_prof32;
         pp.prof32i = db->d_prof32i;
     }
     build_profile_kernel<<<64, 256, 0, s>>>(pp);
     ++db->launches;
-    SWB_CUDA(cudaMemsetAsync(db->d_counters, 0, 4 * sizeof(uint32_t), s));
     SWB_CUDA(cudaEventRecord(db->ev[EV_UP], s));
 
-    // ---- long pool: intra-task kernel ------------------------------------------------------------
-    if (db->meta.n_long) {
-        IntraParams ip{};
-        ip.codes = db->d_long_codes;
-        ip.longs = db->d_longs;
-        ip.n_long = db->meta.n_long;
-        ip.profi = pl.wide ? static_cast<const void*>(db->d_prof32i) : static_cast<const void*>(db->d_prof8i);
-        ip.n_lane_tiles = pl.n_lane_tiles;
-        ip.n_passes = pl.intra_passes;
-        ip.border0 = db->d_lborder0;
-        ip.border1 = db->d_lborder1;
-        ip.long_scores = db->d_long_scores;
-        ip.open = open;
-        ip.ext = ext;
-        if (pl.wide) launch_intra_t<int32_t>(pl.intra_t, ip, pl.intra_w, s);
-        else launch_intra_t<int8_t>(pl.intra_t, ip, pl.intra_w, s);
-        ++db->launches;
-    }
-    SWB_CUDA(cudaEventRecord(db->ev[EV_INTRA], s));
-
-    // ---- short pool: inter-task kernels ------------------------------------------------------------
-    const uint32_t n_groups = static_cast<uint32_t>(db->meta.groups.size());
-    bool need_wide_pass = false;
-    if (n_groups && !pl.wide) {
-        InterParams ip{};
-        ip.codes = reinterpret_cast<const uint4*>(db->d_short_codes);
-        ip.groups = db->d_groups;
-        ip.n_groups = n_groups;
-        ip.prof8 = db->d_prof8;
-        ip.pstride = pl.pstride;
-        ip.n_tiles = (m + kInterTile - 1) / kInterTile;
-        ip.border0 = db->d_border0;
-        ip.border1 = db->d_border1;
-        ip.slot_scores = db->d_slot_scores;
-        ip.flag_list = db->d_flag_list;
-        ip.flag_count = db->d_counters + 1;
-        ip.work_counter = db->d_counters;
-        ip.neg_open2 = pack16(-open);
-        ip.neg_ext2 = pack16(-ext);
-        ip.limit = pl.limit;
+    // ---- the scan ------------------------------------------------------------------------------------
+    if (packed) {
+        WaveParams wp{};
+        wp.codes = reinterpret_cast<const uint4*>(db->d_codes);
+        wp.groups = db->d_groups;
+        wp.n_groups = n_groups;
+        wp.unit_start = db->d_unit_start;
+        wp.n_units = n_units;
+        wp.prof8 = db->d_prof8;
+        wp.pstride = pl.pstride;
+        wp.n_tiles = n_tiles;
+        wp.border0 = db->d_border0;
+        wp.border1 = db->d_border1;
+        wp.slot_scores = db->d_slot_scores;
+        wp.progress = db->d_progress;
+        wp.ticket = db->d_counters;
+        wp.neg_open2 = pack16(-open);
+        wp.neg_ext2 = pack16(-ext);
         const size_t smem = prof_elems;
         const uint32_t warps_per_cta = kInterThreads / 32;
-        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(db->sm_count, (n_groups + warps_per_cta - 1) / warps_per_cta));
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(db->sm_count, (n_units + warps_per_cta - 1) / warps_per_cta));
         if (smem <= db->smem_optin) {
-            SWB_CUDA(cudaFuncSetAttribute(inter_s16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
-            inter_s16_kernel<true><<<grid, kInterThreads, smem, s>>>(ip);
+            if (!db->smem_attr_set) {
+                SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(db->smem_optin)));
+                db->smem_attr_set = true;
+            }
+            wavefront_s16_kernel<true><<<grid, kInterThreads, smem, s>>>(wp);
         } else {
-            inter_s16_kernel<false><<<grid, kInterThreads, 0, s>>>(ip);
+            wavefront_s16_kernel<false><<<grid, kInterThreads, 0, s>>>(wp);
         }
         ++db->launches;
-        need_wide_pass = pl.may_overflow;
     }
-    SWB_CUDA(cudaEventRecord(db->ev[EV_INTER], s));
+    SWB_CUDA(cudaEventRecord(db->ev[EV_SCAN], s));
 
-    if (n_groups && (pl.wide || need_wide_pass)) {
-        if (!db->d_wborder0) {
-            const uint64_t rows = std::max<uint32_t>(db->max_short_rows, 1);
-            uint64_t threads = (256ull << 20) / (rows * 16);
-            threads = std::min<uint64_t>(8192, std::max<uint64_t>(128, threads / 128 * 128));
-            db->wide_threads = static_cast<uint32_t>(threads);
-            if ((st = dev_alloc(&db->d_wborder0, rows * threads, &db->device_bytes)) != SWB_OK) return st;
-            if ((st = dev_alloc(&db->d_wborder1, rows * threads, &db->device_bytes)) != SWB_OK) return st;
-        }
-        WideParams wp{};
-        wp.codes = db->d_short_codes;
-        wp.groups = db->d_groups;
-        wp.slot_len = db->d_slot_len;
-        wp.list = pl.wide ? nullptr : db->d_flag_list;
-        wp.list_count = db->d_counters + 1;
-        wp.n_slots = db->n_slots;
-        wp.prof = pl.wide ? static_cast<const void*>(db->d_prof32) : static_cast<const void*>(db->d_prof8);
-        wp.pstride = pl.pstride;
-        wp.n_tiles = (m + kWideTile - 1) / kWideTile;
-        wp.border0 = db->d_wborder0;
-        wp.border1 = db->d_wborder1;
-        wp.slot_scores = db->d_slot_scores;
-        wp.open = open;
-        wp.ext = ext;
-        const uint32_t blocks = db->wide_threads / 128;
-        if (pl.wide) inter_s32_kernel<int32_t><<<blocks, 128, 0, s>>>(wp);
-        else inter_s32_kernel<int8_t><<<blocks, 128, 0, s>>>(wp);
+    // ---- int32: re-run of lanes above the trust limit, or everything when the packed path is out ----
+    if (!packed) {
+        if ((st = run_intra(db, pl, nullptr, s)) != SWB_OK) return st;
+    } else if (pl.may_overflow) {
+        collect_flagged_kernel<<<std::max(1u, std::min(1024u, (db->n_slots + 255) / 256)), 256, 0, s>>>(
+            db->d_slot_scores, db->n_slots, pl.limit, db->d_flag_list, db->d_counters + 1);
         ++db->launches;
+        if ((st = run_intra(db, pl, db->d_flag_list, s)) != SWB_OK) return st;
     }
     SWB_CUDA(cudaEventRecord(db->ev[EV_RESCORE], s));
     SWB_CUDA(cudaGetLastError());
-    (void)stats;
     return SWB_OK;
 }
 
@@ -432,21 +465,20 @@ void fill_stats(swb_db* db, uint32_t m, swb_stats* st) {
     std::memset(st, 0, sizeof(*st));
     st->lane_scored = db->meta.n_short;
     st->wavefront_scored = db->meta.n_long;
-    st->chunks_claimed = db->meta.groups.size() + db->meta.n_long;
+    st->chunks_claimed = db->last_units ? db->last_units : db->meta.n_local;
+    st->rescored_i32 = db->h_counters ? db->h_counters[1] : 0;
     st->cells = static_cast<uint64_t>(m) * db->meta.residues;
     const uint64_t mpad = (static_cast<uint64_t>(m) + kInterTile - 1) / kInterTile * kInterTile;
-    st->padded_cells = mpad * db->meta.padded_rows * kGroupSeqs + static_cast<uint64_t>(m) * (db->meta.residues - db->meta.short_residues);
+    st->padded_cells = mpad * db->meta.padded_rows * kGroupSeqs;
     st->kernel_launches = db->launches;
-    st->rescored_i32 = db->h_counters ? db->h_counters[1] : 0;
     auto span = [&](int a, int b) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, db->ev[a], db->ev[b]);
         return ms;
     };
-    st->ms_h2d_d2h = span(EV_START, EV_UP);
-    st->ms_intra = span(EV_UP, EV_INTRA);
-    st->ms_inter = span(EV_INTRA, EV_INTER);
-    st->ms_rescore = span(EV_INTER, EV_RESCORE);
+    st->ms_setup = span(EV_START, EV_UP);
+    st->ms_scan = span(EV_UP, EV_SCAN);
+    st->ms_rescore = span(EV_SCAN, EV_RESCORE);
     st->ms_topk = span(EV_RESCORE, EV_TOPK);
     st->ms_total = span(EV_START, EV_END);
 }
@@ -454,36 +486,29 @@ void fill_stats(swb_db* db, uint32_t m, swb_stats* st) {
 swb_status upload_db(swb_db* db) {
     PackedDb& m = db->meta;
     db->n_slots = static_cast<uint32_t>(m.groups.size() * kGroupSeqs);
-    db->max_short_rows = m.groups.empty() ? 0 : m.groups[0].n_chunks * kRowsPerChunk;
-    db->long_rows = m.long_codes.size();
+    db->max_rows = m.groups.empty() ? 0 : m.groups[0].n_chunks * kRowsPerChunk;
     uint64_t* tally = &db->device_bytes;
     swb_status st;
 #define ALLOC_COPY(dptr, vec)                                                                        \
     if ((st = dev_alloc(&(dptr), (vec).size(), tally)) != SWB_OK) return st;                         \
     if (!(vec).empty())                                                                              \
         SWB_CUDA(cudaMemcpy((dptr), (vec).data(), (vec).size() * sizeof((vec)[0]), cudaMemcpyHostToDevice));
-    ALLOC_COPY(db->d_short_codes, m.short_codes);
+    ALLOC_COPY(db->d_codes, m.codes);
     ALLOC_COPY(db->d_groups, m.groups);
-    ALLOC_COPY(db->d_slot_index, m.short_index);
-    ALLOC_COPY(db->d_slot_len, m.short_len);
-    ALLOC_COPY(db->d_long_codes, m.long_codes);
-    ALLOC_COPY(db->d_longs, m.longs);
+    ALLOC_COPY(db->d_slot_index, m.slot_index);
+    ALLOC_COPY(db->d_slot_len, m.slot_len);
 #undef ALLOC_COPY
     const size_t brows = static_cast<size_t>(m.total_chunks) * kRowsPerChunk * 32 + 64;
     if ((st = dev_alloc(&db->d_border0, brows, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_border1, brows, tally)) != SWB_OK) return st;
-    if ((st = dev_alloc(&db->d_lborder0, db->long_rows + 16, tally)) != SWB_OK) return st;
-    if ((st = dev_alloc(&db->d_lborder1, db->long_rows + 16, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_slot_scores, db->n_slots, tally)) != SWB_OK) return st;
-    if ((st = dev_alloc(&db->d_long_scores, m.n_long, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_flag_list, db->n_slots, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_counters, 4, tally)) != SWB_OK) return st;
-    if ((st = dev_alloc(&db->d_keys, static_cast<size_t>(db->n_slots) + m.n_long, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_unit_start, m.groups.size() + 1, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_keys, db->n_slots, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_matrix, 576, tally)) != SWB_OK) return st;
-    SWB_CUDA(cudaMemset(db->d_slot_scores, 0, std::max<size_t>(db->n_slots, 1) * sizeof(int32_t)));
-    // the bulk host copies are no longer needed
-    std::vector<uint8_t>().swap(m.short_codes);
-    std::vector<uint8_t>().swap(m.long_codes);
+    // the bulk host copy is no longer needed
+    std::vector<uint8_t>().swap(m.codes);
     return SWB_OK;
 }
 
@@ -544,19 +569,16 @@ swb_status create_from(const SeqSource& src, uint64_t threshold, int32_t device,
 }
 
 swb_status search_keys_locked(swb_db* db, const uint8_t* query, uint32_t m, const int32_t* matrix,
-                              int32_t open, int32_t ext, uint32_t top_k, const uint64_t** d_out,
-                              swb_stats* stats) {
-    swb_status st = score_core(db, query, m, matrix, open, ext, stats);
+                              int32_t open, int32_t ext, uint32_t top_k, const uint64_t** d_out) {
+    swb_status st = score_core(db, query, m, matrix, open, ext);
     if (st != SWB_OK) return st;
     cudaStream_t s = db->stream;
-    const uint32_t n_keys = db->n_slots + db->meta.n_long;
-    if (n_keys) {
-        build_keys_kernel<<<std::max(1u, std::min(1024u, (n_keys + 255) / 256)), 256, 0, s>>>(
-            db->d_slot_scores, db->d_slot_index, db->n_slots, db->d_long_scores, db->d_longs, db->meta.n_long,
-            db->d_keys);
+    if (db->n_slots) {
+        build_keys_kernel<<<std::max(1u, std::min(1024u, (db->n_slots + 255) / 256)), 256, 0, s>>>(
+            db->d_slot_scores, db->d_slot_index, db->n_slots, db->d_keys);
         ++db->launches;
     }
-    st = select_topk(db, db->d_keys, n_keys, top_k, d_out);
+    st = select_topk(db, db->d_keys, db->n_slots, top_k, d_out);
     if (st != SWB_OK) return st;
     SWB_CUDA(cudaEventRecord(db->ev[EV_TOPK], s));
     return SWB_OK;
@@ -610,12 +632,11 @@ void swb_db_destroy(swb_db* db) {
     {
         DeviceGuard guard(db->device);
         if (db->own_stream) cudaStreamSynchronize(db->own_stream);
-        void* ptrs[] = {db->d_short_codes, db->d_groups,      db->d_slot_index, db->d_slot_len,  db->d_long_codes,
-                        db->d_longs,       db->d_border0,     db->d_border1,    db->d_lborder0,  db->d_lborder1,
-                        db->d_wborder0,    db->d_wborder1,    db->d_slot_scores, db->d_long_scores, db->d_flag_list,
-                        db->d_counters,    db->d_keys,        db->d_sel[0],     db->d_sel[1],    db->d_sort,
-                        db->d_all_scores,  db->d_query,       db->d_matrix,     db->d_prof8,     db->d_prof8i,
-                        db->d_prof32,      db->d_prof32i};
+        void* ptrs[] = {db->d_codes,      db->d_groups,   db->d_slot_index, db->d_slot_len,    db->d_border0,
+                        db->d_border1,    db->d_iborder0, db->d_iborder1,   db->d_slot_scores, db->d_flag_list,
+                        db->d_counters,   db->d_unit_start, db->d_progress, db->d_keys,        db->d_sel[0],
+                        db->d_sel[1],     db->d_sort,     db->d_all_scores, db->d_query,       db->d_matrix,
+                        db->d_prof8,      db->d_prof8i,   db->d_prof32i};
         for (void* p : ptrs)
             if (p) cudaFree(p);
         if (db->h_stage) cudaFreeHost(db->h_stage);
@@ -639,7 +660,7 @@ swb_status swb_db_info_get(const swb_db* db, swb_db_info* info) {
     info->shard_rank = db->meta.shard_rank;
     info->shard_count = db->meta.shard_count;
     info->residues = db->meta.residues;
-    info->padded_residues = db->meta.padded_rows * kGroupSeqs + db->long_rows;
+    info->padded_residues = db->meta.padded_rows * kGroupSeqs;
     info->device_bytes = db->device_bytes;
     info->length_threshold = db->meta.length_threshold;
     info->device = db->device;
@@ -664,10 +685,10 @@ swb_status swb_search_keys(swb_db* db, const uint8_t* query, uint32_t query_len,
     std::lock_guard<std::mutex> lock(db->mu);
     DeviceGuard guard(db->device);
     // never select more than the shard holds (plus zero padding up to top_k on the host side)
-    const uint64_t n_keys = static_cast<uint64_t>(db->n_slots) + db->meta.n_long;
+    const uint64_t n_keys = db->meta.n_local;
     const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint64_t>(n_keys, 1)));
     const uint64_t* d_top = nullptr;
-    st = search_keys_locked(db, query, query_len, matrix, gap_open, gap_extend, k_eff, &d_top, stats);
+    st = search_keys_locked(db, query, query_len, matrix, gap_open, gap_extend, k_eff, &d_top);
     if (st != SWB_OK) return st;
     cudaStream_t s = db->stream;
     if (host_keys) {
@@ -693,7 +714,7 @@ swb_status swb_search(swb_db* db, const uint8_t* query, uint32_t query_len, cons
     if (!hits || !n_hits) return fail(SWB_ERR_INVALID, "hits/n_hits are null");
     if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
     if (!db) return fail(SWB_ERR_INVALID, "db is null");
-    const uint64_t n_keys = static_cast<uint64_t>(db->n_slots) + db->meta.n_long;
+    const uint64_t n_keys = db->meta.n_local;
     const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint64_t>(n_keys, 1)));
     std::vector<uint64_t> keys(k_eff);
     swb_status st = swb_search_keys(db, query, query_len, matrix, gap_open, gap_extend, k_eff, keys.data(), nullptr, stats);
@@ -716,7 +737,7 @@ swb_status swb_score_all(swb_db* db, const uint8_t* query, uint32_t query_len, c
     if (st != SWB_OK) return st;
     std::lock_guard<std::mutex> lock(db->mu);
     DeviceGuard guard(db->device);
-    st = score_core(db, query, query_len, matrix, gap_open, gap_extend, stats);
+    st = score_core(db, query, query_len, matrix, gap_open, gap_extend);
     if (st != SWB_OK) return st;
     cudaStream_t s = db->stream;
     const uint32_t n_total = db->meta.n_total;
@@ -725,11 +746,9 @@ swb_status swb_score_all(swb_db* db, const uint8_t* query, uint32_t query_len, c
     // entries of other shards must stay untouched: stage the caller's values first
     SWB_CUDA(cudaMemcpyAsync(db->d_all_scores, scores, static_cast<size_t>(n_total) * sizeof(int32_t),
                              cudaMemcpyHostToDevice, s));
-    const uint32_t total = db->n_slots + db->meta.n_long;
-    if (total) {
-        scatter_scores_kernel<<<std::max(1u, std::min(1024u, (total + 255) / 256)), 256, 0, s>>>(
-            db->d_slot_scores, db->d_slot_index, db->n_slots, db->d_long_scores, db->d_longs, db->meta.n_long,
-            db->d_all_scores);
+    if (db->n_slots) {
+        scatter_scores_kernel<<<std::max(1u, std::min(1024u, (db->n_slots + 255) / 256)), 256, 0, s>>>(
+            db->d_slot_scores, db->d_slot_index, db->n_slots, db->d_all_scores);
         ++db->launches;
     }
     SWB_CUDA(cudaEventRecord(db->ev[EV_TOPK], s));
@@ -848,9 +867,11 @@ swb_status swb_score_pair(const uint8_t* query, uint32_t query_len, const uint8_
     swb_db* db = nullptr;
     const uint8_t* ptrs[1] = {subject};
     const uint32_t ls[1] = {subject_len};
-    // threshold = 0: the sequence is routed to the intra-task kernel (scheduler.hpp:59-62)
+    // threshold = 0 routes the sequence to the intra-task pool (scheduler.hpp:59-62); force_intra makes
+    // the warp-shuffle wavefront kernel score it (one CTA for the one pair)
     st = swb_db_create(ptrs, ls, 1, 0, device, 0, 1, &db);
     if (st != SWB_OK) return st;
+    db->force_intra = true;
     int32_t out[1] = {0};
     st = swb_score_all(db, query, query_len, matrix, gap_open, gap_extend, out, nullptr);
     const std::string keep = g_error;

@@ -30,7 +30,6 @@ namespace swb {
 constexpr int kProfRows = 25;        // 24 symbols + the pad row
 constexpr int kInterTile = 32;       // query columns held in registers per pass (inter-task)
 constexpr int kInterThreads = 512;   // persistent CTA: 16 warps, one per SMSP x4
-constexpr int kWideTile = 16;        // query columns per pass in the int32 re-run kernel
 constexpr int kIntraDelta = 64;      // step offset between neighbouring warps of an intra-task CTA
 constexpr int kIntraRing = 128;      // rows of border ring buffer between neighbouring warps
 constexpr int kIntraMaxWarps = 8;
@@ -86,42 +85,67 @@ __global__ void build_profile_kernel(ProfileParams p) {
 }
 
 // ------------------------------------------------------------------------------------------------
-// Inter-task kernel, packed int16 (the hot kernel).
+// The hot kernel: packed-int16 DPX tile-wavefront over interleaved groups.
 //
-// One warp owns one interleaved group of 64 sequences at a time (claimed from a global counter in
-// descending-length order); each thread carries two sequences in the two int16 halves of every
-// DPX word.  The query is swept in tiles of 32 columns held in registers (Hm, F per column);
-// between tiles the last column (Hm, E) of every row goes through a database-shaped border array
-// in HBM/L2 (8 bytes per row per thread, coalesced, double-buffered).  The int8 profile lives in
-// shared memory with a row stride of 16 (mod 128) bytes so that the 25 rows spread over the banks.
+// Work decomposition.  A group (64 sequences, R padded rows) times the query's n_tiles tiles of 32
+// columns is cut into units of consecutive tiles: tiles_per_unit = clamp(unit_target / R, 1,
+// n_tiles), so short groups are one unit (pure inter-task: one warp scores 64 sequences end to
+// end) while a long group becomes up to n_tiles units that different warps -- on any SM -- work on
+// at the same time, each one tile (stripe) behind its left neighbour: the anti-diagonal wavefront
+// of the reference's intra-task kernel (align.hpp:194-226) at warp granularity.  Units are handed
+// out by one global ticket counter in (group, tile) order with groups sorted longest first, so a
+// unit's left neighbour always holds an earlier ticket and is already running: waiting on it
+// cannot deadlock, and the longest groups start first (LPT).
 //
-// Exactness: additions wrap (VIADD.16x2 / VIADDMNMX have no saturation), so a lane is trusted only
-// if its best never exceeded limit = 32767 - max(matrix); H grows by at most max(matrix) per
-// step, hence no wrap can precede a value above the limit.  Lanes above the limit are appended to
-// flag_list and re-run by the int32 kernel: the reference's contract for saturated lanes
+// Data flow.  Each thread carries two sequences in the int16 halves of every DPX word and keeps
+// Hm and F of its 32 columns in registers.  The (Hm, E) of a tile's last column goes, row by row,
+// through a database-shaped border array (8 B per row per thread, coalesced, double-buffered by
+// tile parity, L2-resident between neighbouring units).  A unit publishes the rows completed in
+// its last tile after every chunk of 8 rows (fence + store); the unit to its right polls that
+// counter before the chunk's first border load.  Border loads bypass L1 (ld.global.cg) because the
+// producer may sit on another SM.  The int8 profile lives in shared memory with a row stride of
+// 16 (mod 128) bytes so that the 25 rows spread over the banks.
+//
+// Exactness.  Additions wrap (VIADD.16x2 / VIADDMNMX do not saturate), so a lane is trusted only
+// if its best never exceeded limit = 32767 - max(matrix): H grows by at most max(matrix) per step,
+// hence no wrap can precede a value above the limit.  Scores above the limit are re-run in int32
+// by the intra-task kernel below -- the reference's contract for saturated lanes
 // (align.hpp:149-153).
 // ------------------------------------------------------------------------------------------------
-struct InterParams {
+struct WaveParams {
     const uint4* codes;
     const GroupDesc* groups;
     uint32_t n_groups;
+    const uint32_t* unit_start;   // [n_groups + 1] first unit of each group
+    uint32_t n_units;
     const int8_t* prof8;
     uint32_t pstride;
-    uint32_t n_tiles;        // ceil(m / 32)
+    uint32_t n_tiles;             // ceil(m / 32)
     uint2* border0;
     uint2* border1;
-    int32_t* slot_scores;    // [n_groups*64]
-    uint32_t* flag_list;
-    uint32_t* flag_count;
-    uint32_t* work_counter;
-    uint32_t neg_open2;      // (-open, -open) packed
-    uint32_t neg_ext2;       // (-extend, -extend) packed
-    int32_t limit;
-    int32_t prof_in_smem;
+    int32_t* slot_scores;         // [n_groups*64], zeroed per search, updated with atomicMax
+    uint32_t* progress;           // [n_units], zeroed per search
+    uint32_t* ticket;
+    uint32_t neg_open2;           // (-open, -open) packed
+    uint32_t neg_ext2;            // (-extend, -extend) packed
 };
 
+// A group is either one unit (all tiles, one warp) or n_tiles units (one tile each, a wavefront of
+// cooperating warps); the host decides per search (unit_budget in cabi.cu) and the kernel reads the
+// decision back from unit_start.
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <bool kSmemProfile>
-__global__ void __launch_bounds__(kInterThreads, 1) inter_s16_kernel(InterParams p) {
+__global__ void __launch_bounds__(kInterThreads, 1) wavefront_s16_kernel(WaveParams p) {
     constexpr int T = kInterTile;
     extern __shared__ __align__(16) uint8_t smem_prof[];
 
@@ -141,18 +165,36 @@ __global__ void __launch_bounds__(kInterThreads, 1) inter_s16_kernel(InterParams
     const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
 
     for (;;) {
-        uint32_t g = 0;
-        if (lane == 0) g = atomicAdd(p.work_counter, 1u);
-        g = __shfl_sync(0xffffffffu, g, 0);
-        if (g >= p.n_groups) break;
+        uint32_t u = 0;
+        if (lane == 0) u = atomicAdd(p.ticket, 1u);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= p.n_units) break;
+
+        // group of this unit: largest g with unit_start[g] <= u
+        uint32_t lo = 0, hi = p.n_groups;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(p.unit_start + mid) <= u) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t g = lo;
         const GroupDesc gd = p.groups[g];
+        const uint32_t u0 = __ldg(p.unit_start + g);
+        const bool split = __ldg(p.unit_start + g + 1) - u0 > 1;
+        const uint32_t t0 = split ? u - u0 : 0;
+        const uint32_t t1 = split ? t0 + 1 : p.n_tiles;
+        const uint32_t* dep = t0 > 0 ? p.progress + (u - 1) : nullptr;
+        uint32_t* pub = t1 < p.n_tiles ? p.progress + u : nullptr;
+
         const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
         const size_t brow0 = static_cast<size_t>(gd.chunk_base) * kRowsPerChunk * 32 + lane;
         uint32_t best = 0;
 
-        for (uint32_t tile = 0; tile < p.n_tiles; ++tile) {
+        for (uint32_t tile = t0; tile < t1; ++tile) {
             const int8_t* ptile = prof + tile * T;
             const bool first = tile == 0, last = tile + 1 == p.n_tiles;
+            const bool wait = dep != nullptr && tile == t0;
+            const bool publish = pub != nullptr && tile + 1 == t1;
             const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + brow0;
             uint2* bout = ((tile & 1) ? p.border1 : p.border0) + brow0;
 
@@ -160,14 +202,20 @@ __global__ void __launch_bounds__(kInterThreads, 1) inter_s16_kernel(InterParams
 #pragma unroll
             for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
             uint32_t diag_in = NO;
-
-            uint4 cw = gd.n_chunks ? gcodes[0] : make_uint4(0, 0, 0, 0);
-            uint2 bnext = make_uint2(NO, NO);
-            if (!first && gd.n_chunks) bnext = bin[0];
+            uint4 cw = gd.n_chunks ? __ldg(gcodes) : make_uint4(0, 0, 0, 0);
 
             for (uint32_t chunk = 0; chunk < gd.n_chunks; ++chunk) {
                 const uint4 cur = cw;
-                if (chunk + 1 < gd.n_chunks) cw = gcodes[static_cast<size_t>(chunk + 1) * 32];
+                if (chunk + 1 < gd.n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
+                const size_t row0 = static_cast<size_t>(chunk) * kRowsPerChunk;
+                if (wait) {
+                    const uint32_t need = static_cast<uint32_t>(row0) + kRowsPerChunk;
+                    if (lane == 0)
+                        while (ld_acquire(dep) < need) __nanosleep(40);
+                    __syncwarp();
+                }
+                uint2 bnext = make_uint2(NO, NO);
+                if (!first) bnext = __ldcg(bin + row0 * 32);
 #pragma unroll
                 for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
                     const uint32_t wa = r < 4 ? cur.x : cur.y;
@@ -183,14 +231,11 @@ __global__ void __launch_bounds__(kInterThreads, 1) inter_s16_kernel(InterParams
                         wA[4 * i] = va.x, wA[4 * i + 1] = va.y, wA[4 * i + 2] = va.z, wA[4 * i + 3] = va.w;
                         wB[4 * i] = vb.x, wB[4 * i + 1] = vb.y, wB[4 * i + 2] = vb.z, wB[4 * i + 3] = vb.w;
                     }
-                    const size_t row = static_cast<size_t>(chunk) * kRowsPerChunk + r;
+                    const size_t row = row0 + r;
                     const uint2 bi = bnext;
-                    if (!first) {
-                        // prefetch the next row's inbound border (rows are padded to whole chunks,
-                        // one extra row is read only inside the group's own region or the slack)
-                        const size_t nrow = row + 1;
-                        if (nrow < static_cast<size_t>(gd.n_chunks) * kRowsPerChunk) bnext = bin[nrow * 32];
-                    }
+                    // the next row's inbound border, within this chunk only: the rows of the next
+                    // chunk may not have been published yet
+                    if (!first && r + 1 < static_cast<int>(kRowsPerChunk)) bnext = __ldcg(bin + (row + 1) * 32);
                     uint32_t hl = bi.x;   // Hm of the column left of the tile, this row
                     uint32_t E = bi.y;
                     uint32_t diag = diag_in;
@@ -202,14 +247,14 @@ __global__ void __launch_bounds__(kInterThreads, 1) inter_s16_kernel(InterParams
                         // cell k
                         E = __viaddmax_s16x2(E, NE, hl);
                         F[k] = __viaddmax_s16x2(F[k], NE, Hm[k]);
-                        uint32_t h0 = __vimax3_s16x2_relu(__vadd2(diag, s0), E, F[k]);
+                        const uint32_t h0 = __vimax3_s16x2_relu(__vadd2(diag, s0), E, F[k]);
                         diag = Hm[k];
                         hl = __vadd2(h0, NO);
                         Hm[k] = hl;
                         // cell k+1
                         E = __viaddmax_s16x2(E, NE, hl);
                         F[k + 1] = __viaddmax_s16x2(F[k + 1], NE, Hm[k + 1]);
-                        uint32_t h1 = __vimax3_s16x2_relu(__vadd2(diag, s1), E, F[k + 1]);
+                        const uint32_t h1 = __vimax3_s16x2_relu(__vadd2(diag, s1), E, F[k + 1]);
                         diag = Hm[k + 1];
                         hl = __vadd2(h1, NO);
                         Hm[k + 1] = hl;
@@ -217,90 +262,147 @@ __global__ void __launch_bounds__(kInterThreads, 1) inter_s16_kernel(InterParams
                     }
                     if (!last) bout[row * 32] = make_uint2(hl, E);
                 }
+                if (publish) {
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence();
+                        st_release(pub, static_cast<uint32_t>(row0) + kRowsPerChunk);
+                    }
+                }
             }
         }
 
-        // Epilogue: halves -> slots (lane, lane+32); above the limit -> int32 re-run list.
+        // halves -> slots (lane, lane+32); the maximum over the group's units
         const int32_t sa = static_cast<int32_t>(best & 0xffffu);
         const int32_t sb = static_cast<int32_t>(best >> 16);
-        const uint32_t slot_a = gd.first_slot + lane, slot_b = slot_a + 32;
-        if (sa > p.limit) p.flag_list[atomicAdd(p.flag_count, 1u)] = slot_a;
-        else p.slot_scores[slot_a] = sa;
-        if (sb > p.limit) p.flag_list[atomicAdd(p.flag_count, 1u)] = slot_b;
-        else p.slot_scores[slot_b] = sb;
+        const uint32_t slot_a = gd.first_slot + lane;
+        if (sa) atomicMax(p.slot_scores + slot_a, sa);
+        if (sb) atomicMax(p.slot_scores + slot_a + 32, sb);
     }
 }
 
+// Slots whose packed-int16 score is above the trust limit -> list for the int32 re-run.
+__global__ void collect_flagged_kernel(const int32_t* slot_scores, uint32_t n_slots, int32_t limit,
+                                       uint32_t* list, uint32_t* count) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_slots; i += gridDim.x * blockDim.x)
+        if (slot_scores[i] > limit) list[atomicAdd(count, 1u)] = i;
+}
+
 // ------------------------------------------------------------------------------------------------
-// Inter-task kernel, int32: the exact re-run of flagged lanes (align.hpp:149-153 -> :42-64), and
-// the only inter-task kernel in "wide" mode (matrix + open outside int8).  One thread per
-// sequence, 16 query columns per pass, thread-private border rows laid out [row][thread].
-// PT = int8_t (prof8) or int32_t (prof32).
+// Intra-task kernel (int32, warp shuffles): one CTA per sequence (align.hpp:166-229 re-designed).
+// Used for (a) the exact re-run of lanes flagged by the int16 kernel (align.hpp:149-153), (b)
+// swb_score_pair / sw_score_wavefront, (c) every sequence in "wide" mode (matrix + open outside
+// int8), where the packed kernel does not apply.
+//
+// The query is striped over lanes, T (<= 8) columns per lane, 32*T per warp, W warps side by side
+// (W*32*T columns per pass).  Lane l of warp w handles subject row  d - w*Delta - l  at step d:
+// an anti-diagonal wavefront.  The (Hm, E) border of a lane's last column moves to its right
+// neighbour with one __shfl_up per step; between warps it goes through a shared-memory ring
+// (written by lane 31, read by the next warp's lane 0 >= 33 steps later, one __syncthreads every
+// 32 steps); between passes it goes through a per-CTA border row in global memory.
+// The diagonal seed is the previous step's inbound Hm, exactly the reference's diag_seed
+// (align.hpp:223).  Rows outside [0, n) are pad rows: before the start they leave the initial
+// state untouched, after the end they cannot raise `best`.
 // ------------------------------------------------------------------------------------------------
-struct WideParams {
-    const uint8_t* codes;       // interleaved short pool, as bytes
+struct IntraParams {
+    const uint8_t* codes;       // interleaved group layout, as bytes
     const GroupDesc* groups;
     const uint32_t* slot_len;
     const uint32_t* list;       // slots to score; nullptr = every slot 0..n_slots-1
     const uint32_t* list_count; // device count for `list`
     uint32_t n_slots;
-    const void* prof;
-    uint32_t pstride;
-    uint32_t n_tiles;           // ceil(m / 16)
-    uint2* border0;             // [max_rows][n_threads]
+    const void* profi;          // prof8i or prof32i
+    uint32_t n_lane_tiles;      // 8-slot words per profile row
+    uint32_t n_passes;
+    uint2* border0;             // [gridDim.x][border_rows]
     uint2* border1;
+    uint64_t border_rows;
     int32_t* slot_scores;
     int32_t open, ext;
 };
 
-template <typename PT>
-__global__ void __launch_bounds__(128) inter_s32_kernel(WideParams p) {
-    constexpr int T = kWideTile;
-    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t n_threads = gridDim.x * blockDim.x;
-    const uint32_t count = p.list ? *p.list_count : p.n_slots;
-    const int32_t NO = -p.open, NE = -p.ext;
-    const PT* prof = static_cast<const PT*>(p.prof);
+template <int T, typename PT>
+__global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraParams p) {
+    __shared__ uint2 ring[kIntraMaxWarps][kIntraRing];
+    __shared__ int32_t warp_best[kIntraMaxWarps];
 
-    for (uint32_t item = tid; item < count; item += n_threads) {
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int32_t NO = -p.open, NE = -p.ext;
+    const PT* prof = static_cast<const PT*>(p.profi);
+    const uint32_t row_words = p.n_lane_tiles * 8;
+    const uint32_t count = p.list ? *p.list_count : p.n_slots;
+    uint2* const my_b0 = p.border0 + static_cast<size_t>(blockIdx.x) * p.border_rows;
+    uint2* const my_b1 = p.border1 + static_cast<size_t>(blockIdx.x) * p.border_rows;
+
+    for (uint32_t item = blockIdx.x; item < count; item += gridDim.x) {
         const uint32_t slot = p.list ? p.list[item] : item;
-        const uint32_t len = p.slot_len[slot];
+        const int64_t n = p.slot_len[slot];
         const GroupDesc gd = p.groups[slot / kGroupSeqs];
-        const uint32_t s = slot % kGroupSeqs, lane = s & 31, half = s >> 5;
-        const uint8_t* seq = p.codes + (static_cast<size_t>(gd.chunk_base) * 32 + lane) * 16 + half * 8;
+        const uint32_t sl = slot % kGroupSeqs;
+        // residue r of this sequence: seq[(r / 8) * 512 + (r % 8)]
+        const uint8_t* seq = p.codes + (static_cast<size_t>(gd.chunk_base) * 32 + (sl & 31)) * 16 + (sl >> 5) * 8;
+
         int32_t best = 0;
-        for (uint32_t tile = 0; tile < p.n_tiles; ++tile) {
-            const PT* ptile = prof + tile * T;
-            const bool first = tile == 0, last = tile + 1 == p.n_tiles;
-            const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + tid;
-            uint2* bout = ((tile & 1) ? p.border1 : p.border0) + tid;
+        const int64_t steps = n + 31 + static_cast<int64_t>(kIntraDelta) * (W - 1);
+
+        for (uint32_t pass = 0; pass < p.n_passes && n > 0; ++pass) {
+            const uint32_t lane_tile = (pass * W + w) * 32 + lane;   // which T-column stripe this lane owns
+            const bool tile_valid = lane_tile < p.n_lane_tiles;
+            const PT* ptile = prof + static_cast<size_t>(tile_valid ? lane_tile : 0) * 8;
+            const bool first = pass == 0, last = pass + 1 == p.n_passes;
+            const uint2* bin = (pass & 1) ? my_b0 : my_b1;
+            uint2* bout = (pass & 1) ? my_b1 : my_b0;
+
             int32_t Hm[T], F[T];
 #pragma unroll
             for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
-            int32_t diag_in = NO;
-            for (uint32_t row = 0; row < len; ++row) {
-                const uint32_t a = seq[static_cast<size_t>(row / kRowsPerChunk) * 512 + (row % kRowsPerChunk)];
-                int32_t sub[T];
-                if (sizeof(PT) == 1) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(ptile + a * p.pstride);
-                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int k = 0; k < T; ++k)
-                        sub[k] = static_cast<int32_t>(static_cast<int8_t>((w[k / 4] >> (8 * (k & 3))) & 0xff));
-                } else {
-#pragma unroll
-                    for (int i = 0; i < T / 4; ++i) {
-                        const int4 v = *reinterpret_cast<const int4*>(ptile + a * p.pstride + 4 * i);
-                        sub[4 * i] = v.x, sub[4 * i + 1] = v.y, sub[4 * i + 2] = v.z, sub[4 * i + 3] = v.w;
+            int32_t diag_in = NO, out_h = NO, out_e = NO;
+
+            __syncthreads();   // ring and border rows are reused across passes and items
+
+            for (int64_t d = 0; d < steps; ++d) {
+                const int64_t r = d - static_cast<int64_t>(w) * kIntraDelta - lane;
+                const bool in_range = r >= 0 && r < n;
+                const uint32_t a = (in_range && tile_valid) ? seq[(r >> 3) * 512 + (r & 7)] : kPadCode;
+
+                // inbound border: from the left lane (previous step), the left warp's ring, the
+                // previous pass's global row, or the matrix edge
+                int32_t in_h = __shfl_up_sync(0xffffffffu, out_h, 1);
+                int32_t in_e = __shfl_up_sync(0xffffffffu, out_e, 1);
+                if (lane == 0) {
+                    in_h = NO, in_e = NO;
+                    if (in_range) {
+                        if (w > 0) {
+                            const uint2 v = ring[w][r & (kIntraRing - 1)];
+                            in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
+                        } else if (!first) {
+                            const uint2 v = bin[r];
+                            in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
+                        }
                     }
                 }
-                int32_t hl = NO, E = NO;
-                if (!first) {
-                    const uint2 bi = bin[static_cast<size_t>(row) * n_threads];
-                    hl = static_cast<int32_t>(bi.x), E = static_cast<int32_t>(bi.y);
+
+                int32_t sub[T];
+                if (sizeof(PT) == 1) {
+                    const uint2 v = *reinterpret_cast<const uint2*>(ptile + static_cast<size_t>(a) * row_words);
+#pragma unroll
+                    for (int k = 0; k < T; ++k) {
+                        const uint32_t word = k < 4 ? v.x : v.y;
+                        const uint32_t sel = (k & 3) == 0 ? 0x8880u : (k & 3) == 1 ? 0x9991u : (k & 3) == 2 ? 0xAAA2u : 0xBBB3u;
+                        sub[k] = static_cast<int32_t>(prmt(word, 0, sel));
+                    }
+                } else {
+                    const int4* q = reinterpret_cast<const int4*>(ptile + static_cast<size_t>(a) * row_words);
+                    const int4 v0 = q[0];
+                    const int4 v1 = T > 4 ? q[1] : make_int4(0, 0, 0, 0);
+                    const int32_t all[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                    for (int k = 0; k < T; ++k) sub[k] = all[k];
                 }
+
+                int32_t hl = in_h, E = in_e;
                 int32_t diag = diag_in;
-                diag_in = hl;
+                diag_in = in_h;
 #pragma unroll
                 for (int k = 0; k < T; ++k) {
                     E = __viaddmax_s32(E, NE, hl);
@@ -311,140 +413,25 @@ __global__ void __launch_bounds__(128) inter_s32_kernel(WideParams p) {
                     Hm[k] = hl;
                     best = max(best, h);
                 }
-                if (!last) bout[static_cast<size_t>(row) * n_threads] = make_uint2(hl, E);
+                out_h = hl, out_e = E;
+
+                if (lane == 31 && in_range) {
+                    if (w + 1 < W) ring[w + 1][r & (kIntraRing - 1)] = make_uint2(hl, E);
+                    else if (!last) bout[r] = make_uint2(hl, E);
+                }
+                if (W > 1 && (d & 31) == 31) __syncthreads();
             }
         }
-        p.slot_scores[slot] = best;
-    }
-}
 
-// ------------------------------------------------------------------------------------------------
-// Intra-task kernel (int32): one CTA per long sequence (align.hpp:166-229 re-designed).
-//
-// The query is striped over lanes, T (<= 8) columns per lane, 32*T per warp, W warps side by side
-// (W*32*T columns per pass).  Lane l of warp w handles subject row  d - w*Delta - l  at step d:
-// an anti-diagonal wavefront.  The (Hm, E) border of a lane's last column moves to its right
-// neighbour with one __shfl_up per step; between warps it goes through a shared-memory ring
-// (written by lane 31, read by the next warp's lane 0 >= 33 steps later, one __syncthreads every
-// 32 steps); between passes it goes through a per-sequence border row in global memory.
-// The diagonal seed is the previous step's inbound Hm, exactly the reference's diag_seed
-// (align.hpp:223).  Rows outside [0, n) are pad rows: before the start they leave the initial
-// state untouched, after the end they cannot raise `best`.
-// ------------------------------------------------------------------------------------------------
-struct IntraParams {
-    const uint8_t* codes;     // long pool
-    const LongDesc* longs;
-    uint32_t n_long;
-    const void* profi;        // prof8i or prof32i
-    uint32_t n_lane_tiles;    // 8-slot words per profile row
-    uint32_t n_passes;
-    uint2* border0;           // [long pool rows] (indexed by LongDesc::offset + row)
-    uint2* border1;
-    int32_t* long_scores;     // [n_long]
-    int32_t open, ext;
-};
-
-template <int T, typename PT>
-__global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraParams p) {
-    __shared__ uint2 ring[kIntraMaxWarps][kIntraRing];
-    __shared__ int32_t warp_best[kIntraMaxWarps];
-
-    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
-    const LongDesc ld = p.longs[blockIdx.x];
-    const int64_t n = ld.length;
-    const uint8_t* seq = p.codes + ld.offset;
-    const int32_t NO = -p.open, NE = -p.ext;
-    const PT* prof = static_cast<const PT*>(p.profi);
-    const uint32_t row_words = p.n_lane_tiles * 8;
-
-    int32_t best = 0;
-    const int64_t steps = n + 31 + static_cast<int64_t>(kIntraDelta) * (W - 1);
-
-    for (uint32_t pass = 0; pass < p.n_passes; ++pass) {
-        const uint32_t lane_tile = (pass * W + w) * 32 + lane;   // which T-column stripe this lane owns
-        const bool tile_valid = lane_tile < p.n_lane_tiles;
-        const PT* ptile = prof + static_cast<size_t>(tile_valid ? lane_tile : 0) * 8;
-        const bool first = pass == 0, last = pass + 1 == p.n_passes;
-        const uint2* bin = ((pass & 1) ? p.border0 : p.border1) + ld.offset;
-        uint2* bout = ((pass & 1) ? p.border1 : p.border0) + ld.offset;
-
-        int32_t Hm[T], F[T];
 #pragma unroll
-        for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
-        int32_t diag_in = NO, out_h = NO, out_e = NO;
-
-        if (W > 1) __syncthreads();   // ring reuse across passes
-
-        for (int64_t d = 0; d < steps; ++d) {
-            const int64_t r = d - static_cast<int64_t>(w) * kIntraDelta - lane;
-            const bool in_range = r >= 0 && r < n;
-            const uint32_t a = (in_range && tile_valid) ? seq[r] : kPadCode;
-
-            // inbound border: from the left lane (previous step), the left warp's ring, the
-            // previous pass's global row, or the matrix edge
-            int32_t in_h = __shfl_up_sync(0xffffffffu, out_h, 1);
-            int32_t in_e = __shfl_up_sync(0xffffffffu, out_e, 1);
-            if (lane == 0) {
-                in_h = NO, in_e = NO;
-                if (in_range) {
-                    if (w > 0) {
-                        const uint2 v = ring[w][r & (kIntraRing - 1)];
-                        in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
-                    } else if (!first) {
-                        const uint2 v = bin[r];
-                        in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
-                    }
-                }
-            }
-
-            int32_t sub[T];
-            if (sizeof(PT) == 1) {
-                const uint2 v = *reinterpret_cast<const uint2*>(ptile + static_cast<size_t>(a) * row_words);
-#pragma unroll
-                for (int k = 0; k < T; ++k) {
-                    const uint32_t word = k < 4 ? v.x : v.y;
-                    const uint32_t sel = (k & 3) == 0 ? 0x8880u : (k & 3) == 1 ? 0x9991u : (k & 3) == 2 ? 0xAAA2u : 0xBBB3u;
-                    sub[k] = static_cast<int32_t>(prmt(word, 0, sel));
-                }
-            } else {
-                const int4* q = reinterpret_cast<const int4*>(ptile + static_cast<size_t>(a) * row_words);
-                const int4 v0 = q[0];
-                const int4 v1 = T > 4 ? q[1] : make_int4(0, 0, 0, 0);
-                const int32_t all[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-                for (int k = 0; k < T; ++k) sub[k] = all[k];
-            }
-
-            int32_t hl = in_h, E = in_e;
-            int32_t diag = diag_in;
-            diag_in = in_h;
-#pragma unroll
-            for (int k = 0; k < T; ++k) {
-                E = __viaddmax_s32(E, NE, hl);
-                F[k] = __viaddmax_s32(F[k], NE, Hm[k]);
-                const int32_t h = __vimax3_s32_relu(diag + sub[k], E, F[k]);
-                diag = Hm[k];
-                hl = h + NO;
-                Hm[k] = hl;
-                best = max(best, h);
-            }
-            out_h = hl, out_e = E;
-
-            if (lane == 31 && in_range) {
-                if (w + 1 < W) ring[w + 1][r & (kIntraRing - 1)] = make_uint2(hl, E);
-                else if (!last) bout[r] = make_uint2(hl, E);
-            }
-            if (W > 1 && (d & 31) == 31) __syncthreads();
+        for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+        __syncthreads();
+        if (lane == 0) warp_best[w] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (uint32_t i = 1; i < W; ++i) best = max(best, warp_best[i]);
+            p.slot_scores[slot] = best;
         }
-    }
-
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if (lane == 0) warp_best[w] = best;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (uint32_t i = 1; i < W; ++i) best = max(best, warp_best[i]);
-        p.long_scores[blockIdx.x] = best;
     }
 }
 
@@ -460,35 +447,20 @@ constexpr int kSelectThreads = 1024;
 constexpr uint32_t kSelectMaxK = 1024;
 
 __global__ void build_keys_kernel(const int32_t* slot_scores, const uint32_t* slot_index, uint32_t n_slots,
-                                  const int32_t* long_scores, const LongDesc* longs, uint32_t n_long,
                                   uint64_t* keys) {
-    const uint32_t total = n_slots + n_long;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        uint64_t key = 0;
-        if (i < n_slots) {
-            const uint32_t idx = slot_index[i];
-            if (idx != kNoSequence)
-                key = (static_cast<uint64_t>(static_cast<uint32_t>(slot_scores[i])) << 32) | (0xFFFFFFFFu - idx);
-        } else {
-            const uint32_t pidx = i - n_slots;
-            key = (static_cast<uint64_t>(static_cast<uint32_t>(long_scores[pidx])) << 32) |
-                  (0xFFFFFFFFu - longs[pidx].db_index);
-        }
-        keys[i] = key;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_slots; i += gridDim.x * blockDim.x) {
+        const uint32_t idx = slot_index[i];
+        keys[i] = idx == kNoSequence
+                      ? 0ull
+                      : (static_cast<uint64_t>(static_cast<uint32_t>(slot_scores[i])) << 32) | (0xFFFFFFFFu - idx);
     }
 }
 
 __global__ void scatter_scores_kernel(const int32_t* slot_scores, const uint32_t* slot_index, uint32_t n_slots,
-                                      const int32_t* long_scores, const LongDesc* longs, uint32_t n_long,
                                       int32_t* out) {
-    const uint32_t total = n_slots + n_long;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        if (i < n_slots) {
-            const uint32_t idx = slot_index[i];
-            if (idx != kNoSequence) out[idx] = slot_scores[i];
-        } else {
-            out[longs[i - n_slots].db_index] = long_scores[i - n_slots];
-        }
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_slots; i += gridDim.x * blockDim.x) {
+        const uint32_t idx = slot_index[i];
+        if (idx != kNoSequence) out[idx] = slot_scores[i];
     }
 }
 

@@ -260,11 +260,10 @@ swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len
             stats->padded_cells += sstats[r].padded_cells;
             stats->kernel_launches += sstats[r].kernel_launches;
             stats->ms_total = std::max(stats->ms_total, sstats[r].ms_total);
-            stats->ms_inter = std::max(stats->ms_inter, sstats[r].ms_inter);
-            stats->ms_intra = std::max(stats->ms_intra, sstats[r].ms_intra);
+            stats->ms_setup = std::max(stats->ms_setup, sstats[r].ms_setup);
+            stats->ms_scan = std::max(stats->ms_scan, sstats[r].ms_scan);
             stats->ms_rescore = std::max(stats->ms_rescore, sstats[r].ms_rescore);
             stats->ms_topk = std::max(stats->ms_topk, sstats[r].ms_topk);
-            stats->ms_h2d_d2h = std::max(stats->ms_h2d_d2h, sstats[r].ms_h2d_d2h);
         }
     }
     return SWB_OK;

@@ -108,39 +108,50 @@ std::string pack_database(const SeqSource& src, uint64_t threshold, uint32_t sha
     out.n_long = static_cast<uint32_t>(longs.size());
     out.n_local = out.n_short + out.n_long;
 
-    // ---- short pool: groups of 64 -------------------------------------------------------------
-    const size_t n_groups = (shorts.size() + kGroupSeqs - 1) / kGroupSeqs;
+    // ---- groups of 64 over the whole shard, longest first ------------------------------------------
+    // every long sequence is at least as long as every short one, so longs + shorts is sorted
+    std::vector<Key> pool(std::move(longs));
+    pool.insert(pool.end(), shorts.begin(), shorts.end());
+    const size_t n_groups = (pool.size() + kGroupSeqs - 1) / kGroupSeqs;
     out.groups.resize(n_groups);
-    out.short_index.assign(n_groups * kGroupSeqs, kNoSequence);
-    out.short_len.assign(n_groups * kGroupSeqs, 0);
+    out.slot_index.assign(n_groups * kGroupSeqs, kNoSequence);
+    out.slot_len.assign(n_groups * kGroupSeqs, 0);
+
+    // member(g, s): the sequence in slot s of group g, or nullptr
+    auto member = [&](size_t g, uint32_t s) -> const Key* {
+        const size_t pos = g * kGroupSeqs + s;
+        return pos < pool.size() ? &pool[pos] : nullptr;
+    };
+
     uint64_t chunk_cursor = 0;
     for (size_t g = 0; g < n_groups; ++g) {
-        const uint32_t longest = shorts[g * kGroupSeqs].len;  // sorted: first member is the longest
+        const uint32_t longest = member(g, 0)->len;  // sorted: first member is the longest
         const uint32_t n_chunks = (longest + kRowsPerChunk - 1) / kRowsPerChunk;
         out.groups[g] = GroupDesc{chunk_cursor, n_chunks, static_cast<uint32_t>(g * kGroupSeqs)};
         chunk_cursor += n_chunks;
         out.padded_rows += static_cast<uint64_t>(n_chunks) * kRowsPerChunk;
+        out.max_length = std::max(out.max_length, longest);
     }
     out.total_chunks = chunk_cursor;
-    out.short_codes.assign(static_cast<size_t>(chunk_cursor) * 32 * 16, kPadCode);
+    out.codes.assign(static_cast<size_t>(chunk_cursor) * 32 * 16, kPadCode);
 
     std::atomic<bool> bad{false};
-    std::atomic<uint64_t> short_res{0};
+    std::atomic<uint64_t> residues{0};
     parallel_for(n_groups, [&](size_t g) {
         const GroupDesc& gd = out.groups[g];
-        uint8_t* base = out.short_codes.data() + static_cast<size_t>(gd.chunk_base) * 32 * 16;
+        uint8_t* base = out.codes.data() + static_cast<size_t>(gd.chunk_base) * 32 * 16;
         uint64_t res = 0;
         for (uint32_t s = 0; s < kGroupSeqs; ++s) {
-            const size_t pos = g * kGroupSeqs + s;
-            if (pos >= shorts.size()) break;
-            const Key k = shorts[pos];
-            out.short_index[pos] = k.idx;
-            out.short_len[pos] = k.len;
-            res += k.len;
+            const Key* k = member(g, s);
+            if (!k) break;
+            const size_t slot = g * kGroupSeqs + s;
+            out.slot_index[slot] = k->idx;
+            out.slot_len[slot] = k->len;
+            res += k->len;
             const uint32_t lane = s & 31, half = s >> 5;
-            const uint8_t* codes = src.data(k.idx);
-            for (uint32_t r0 = 0; r0 < k.len; r0 += kRowsPerChunk) {
-                const uint32_t cnt = std::min(kRowsPerChunk, k.len - r0);
+            const uint8_t* codes = src.data(k->idx);
+            for (uint32_t r0 = 0; r0 < k->len; r0 += kRowsPerChunk) {
+                const uint32_t cnt = std::min(kRowsPerChunk, k->len - r0);
                 uint8_t* dst = base + (static_cast<size_t>(r0 / kRowsPerChunk) * 32 + lane) * 16 + half * 8;
                 for (uint32_t r = 0; r < cnt; ++r) {
                     const uint8_t c = codes[r0 + r];
@@ -149,32 +160,9 @@ std::string pack_database(const SeqSource& src, uint64_t threshold, uint32_t sha
                 }
             }
         }
-        short_res.fetch_add(res, std::memory_order_relaxed);
+        residues.fetch_add(res, std::memory_order_relaxed);
     });
-    out.short_residues = short_res.load();
-    out.residues = out.short_residues;
-
-    // ---- long pool: contiguous, 16-byte aligned starts, padded tail -----------------------------
-    out.longs.resize(longs.size());
-    uint64_t cursor = 0;
-    for (size_t p = 0; p < longs.size(); ++p) {
-        out.longs[p] = LongDesc{cursor, longs[p].len, longs[p].idx};
-        cursor += (static_cast<uint64_t>(longs[p].len) + 15) & ~15ull;
-        out.residues += longs[p].len;
-    }
-    out.long_codes.assign(static_cast<size_t>(cursor) + 16, kPadCode);
-    parallel_for(longs.size(), [&](size_t p) {
-        const LongDesc& ld = out.longs[p];
-        const uint8_t* codes = src.data(ld.db_index);
-        uint8_t* dst = out.long_codes.data() + ld.offset;
-        for (uint32_t r = 0; r < ld.length; ++r) {
-            if (codes[r] >= kAlphabet) bad.store(true, std::memory_order_relaxed);
-            dst[r] = codes[r];
-        }
-    });
-
-    for (const Key& k : shorts) out.max_length = std::max(out.max_length, k.len);
-    for (const Key& k : longs) out.max_length = std::max(out.max_length, k.len);
+    out.residues = residues.load();
 
     if (bad.load()) {
         if (bad_code) *bad_code = true;

@@ -1,21 +1,23 @@
 // pack.hpp -- host-side database packing for the B200 scoring path.
 //
 // Replaces the reference's per-search routing (partition_database, scheduler.hpp:56-65) and its
-// per-chunk pointer gather (scheduler.hpp:156-160) with a one-off layout the kernels can stream:
+// per-chunk pointer gather (scheduler.hpp:156-160) with a one-off layout the kernels can stream.
 //
-//   short pool (length < threshold, inter-task kernel)
-//     sequences of this shard sorted by (length desc, db_index asc), cut into groups of 64
-//     (one warp: 32 lanes x 2 sequences, the two int16 halves of a DPX word).  Lane l of a group
-//     owns sorted positions base+l (half A, low 16 bits) and base+32+l (half B, high 16 bits).
-//     Rows are padded with PAD_CODE to the group's longest member rounded up to 8.  Residues are
-//     interleaved so that one warp load of 512 contiguous bytes fetches 8 rows for all 64
-//     sequences:   codes[(chunk*32 + lane)*16 + half*8 + r]   (chunk = row/8, r = row%8).
+// All sequences of a shard are sorted by (length desc, db_index asc) and cut into groups of 64
+// (one warp: 32 lanes x 2 sequences, the two int16 halves of a DPX word).  Lane l of a group owns
+// sorted positions base+l (half A, low 16 bits) and base+32+l (half B, high 16 bits).  Rows are
+// padded with kPadCode to the group's longest member rounded up to 8.  Residues are interleaved
+// so that one warp load of 512 contiguous bytes fetches 8 rows for all 64 sequences:
 //
-//   long pool (length >= threshold, intra-task kernel)
-//     sequences sorted the same way, stored contiguously, each start 16-byte aligned.
+//       codes[(chunk*32 + lane)*16 + half*8 + r]        chunk = row / 8,  r = row % 8
 //
-// Sharding: both pools are dealt over the shards in "snake" order of the global sorted lists so
-// every shard gets the same length distribution and residue count to within one sequence.
+// Routing by SearchConfig::length_threshold (scheduler.hpp:24,59-62) survives as bookkeeping
+// (n_short / n_long feed SearchStats) and in the sharding below; execution-wise every group goes
+// through the same tile-wavefront kernel, which gives a group as many cooperating warps as it has
+// query tiles -- long sequences automatically get intra-task parallelism.
+//
+// Sharding: the long and the short sorted lists are each dealt over the shards in "snake" order,
+// so every shard gets the same length distribution and residue count to within one sequence.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -24,21 +26,15 @@
 namespace swb {
 
 constexpr uint32_t kAlphabet = 24;       // scoring.hpp:25
-constexpr uint8_t kPadCode = 24;         // extra profile row, scores <= 0 against everything
+constexpr uint8_t kPadCode = 24;         // extra profile row: substitution score 0 against everything
 constexpr uint32_t kGroupSeqs = 64;      // sequences per interleaved group
 constexpr uint32_t kRowsPerChunk = 8;    // residues of one sequence per 16-byte lane slot
 constexpr uint32_t kNoSequence = 0xFFFFFFFFu;
 
 struct GroupDesc {
-    uint64_t chunk_base;  // index of the group's first (chunk, lane=0) slot, in units of 32 lanes x 16 B
+    uint64_t chunk_base;  // index of the group's first chunk, in units of (32 lanes x 16 B)
     uint32_t n_chunks;    // padded rows / 8
-    uint32_t first_slot;  // index of the group's first entry in short_index / short_len
-};
-
-struct LongDesc {
-    uint64_t offset;    // byte offset into long_codes (16-byte aligned)
-    uint32_t length;
-    uint32_t db_index;
+    uint32_t first_slot;  // index of the group's first entry in slot_index / slot_len
 };
 
 struct PackedDb {
@@ -46,17 +42,14 @@ struct PackedDb {
     uint32_t shard_rank = 0, shard_count = 1;
     uint32_t max_length = 0;
     uint64_t residues = 0;         // real residues in this shard
-    uint64_t short_residues = 0;   // real residues in the short pool
-    uint64_t padded_rows = 0;      // sum over groups of padded rows (x64 = stored short residues)
+    uint64_t padded_rows = 0;      // sum over groups of padded rows (x64 = stored residues)
     uint64_t total_chunks = 0;
     uint64_t length_threshold = 0;
 
-    std::vector<GroupDesc> groups;
-    std::vector<uint32_t> short_index;  // [n_groups*64] slot -> db_index, kNoSequence for unused slots
-    std::vector<uint32_t> short_len;    // [n_groups*64]
-    std::vector<uint8_t> short_codes;   // total_chunks * 32 * 16 bytes
-    std::vector<LongDesc> longs;        // sorted by length desc
-    std::vector<uint8_t> long_codes;
+    std::vector<GroupDesc> groups;      // descending padded rows
+    std::vector<uint32_t> slot_index;   // [n_groups*64] slot -> db_index, kNoSequence for unused slots
+    std::vector<uint32_t> slot_len;     // [n_groups*64]
+    std::vector<uint8_t> codes;         // total_chunks * 32 * 16 bytes
 };
 
 // Source of sequences: either pointer-per-sequence or flat codes + offsets.
