@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""bench.py -- GCUPS of the SW#db scoring path on BASELINE config 2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference] [--scale S]
+
+Workload (config.workload): the 20-query sweep (lengths 144..5478) against a synthetic Swiss-Prot-shaped
+database (565,928 sequences, ~204 M residues), BLOSUM62, gap open 10 / extend 2, top_k 10.  One *step* is
+one full sweep: 20 searches, 8.5e12 cell updates.  GCUPS = sum(query_len x db_residues) / seconds / 1e9
+(SPEC.md:353), real residues only (padding is never counted).
+
+  value      device-timed: per-search CUDA-event time on the search stream (database already resident in HBM,
+             packed once outside the timed region like the reference's load phase), summed over
+             the sweep; max over ranks.
+  e2e        the same sweep through the C-ABI call a user makes (swb_search: HOST query/matrix buffers in, HOST
+             hits out, host<->device copies and host gaps inside the timed region), bracketed by CUDA events on
+             the stream the kernels run on plus a barrier; max over ranks.
+  roofline   the dominant kernel (wavefront_s16_kernel) against the DPX cell-update roofline P_dpx x 2 / 6
+             (SURVEY.md 8(d)); P_dpx is measured live by swb_measure_pipe_rates.  The HBM side (packed-database
+             stream, 1 byte per residue per search) is reported against MEASURED_PEAKS.json.
+  cpu_baseline  the unmodified reference (oracle/_ref/libswref.so, run_search without traceback) on the host
+             cores, on a bounded subsample of the same workload (N=1, rank 0 only).
+
+N > 1 (torchrun, one rank per GPU): the same database is sharded by residue count (strong scaling); every
+search ends with one all-gather of k packed keys per rank (NCCL) and a device-side merge.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+TOP_K = 10
+GAPS = (10, 2)
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0, help="database size relative to Swiss-Prot (debug only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+
+
+# ------------------------------------------------------------------------------------------------------------
+# clocks: sampled with NVML while the timed region runs
+# ------------------------------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.power = [], set(), []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:   # NVML missing: report that instead of inventing numbers
+            self.nv = None
+            self.err = str(exc)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons") \
+                    else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def start(self):
+        if self.nv:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._thread:
+            self._thread.join()
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "nvml unavailable")}
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "power_w_max": max(self.power) if self.power else None,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------------------------
+# CPU reference leg
+# ------------------------------------------------------------------------------------------------------------
+def cpu_sample(queries, sdb, seed=7, n_seqs=6000, query_ids=(0, 9, 19)):
+    """A bounded sample of the workload: a seeded subsample of the database (with one long sequence) and three
+    of the twenty queries."""
+    rng = np.random.default_rng(seed)
+    lens = sdb.lengths()
+    pick = rng.choice(sdb.n, size=min(n_seqs, sdb.n), replace=False)
+    longs = np.nonzero(lens >= 3000)[0]
+    if len(longs):
+        pick[0] = longs[len(longs) // 2]
+    sub = sdb.subset(np.sort(pick))
+    return [queries[i] for i in query_ids if i < len(queries)], sub
+
+
+def run_cpu_reference(queries, sub, threads, repeats=1):
+    """Times the unmodified reference's run_search (compute_alignments=false) on the sample. Returns
+    (GCUPS, seconds, kind)."""
+    from oracle import pyoracle as po
+    from paper_2203_11100_b200 import synth
+    b62 = synth.blosum62()
+    cells = sum(len(q) for q in queries) * sub.residues
+    if po.Ref.available():
+        ref = po.Ref()
+        h = ref.db_create(po.FlatDb(sub.codes, sub.offsets))
+        best = None
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            for q in queries:
+                ref.run_search(h, q, b62, GAPS[0], GAPS[1], worker_count=threads, lane_width=8, chunk_width=64,
+                               length_threshold=3000, top_k=TOP_K, cpu_pool_threads=threads)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        ref.db_destroy(h)
+        return cells / best / 1e9, best, "reference"
+    port = po.Port()      # the C restatement, OpenMP over sequences
+    fdb = po.FlatDb(sub.codes, sub.offsets)
+    t0 = time.perf_counter()
+    for q in queries:
+        port.score_all(q, fdb, b62, GAPS[0], GAPS[1])
+    dt = time.perf_counter() - t0
+    return cells / dt / 1e9, dt, "port"
+
+
+def describe_sample(queries, sub):
+    return (f"{sub.n} sequences ({sub.residues} residues, seeded subsample of the config-2 database incl. one long "
+            f"sequence) x queries of length {[len(q) for q in queries]}")
+
+
+def workload_name(scale):
+    base = ("config2: 20-query sweep (len 144-5478) vs synthetic Swiss-Prot-shaped DB (565,928 seqs, ~204M residues), "
+            "BLOSUM62, gap 10/2, top_k 10")
+    return base if scale == 1.0 else base + f" [DEBUG scale={scale}]"
+
+
+def main_reference(args):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return 0
+    from paper_2203_11100_b200 import synth
+    queries, sdb = synth.config2(scale=args.scale)
+    qs, sub = cpu_sample(queries, sdb)
+    threads = os.cpu_count() or 1
+    times = []
+    for step in range(args.warmup + args.steps):
+        gc, dt, kind = run_cpu_reference(qs, sub, threads)
+        if step >= args.warmup:
+            times.append(dt)
+    cells = sum(len(q) for q in qs) * sub.residues
+    sec = float(np.mean(times))
+    value = cells / sec / 1e9
+    line = {
+        "impl": "reference", "metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int16 saturating + int32 re-run (CPU)", "data": "synthetic",
+        "config": {"workload": workload_name(args.scale), "step": "bounded CPU sample: " + describe_sample(qs, sub)},
+        "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": threads, "kind": kind, "sample": describe_sample(qs, sub)},
+        "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------------------
+# native leg
+# ------------------------------------------------------------------------------------------------------------
+def main_native(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2203_11100_b200 import GapModel, measure_pipe_rates, synth
+    from paper_2203_11100_b200.dist import ShardedSearch
+
+    rank, local_rank, world = env_rank()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device: the native path has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    b62 = synth.blosum62()
+    gaps = GapModel(*GAPS)
+    queries, sdb = synth.config2(scale=args.scale)
+    t0 = time.perf_counter()
+    engine = ShardedSearch(sdb.codes, sdb.offsets, length_threshold=3000, device_index=local_rank)
+    pack_upload_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream(device)
+    engine.db.set_stream(stream.cuda_stream)      # all kernels now run on the stream torch's events record on
+    info = engine.db.info()
+
+    total_cells = sum(len(q) for q in queries) * sdb.residues     # whole job, all ranks
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else None
+    rates = measure_pipe_rates(local_rank, 1.0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    def one_step():
+        """One sweep. Returns (device ms summed over searches, kernel ms of the scan, launches, hits, per-query)."""
+        dev_ms = scan_ms = 0.0
+        launches = 0
+        hits, per_query = [], []
+        for q in queries:
+            idx, sc, st = engine.search(q, b62, gaps, TOP_K)
+            dev_ms += st["ms_total"]
+            scan_ms += st["ms_scan"]
+            launches += st["kernel_launches"]
+            hits.append((idx.copy(), sc.copy()))
+            per_query.append((len(q), st["ms_total"], st["ms_scan"], st["rescored_i32"], st["chunks_claimed"]))
+        return dev_ms, scan_ms, launches, hits, per_query
+
+    first_hits = None
+    for _ in range(max(args.warmup, 0)):
+        _, _, _, hits, _ = one_step()
+        first_hits = first_hits or hits
+
+    sampler = ClockSampler(local_rank)
+    barrier()
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    dev_ms = scan_ms = 0.0
+    launches = 0
+    per_query = None
+    for _ in range(args.steps):
+        d, s, l, hits, per_query = one_step()
+        dev_ms += d
+        scan_ms += s
+        launches += l
+        if first_hits is None:
+            first_hits = hits
+        for (a, b), (c, e) in zip(hits, first_hits):       # determinism check of SPEC.md:377
+            if not ((a == c).all() and (b == e).all()):
+                raise SystemExit("determinism_error: a repetition returned a different ranked list")
+    ev1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    e2e_ms = ev0.elapsed_time(ev1)
+
+    t = torch.tensor([dev_ms, e2e_ms, scan_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms, scan_ms = (float(x) for x in t.cpu())
+    if world > 1:
+        lt = torch.tensor([launches], dtype=torch.int64, device=device)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+
+    if rank == 0:
+        steps = max(args.steps, 1)
+        value = total_cells * steps / (dev_ms * 1e-3) / 1e9
+        e2e = total_cells * steps / (e2e_ms * 1e-3) / 1e9
+        # planted exact copies must be the top hit of every query (cheap sanity on the full size)
+        for qi, (idx, sc) in enumerate(first_hits):
+            if args.scale == 1.0 and world == 1 and idx[0] != sdb.planted[qi][0]:
+                raise SystemExit(f"query {qi}: top hit {idx[0]} is not the planted exact copy")
+        p_dpx = rates["viaddmnmx_s16x2"]                      # 1e9 thread-instructions/s, all SMs
+        roof = p_dpx * 2.0 / 6.0 * world                      # GCUPS: 6 DPX instr per 2 cells
+        scan_gcups = total_cells * steps / (scan_ms * 1e-3) / 1e9
+        hbm_peak = peaks["hbm_gbs"] if peaks else 6650.0
+        db_stream_gbs = sdb.residues * len(queries) * steps / (scan_ms * 1e-3) / 1e9
+        traffic = None
+        tfile = ROOT / "profiles" / "traffic.json"
+        if tfile.exists():
+            traffic = json.loads(tfile.read_text())
+        line = {
+            "metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": e2e_ms / steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "s16x2 (packed int16 DPX) + int32 re-run", "data": "synthetic",
+            "config": {"workload": workload_name(args.scale), "parallelism": f"db-shard x{world}",
+                       "l2": "inputs larger than L2: 207 MB packed database + 1.7 GB border rows per sweep vs 126 MB L2",
+                       "db": {k: info[k] for k in ("n_total", "n_local", "n_groups", "residues", "padded_residues", "device_bytes")},
+                       "pack_upload_s_outside_timing": pack_upload_s},
+            "e2e": {"value": e2e, "unit": "GCUPS",
+                    "h2d_bytes_per_step": int(sum(len(q) + 2304 + 4 * (info["n_groups"] + 1) for q in queries)),
+                    "d2h_bytes_per_step": int(len(queries) * (TOP_K * 8 + 16)),
+                    "cold_first_search_incl_pack_upload_s": pack_upload_s},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "roofline": {"bound": "dpx_alu", "kernel": "wavefront_s16_kernel", "achieved": scan_gcups, "peak": roof,
+                         "unit": "GCUPS", "frac": scan_gcups / roof,
+                         "peak_def": "P_dpx x 2 / 6, P_dpx = measured VIADDMNMX.S16x2 thread-instr/s (live, this run)",
+                         "p_dpx_ginst_per_s": p_dpx, "pipe_rates": rates, "traffic": traffic,
+                         "hbm": {"bound": "hbm", "achieved": db_stream_gbs, "peak": hbm_peak, "unit": "GB/s",
+                                 "frac": db_stream_gbs / hbm_peak,
+                                 "peak_src": "MEASURED_PEAKS.json" if peaks else "fallback",
+                                 "def": "packed-database stream: 1 byte per residue per search / scan-kernel time"}},
+            "per_query": [{"m": m, "gcups": m * sdb.residues / (ms * 1e-3) / 1e9, "ms": ms, "scan_ms": sms,
+                           "rescored_i32": int(r), "units": int(u)} for (m, ms, sms, r, u) in per_query],
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            qs, sub = cpu_sample(queries, sdb)
+            threads = os.cpu_count() or 1
+            gc, dt, kind = run_cpu_reference(qs, sub, threads)
+            line["cpu_baseline"] = {"value": gc, "unit": "GCUPS", "cores": threads, "kind": kind,
+                                    "sample": describe_sample(qs, sub), "seconds": dt}
+        print(json.dumps(line))
+    engine.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    a = parse_args()
+    sys.exit(main_reference(a) if a.impl == "reference" else main_native(a))

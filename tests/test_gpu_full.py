@@ -1,0 +1,70 @@
+"""BASELINE.json's full-size configuration (config 2: Swiss-Prot-shaped database, 565,928 sequences,
+~204 M residues) checked through size-independent properties plus sampled parity against the oracle."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2203_11100_b200 import Database, GapModel, MultiGpuDatabase, synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def full(lib):
+    import torch
+    assert torch.cuda.is_available()
+    queries, sdb = synth.config2()
+    db = Database(sdb.codes, sdb.offsets)
+    yield queries, sdb, db
+    db.close()
+
+
+def test_shape(full):
+    queries, sdb, db = full
+    info = db.info()
+    assert info["n_total"] == synth.SWISSPROT_SEQS
+    assert abs(info["residues"] - synth.SWISSPROT_RESIDUES) / synth.SWISSPROT_RESIDUES < 0.01
+    assert info["max_length"] == synth.SWISSPROT_MAXLEN
+    assert info["n_long"] > 1000 and info["n_short"] + info["n_long"] == info["n_total"]
+    assert info["padded_residues"] / info["residues"] < 1.03       # length sorting keeps padding under 3 %
+
+
+@pytest.mark.parametrize("qi", [0, 9, 19])
+def test_planted_copy_is_top_hit_with_self_score(full, port, b62, qi):
+    queries, sdb, db = full
+    q = queries[qi]
+    idx, sc, st = db.search(q, b62, GapModel(10, 2), 10)
+    exact = sdb.planted[qi][0]
+    assert idx[0] == exact
+    assert sc[0] == port.score_scalar(q, q, b62, 10, 2)            # self score = the ceiling for this query
+    assert (np.diff(sc.astype(np.int64)) <= 0).all()               # sorted
+    for i, s in zip(idx[:4], sc[:4]):                              # planted homologs, exact values
+        assert s == port.score_scalar(q, sdb.seq(int(i)), b62, 10, 2)
+    assert set(sdb.planted[qi][:3]) <= set(int(i) for i in idx)
+    assert st["cells"] == len(q) * sdb.residues
+    idx2, sc2, _ = db.search(q, b62, GapModel(10, 2), 10)           # determinism
+    assert (idx2 == idx).all() and (sc2 == sc).all()
+
+
+def test_sampled_score_parity(full, port, b62):
+    queries, sdb, db = full
+    q = queries[3]                                                  # m = 375
+    got, _ = db.score_all(q, b62, GapModel(10, 2))
+    rng = np.random.default_rng(2)
+    lens = sdb.lengths()
+    sample = np.unique(np.concatenate([rng.choice(sdb.n, 3000, replace=False), np.argsort(lens)[-40:],
+                                       np.nonzero(lens == 0)[0][:5], np.array(sdb.planted[3])]))
+    sub = po.FlatDb.from_list([sdb.seq(int(i)) for i in sample])
+    exp = port.score_all(q, sub, b62, 10, 2)
+    assert (got[sample] == exp).all()
+    assert (got >= 0).all()
+
+
+def test_sharded_full_database(full, b62):
+    queries, sdb, db = full
+    q = queries[6]
+    i1, s1, _ = db.search(q, b62, GapModel(10, 2), 50)
+    mdb = MultiGpuDatabase(sdb.codes, sdb.offsets, [0, 0, 0, 0])
+    i2, s2, st = mdb.search(q, b62, GapModel(10, 2), 50)
+    mdb.close()
+    assert (i1 == i2).all() and (s1 == s2).all()

@@ -1,0 +1,251 @@
+"""Parity tests proper: the CUDA path, called through the C-ABI (libswb200.so via ctypes), against the oracle
+(oracle/sw_oracle.c), the committed reference fixtures, and -- where oracle/_ref travelled -- the unmodified
+reference itself.  Everything here is integer work: the bar is bit-exact."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2203_11100_b200 import (Database, GapModel, MultiGpuDatabase, SearchConfig, decode_keys, merge_keys,
+                                   run_search, score_batch, score_wavefront, synth)
+from tests._util import enc, golden, naive_rank
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _loaded(lib):
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return lib
+
+
+def test_known_answers(b62):
+    A, g = enc("AAA"), GapModel(10, 2)
+    assert score_wavefront(A, A, b62, g, 1) == 12
+    assert score_batch(A, [A], 4, b62, g).tolist() == [12, 0, 0, 0]
+    assert score_wavefront(enc("ARN"), enc("RNA"), b62, g, 64) == 11
+    with Database.from_sequences([A]) as db:
+        idx, sc, stats, _ = run_search(A, db, b62, g, SearchConfig(top_k=1))
+        assert idx.tolist() == [0] and sc.tolist() == [12]
+    with Database.from_sequences([enc(""), synth.random_residues(np.random.default_rng(0), 50)]) as db:
+        idx, sc, _, _ = run_search(A, db, b62, g)                           # every sequence is a hit, even empty ones
+        assert len(idx) == 2 and idx[-1] == 0 and sc[-1] == 0
+
+
+def test_golden_pairs(b62):
+    for rec in golden()["pairs"]:
+        q, s, g = enc(rec["q"]), enc(rec["s"]), GapModel(rec["open"], rec["extend"])
+        for cw in (1, 64):
+            assert score_wavefront(q, s, b62, g, cw) == rec["scalar"]      # intra-task kernel
+        assert score_batch(q, [s], 1, b62, g).tolist() == [rec["scalar"]]   # packed int16 kernel (+ re-run)
+
+
+def test_golden_batches(b62):
+    for rec in golden()["batches"]:
+        subs = [None if s is None else enc(s) for s in rec["subjects"]]
+        got = score_batch(enc(rec["q"]), subs, rec["lane_width"], b62, GapModel(rec["open"], rec["extend"]))
+        assert got.tolist() == rec["scores"], rec.get("note")
+
+
+def test_golden_searches(b62):
+    for rec in golden()["searches"]:
+        seqs = [enc(s) for s in rec["db"]]
+        q, g = enc(rec["q"]), GapModel(rec["open"], rec["extend"])
+        with Database.from_sequences(seqs, length_threshold=rec["length_threshold"]) as db:
+            idx, sc, stats, _ = run_search(q, db, b62, g, SearchConfig(top_k=rec["top_k"]))
+            assert idx.tolist() == rec["hits_index"] and sc.tolist() == rec["hits_score"]
+            assert stats["lane_scored"] == rec["lane_scored"] and stats["wavefront_scored"] == rec["wavefront_scored"]
+            if seqs:
+                allsc, _ = db.score_all(q, b62, g)
+                assert allsc.tolist() == rec["all_scores"]
+
+
+@pytest.mark.parametrize("seed,thr,gaps", [(1, 3000, (10, 2)), (2, 100, (11, 1)), (3, 0, (5, 5)), (4, 10 ** 9, (0, 0)),
+                                           (5, 250, (12, 2)), (6, 33, (10, 2))])
+def test_random_databases(port, b62, seed, thr, gaps):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 500))
+    seqs = [synth.random_residues(rng, int(rng.integers(0, 300))) for _ in range(n)]
+    seqs[0] = synth.random_residues(rng, 900)
+    m = int(rng.integers(1, 300))
+    q = synth.random_residues(rng, m)
+    seqs[n // 2] = synth.mutate(rng, q, 0.1, 2)
+    fdb = po.FlatDb.from_list(seqs)
+    with Database(fdb.codes, fdb.offsets, length_threshold=thr) as db:
+        got, st = db.score_all(q, b62, GapModel(*gaps))
+        exp = port.score_all(q, fdb, b62, *gaps)
+        assert (got == exp).all()
+        idx, sc, _ = db.search(q, b62, GapModel(*gaps), 17)
+        ei, es, _ = port.run_search(q, fdb, b62, *gaps, length_threshold=thr, top_k=17)
+        assert (idx == ei).all() and (sc == es).all()
+        assert st["lane_scored"] + st["wavefront_scored"] == n
+
+
+def test_config1_full_parity(port, b62):
+    """BASELINE config 1: one 144-residue query vs 10,000 sequences, every score and the ranked list."""
+    qs, sdb = synth.config1()
+    fdb = po.FlatDb(sdb.codes, sdb.offsets)
+    with Database(sdb.codes, sdb.offsets) as db:
+        got, st = db.score_all(qs[0], b62, GapModel(10, 2))
+        exp = port.score_all(qs[0], fdb, b62, 10, 2)
+        assert (got == exp).all()
+        idx, sc, stats, _ = run_search(qs[0], db, b62, GapModel(10, 2))
+        ei, es, est = port.run_search(qs[0], fdb, b62, 10, 2)
+        assert (idx == ei).all() and (sc == es).all()
+        assert stats["lane_scored"] == est[0] and stats["wavefront_scored"] == est[1]
+        assert idx[0] == sdb.planted[0][0]
+        # determinism: a repeat gives the identical list
+        idx2, sc2, _, _ = run_search(qs[0], db, b62, GapModel(10, 2))
+        assert (idx2 == idx).all() and (sc2 == sc).all()
+
+
+def test_config1_against_reference_itself(ref, b62):
+    qs, sdb = synth.config1()
+    h = ref.db_create(po.FlatDb(sdb.codes, sdb.offsets))
+    ri, rs, rst = ref.run_search(h, qs[0], b62, 10, 2, worker_count=4, cpu_pool_threads=2)
+    ref.db_destroy(h)
+    with Database(sdb.codes, sdb.offsets) as db:
+        idx, sc, stats, _ = run_search(qs[0], db, b62, GapModel(10, 2))
+    assert (idx == ri).all() and (sc == rs).all()
+    assert stats["lane_scored"] == rst[0] and stats["wavefront_scored"] == rst[1]
+
+
+def test_int16_overflow_is_rerun_in_int32(port, b62):
+    rng = np.random.default_rng(12)
+    q = synth.random_residues(rng, 4000)
+    q[::2] = 17          # W: 11 per match
+    q[1::4] = 4          # C: 9 per match
+    seqs = [q.copy(), synth.random_residues(rng, 500), q[:3500].copy(), synth.mutate(rng, q, 0.02, 2)]
+    seqs += [synth.random_residues(rng, int(rng.integers(0, 900))) for _ in range(150)]
+    fdb = po.FlatDb.from_list(seqs)
+    exp = port.score_all(q, fdb, b62, 10, 2)
+    assert exp.max() > 32767
+    for thr in (10 ** 9, 3000, 0):
+        with Database(fdb.codes, fdb.offsets, length_threshold=thr) as db:
+            got, st = db.score_all(q, b62, GapModel(10, 2))
+            assert (got == exp).all()
+            assert st["rescored_i32"] >= 1
+
+
+def test_wide_mode_matrix_outside_int8(port, b62):
+    """Matrix entries x40 and large gaps: the packed path does not apply, everything runs in int32."""
+    rng = np.random.default_rng(13)
+    big = (b62 * 40).astype(np.int32)
+    seqs = [synth.random_residues(rng, int(rng.integers(0, 400))) for _ in range(90)]
+    q = synth.random_residues(rng, 333)
+    seqs[7] = synth.mutate(rng, q, 0.1, 1)
+    fdb = po.FlatDb.from_list(seqs)
+    for gaps in [(400, 80), (200, 200)]:
+        with Database(fdb.codes, fdb.offsets, length_threshold=200) as db:
+            got, _ = db.score_all(q, big, GapModel(*gaps))
+            assert (got == port.score_all(q, fdb, big, *gaps)).all()
+    # an asymmetric matrix: the lookup order matrix[subject][query] (align.hpp:34,74) is what matters
+    asym = b62.copy()
+    asym[3, 5] += 6
+    asym[11, 2] -= 3
+    with Database(fdb.codes, fdb.offsets) as db:
+        got, _ = db.score_all(q, asym, GapModel(10, 2))
+        assert (got == port.score_all(q, fdb, asym, 10, 2)).all()
+
+
+def test_topk_edges(port, b62):
+    rng = np.random.default_rng(14)
+    g = GapModel(10, 2)
+    # many ties, including at the top-k boundary: 40 copies of 5 distinct sequences + empties
+    base = [synth.random_residues(rng, 60) for _ in range(5)]
+    seqs = [base[i % 5].copy() for i in range(200)] + [enc("")] * 5
+    q = base[2][:40]
+    fdb = po.FlatDb.from_list(seqs)
+    exp = port.score_all(q, fdb, b62, 10, 2)
+    with Database(fdb.codes, fdb.offsets) as db:
+        for k in (1, 39, 40, 41, 205, 1000, 1025, 5000):
+            idx, sc, _ = db.search(q, b62, g, k)
+            ni, ns = naive_rank(exp, k)
+            assert (idx == ni).all() and (sc == ns).all(), k
+    # N < top_k and all-zero scores: order is db_index ascending
+    stars = [np.full(int(rng.integers(0, 9)), 23, np.uint8) for _ in range(7)]
+    with Database.from_sequences(stars) as db:
+        idx, sc, _ = db.search(enc("AAAA"), b62, g, 10)
+        assert idx.tolist() == list(range(7)) and sc.tolist() == [0] * 7
+    # k > 1024 on a larger database takes the full-sort path
+    seqs = [synth.random_residues(rng, int(rng.integers(0, 80))) for _ in range(6000)]
+    fdb = po.FlatDb.from_list(seqs)
+    q = synth.random_residues(rng, 50)
+    exp = port.score_all(q, fdb, b62, 10, 2)
+    with Database(fdb.codes, fdb.offsets) as db:
+        for k in (1024, 1500, 6000):
+            idx, sc, _ = db.search(q, b62, g, k)
+            ni, ns = naive_rank(exp, k)
+            assert (idx == ni).all() and (sc == ns).all(), k
+
+
+def test_empty_database_and_empty_query(b62):
+    g = GapModel(10, 2)
+    with Database(np.zeros(0, np.uint8), np.zeros(1, np.uint64)) as db:
+        idx, sc, _ = db.search(enc("AAA"), b62, g, 10)
+        assert len(idx) == 0 and len(sc) == 0
+    rng = np.random.default_rng(15)
+    seqs = [synth.random_residues(rng, 30) for _ in range(12)]
+    with Database.from_sequences(seqs) as db:
+        idx, sc, _ = db.search(enc(""), b62, g, 5)                            # empty query: all zeros, index order
+        assert idx.tolist() == [0, 1, 2, 3, 4] and sc.tolist() == [0] * 5
+        with pytest.raises(IndexError, match="query code outside matrix alphabet"):
+            db.search(np.array([1, 2, 24], np.uint8), b62, g, 5)
+        with pytest.raises(ValueError, match="top_k must be >= 1"):
+            db.search(enc("AAA"), b62, g, 0)
+    with pytest.raises(IndexError):                                            # subject residue outside the alphabet
+        Database.from_sequences([np.array([3, 99], np.uint8)])
+
+
+def test_long_query_profile_from_global_memory(port, b62):
+    """m = 9,600: the int8 profile (25 x m) no longer fits the 227 KB of shared memory."""
+    rng = np.random.default_rng(16)
+    q = synth.random_residues(rng, 9600)
+    seqs = [synth.random_residues(rng, int(rng.integers(1, 260))) for _ in range(70)]
+    seqs[5] = q[4000:4200].copy()
+    fdb = po.FlatDb.from_list(seqs)
+    with Database(fdb.codes, fdb.offsets) as db:
+        got, _ = db.score_all(q, b62, GapModel(10, 2))
+        assert (got == port.score_all(q, fdb, b62, 10, 2)).all()
+
+
+def test_intra_task_multi_pass_and_long_subject(port, b62):
+    """Query wider than one intra-task pass (8 warps x 32 lanes x 8 columns = 2048) and a long subject."""
+    rng = np.random.default_rng(17)
+    q = synth.random_residues(rng, 4700)
+    s = synth.mutate(rng, q, 0.3, 4)
+    s = np.concatenate([synth.random_residues(rng, 800), s, synth.random_residues(rng, 1500)])
+    exp = port.score_scalar(q, s, b62, 10, 2)
+    assert score_wavefront(q, s, b62, GapModel(10, 2), 64) == exp
+    assert score_wavefront(s, q, b62, GapModel(10, 2), 1) == port.score_scalar(s, q, b62, 10, 2)
+    # the same pair through the database path with a wavefront of units (threshold 0 -> long pool)
+    with Database.from_sequences([s, q[:100]], length_threshold=0) as db:
+        got, st = db.score_all(q, b62, GapModel(10, 2))
+        assert got[0] == exp and st["wavefront_scored"] == 2
+
+
+def test_multi_shard_equals_single(port, b62):
+    """Scheduling invisibility, GPU edition: shard counts 1/2/3/8 give the identical ranked list."""
+    qs, sdb = synth.config1()
+    g = GapModel(10, 2)
+    with Database(sdb.codes, sdb.offsets) as db:
+        i1, s1, _ = db.search(qs[0], b62, g, 25)
+    for shards in (2, 3, 8):
+        mdb = MultiGpuDatabase(sdb.codes, sdb.offsets, [0] * shards)
+        i2, s2, st = mdb.search(qs[0], b62, g, 25)
+        mdb.close()
+        assert (i1 == i2).all() and (s1 == s2).all()
+        assert st["lane_scored"] + st["wavefront_scored"] == sdb.n
+        # the per-rank flavour: every shard's keys, merged on the device
+        keys = []
+        total = np.full(sdb.n, -1, dtype=np.int32)
+        for r in range(shards):
+            with Database(sdb.codes, sdb.offsets, shard_rank=r, shard_count=shards) as part:
+                k, _, _ = part.search_keys(qs[0], b62, g, 25)
+                keys.append(k)
+                part.score_all(qs[0], b62, g, out=total)
+        i3, s3 = merge_keys(np.concatenate(keys), 25)
+        assert (i1 == i3).all() and (s1 == s3).all()
+        assert (total >= 0).all()            # every sequence was scored by exactly one shard
+    i4, s4 = decode_keys(keys[0])
+    assert len(i4) <= 25

@@ -1,0 +1,110 @@
+"""CPU-side checks: the C-ABI library builds, loads and exports every symbol include/swb200.h declares
+(no compute without a GPU), argument validation that happens before any CUDA call, the deterministic
+sharding rule, the packed-key encoding, the synthetic data generator."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2203_11100_b200 import _cabi, search, synth
+from tests._util import enc
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_library_exports_every_declared_symbol(lib):
+    header = (ROOT / "include" / "swb200.h").read_text()
+    declared = set(re.findall(r"\b(swb_[a-z0-9_]+)\s*\(", header))
+    declared -= {"swb_status"}
+    assert len(declared) >= 20
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"libswb200.so does not export {name}"
+        assert name in _cabi.SIGNATURES, f"{name} has no ctypes signature"
+    assert lib.swb_version().decode().startswith("swb200")
+
+
+def test_no_cpu_fallback_without_gpu(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    A = enc("AAA")
+    with pytest.raises(search.SwbError):
+        search.Database.from_sequences([A])
+    with pytest.raises(search.SwbError):
+        search.score_wavefront(A, A, synth.blosum62(), search.GapModel(10, 2), 4)
+    with pytest.raises(search.SwbError):
+        search.score_batch(A, [A], 4, synth.blosum62(), search.GapModel(10, 2))
+
+
+def test_validation_before_cuda(lib, b62):
+    A = enc("AAA")
+    g = search.GapModel(10, 2)
+    with pytest.raises(ValueError, match="lane_width must be >= 1"):       # align.hpp:93
+        search.score_batch(A, [], 0, b62, g)
+    with pytest.raises(ValueError, match="more subjects than lanes"):      # align.hpp:94-95
+        search.score_batch(A, [A, A], 1, b62, g)
+    with pytest.raises(ValueError, match="chunk_width must be >= 1"):      # align.hpp:169
+        search.score_wavefront(A, A, b62, g, 0)
+    with pytest.raises(IndexError, match="query code outside matrix alphabet"):   # scoring.hpp:203-205
+        search.score_wavefront(np.array([24], np.uint8), A, b62, g, 4)
+    with pytest.raises(ValueError, match="open >= extend >= 0"):           # scoring.hpp:51-52
+        search.GapModel(1, 2)
+    with pytest.raises(ValueError):
+        search.GapModel(3, -1)
+    for bad in (dict(worker_count=0), dict(lane_width=0), dict(chunk_width=0), dict(top_k=0)):
+        with pytest.raises(ValueError, match="must be >= 1"):              # scheduler.hpp:30-35
+            search.SearchConfig(**bad).validate()
+    # degenerate inputs are not errors (align.hpp:45,100,172)
+    assert search.score_wavefront(enc(""), A, b62, g, 4) == 0
+    assert search.score_wavefront(A, enc(""), b62, g, 4) == 0
+    assert search.score_batch(enc(""), [A], 2, b62, g).tolist() == [0, 0]
+    assert search.score_batch(A, [], 3, b62, g).tolist() == [0, 0, 0]
+
+
+def test_shard_assignment_balanced_and_deterministic(lib):
+    rng = np.random.default_rng(3)
+    lens = synth.random_lengths(rng, 20000, 7_200_000, 35213)
+    for shards in (1, 2, 4, 8):
+        a = search.shard_assignment(lens, 3000, shards)
+        b = search.shard_assignment(lens, 3000, shards)
+        assert (a == b).all() and a.max() == shards - 1
+        res = np.array([lens[a == r].sum() for r in range(shards)], dtype=np.float64)
+        cnt = np.array([(a == r).sum() for r in range(shards)])
+        assert cnt.max() - cnt.min() <= 2
+        assert res.max() / res.mean() < 1.02, res          # residue-balanced to 2 %
+        long_cnt = np.array([((a == r) & (lens >= 3000)).sum() for r in range(shards)])
+        assert long_cnt.max() - long_cnt.min() <= 1        # every shard gets its share of the long pool
+    assert (search.shard_assignment(lens, 3000, 1) == 0).all()
+    assert len(search.shard_assignment(np.zeros(0, np.uint32), 3000, 4)) == 0
+
+
+def test_key_encoding_orders_like_merge_results(port):
+    rng = np.random.default_rng(4)
+    idx = rng.permutation(5000).astype(np.uint32)
+    sc = rng.integers(0, 40, size=5000).astype(np.int32)          # many ties
+    keys = search.encode_keys(idx, sc)
+    order = np.argsort(keys)[::-1]
+    oi, os_ = port.merge(idx, sc, 5000)                             # scheduler.hpp:111-114
+    assert (idx[order] == oi).all() and (sc[order] == os_).all()
+    di, ds = search.decode_keys(keys)
+    assert (di == idx).all() and (ds == sc).all()
+    assert (keys != 0).all()                                        # 0 is reserved as padding
+
+
+def test_synth_is_deterministic_and_shaped():
+    q1, d1 = synth.config1()
+    q2, d2 = synth.config1()
+    assert (d1.codes == d2.codes).all() and (d1.offsets == d2.offsets).all() and (q1[0] == q2[0]).all()
+    assert d1.n == 10000 and len(q1[0]) == 144
+    lens = d1.lengths()
+    assert lens.max() == synth.SWISSPROT_MAXLEN and (lens == 0).sum() >= 2 and (lens == 1).sum() >= 2
+    assert 3.3e6 < d1.residues < 3.9e6
+    assert d1.codes.max() <= 22 and (d1.codes >= 20).mean() < 0.005
+    exact = d1.planted[0][0]
+    assert (d1.seq(exact) == q1[0]).all()
+    assert (synth.blosum50() == synth.blosum50().T).all()
+    assert synth.QUERY_LENGTHS[0] == 144 and synth.QUERY_LENGTHS[-1] == 5478 and len(synth.QUERY_LENGTHS) == 20
+    # the GCUPS identity of SPEC.md:370
+    assert abs(144 * synth.SWISSPROT_RESIDUES / 1.0 / 1e9 - 29.4009) < 1e-3
