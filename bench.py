@@ -113,7 +113,7 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------------------
 # CPU reference leg
 # ------------------------------------------------------------------------------------------------------------
-def cpu_sample(queries, sdb, seed=7, n_seqs=6000, query_ids=(0, 9, 19)):
+def cpu_sample(queries, sdb, seed=7, n_seqs=20000, query_ids=(0, 9, 19)):
     """A bounded sample of the workload: a seeded subsample of the database (with one long sequence) and three
     of the twenty queries."""
     rng = np.random.default_rng(seed)
