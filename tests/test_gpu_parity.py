@@ -111,20 +111,22 @@ def test_config1_against_reference_itself(ref, b62):
 
 
 def test_int16_overflow_is_rerun_in_int32(port, b62):
+    """Scores beyond the packed kernels' trusted range (32767 - max(matrix) for the int16 kernel, 65535 - bias -
+    max(matrix) for the unsigned variant) must come back exact from the int32 re-run (align.hpp:149-153)."""
     rng = np.random.default_rng(12)
-    q = synth.random_residues(rng, 4000)
+    q = synth.random_residues(rng, 8000)
     q[::2] = 17          # W: 11 per match
     q[1::4] = 4          # C: 9 per match
-    seqs = [q.copy(), synth.random_residues(rng, 500), q[:3500].copy(), synth.mutate(rng, q, 0.02, 2)]
+    seqs = [q.copy(), synth.random_residues(rng, 500), q[:3500].copy(), synth.mutate(rng, q, 0.02, 2), q[:5000].copy()]
     seqs += [synth.random_residues(rng, int(rng.integers(0, 900))) for _ in range(150)]
     fdb = po.FlatDb.from_list(seqs)
     exp = port.score_all(q, fdb, b62, 10, 2)
-    assert exp.max() > 32767
+    assert exp.max() > 65535 and ((exp > 32767) & (exp < 65535)).any()
     for thr in (10 ** 9, 3000, 0):
         with Database(fdb.codes, fdb.offsets, length_threshold=thr) as db:
             got, st = db.score_all(q, b62, GapModel(10, 2))
             assert (got == exp).all()
-            assert st["rescored_i32"] >= 1
+            assert st["rescored_i32"] >= 2
 
 
 def test_wide_mode_matrix_outside_int8(port, b62):
