@@ -69,6 +69,8 @@ struct QueryPlan {
     int32_t limit = 0;
     int32_t open = 0, ext = 0;
     uint32_t m = 0;
+    uint32_t tile = kInterTile; // query columns per register tile of the packed kernel
+    uint32_t threads = kInterThreads;
     uint32_t pstride = 0;       // inter profile row stride
     uint32_t intra_t = 8, n_lane_tiles = 0, intra_w = 1, intra_passes = 0;
 };
@@ -124,6 +126,7 @@ struct swb_db {
     cudaEvent_t ev[EV_COUNT] = {};
     uint32_t launches = 0;
     uint32_t last_units = 0;
+    uint32_t last_tile = kInterTile;
     bool smem_attr_set = false;
 };
 
@@ -224,8 +227,21 @@ QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t
     const uint64_t reach = static_cast<uint64_t>(top) * std::min<uint64_t>(m, db->meta.max_length);
     pl.may_overflow = reach > static_cast<uint64_t>(pl.limit);
 
-    // wavefront profile stride: columns padded to the 32-column tile, then to 16 (mod 128) bytes
-    const uint32_t mpad = std::max<uint32_t>(32, (m + 31) / 32 * 32);
+    // register-tile geometry of the s16 kernel (SWB200_TILE = "<columns>x<threads>", for tuning)
+    static const std::pair<uint32_t, uint32_t> geometry = [] {
+        const char* e = std::getenv("SWB200_TILE");
+        const std::string v = e ? e : "";
+        if (v == "32x384") return std::make_pair(32u, 384u);
+        if (v == "48x384") return std::make_pair(48u, 384u);
+        if (v == "16x1024") return std::make_pair(16u, 1024u);
+        if (v == "16x768") return std::make_pair(16u, 768u);
+        if (v == "32x512") return std::make_pair(32u, 512u);
+        return std::make_pair(static_cast<uint32_t>(kInterTile), static_cast<uint32_t>(kInterThreads));
+    }();
+    pl.tile = pl.main == kMainS16 ? geometry.first : kInterTile;
+    pl.threads = pl.main == kMainS16 ? geometry.second : kInterThreads;
+    // wavefront profile stride: columns padded to whole tiles, then to 16 (mod 128) bytes
+    const uint32_t mpad = std::max<uint32_t>(pl.tile, (m + pl.tile - 1) / pl.tile * pl.tile);
     pl.pstride = mpad + ((16 + 128 - (mpad % 128)) % 128);
 
     // intra-task geometry: T columns per lane (4..8), W warps per CTA, passes
@@ -305,6 +321,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     const QueryPlan pl = make_plan(db, m, matrix, open, ext);
     db->launches = 0;
     db->last_units = 0;
+    db->last_tile = pl.tile;
     SWB_CUDA(cudaEventRecord(db->ev[EV_START], s));
     SWB_CUDA(cudaMemsetAsync(db->d_slot_scores, 0, std::max<size_t>(db->n_slots, 1) * sizeof(int32_t), s));
     SWB_CUDA(cudaMemsetAsync(db->d_counters, 0, 4 * sizeof(uint32_t), s));
@@ -333,7 +350,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     }
     std::memcpy(db->h_stage, matrix, off_query);
     std::memcpy(db->h_stage + off_query, query, m);
-    const uint32_t n_tiles = (m + kInterTile - 1) / kInterTile;
+    const uint32_t n_tiles = (m + pl.tile - 1) / pl.tile;
     uint32_t n_units = 0;
     if (packed) {
         // Unit policy: a group whose whole (rows x tiles) sweep exceeds the budget -- a fraction of one
@@ -341,7 +358,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         // everything else is a single unit scored end to end by one warp.
         uint32_t* us = reinterpret_cast<uint32_t*>(db->h_stage + off_units);
         const uint64_t total_row_tiles = db->meta.padded_rows * n_tiles;
-        const uint64_t warps = static_cast<uint64_t>(db->sm_count) * (kInterThreads / 32);
+        const uint64_t warps = static_cast<uint64_t>(db->sm_count) * (pl.threads / 32);
         const uint64_t budget = std::max<uint64_t>(4096, static_cast<uint64_t>(unit_budget_fraction() * total_row_tiles / warps));
         for (uint32_t g = 0; g < n_groups; ++g) {
             us[g] = n_units;
@@ -409,22 +426,35 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.one = 1;
         wp.bias = pl.bias;
         const size_t smem = prof_elems;
-        const uint32_t warps_per_cta = kInterThreads / 32;
+        const uint32_t warps_per_cta = pl.threads / 32;
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(db->sm_count, (n_units + warps_per_cta - 1) / warps_per_cta));
         const bool in_smem = smem <= db->smem_optin;
-        if (in_smem && !db->smem_attr_set) {
-            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(db->smem_optin)));
-            SWB_CUDA(cudaFuncSetAttribute(wavefront_u16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(db->smem_optin)));
-            db->smem_attr_set = true;
-        }
         if (pl.main == kMainU16) {
-            if (in_smem) wavefront_u16_kernel<true><<<grid, kInterThreads, smem, s>>>(wp);
-            else wavefront_u16_kernel<false><<<grid, kInterThreads, 0, s>>>(wp);
+            if (in_smem) {
+                SWB_CUDA(cudaFuncSetAttribute(wavefront_u16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(db->smem_optin)));
+                wavefront_u16_kernel<true><<<grid, kInterThreads, smem, s>>>(wp);
+            } else {
+                wavefront_u16_kernel<false><<<grid, kInterThreads, 0, s>>>(wp);
+            }
         } else {
-            if (in_smem) wavefront_s16_kernel<true><<<grid, kInterThreads, smem, s>>>(wp);
-            else wavefront_s16_kernel<false><<<grid, kInterThreads, 0, s>>>(wp);
+#define SWB_LAUNCH_S16(TT, TH)                                                                                     \
+    if (pl.tile == TT && pl.threads == TH) {                                                                       \
+        if (in_smem) {                                                                                             \
+            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, TT, TH>,                                      \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,                             \
+                                          static_cast<int>(db->smem_optin)));                                      \
+            wavefront_s16_kernel<true, TT, TH><<<grid, TH, smem, s>>>(wp);                                         \
+        } else {                                                                                                   \
+            wavefront_s16_kernel<false, TT, TH><<<grid, TH, 0, s>>>(wp);                                           \
+        }                                                                                                          \
+    }
+            SWB_LAUNCH_S16(32, 512)
+            SWB_LAUNCH_S16(32, 384)
+            SWB_LAUNCH_S16(48, 384)
+            SWB_LAUNCH_S16(16, 1024)
+            SWB_LAUNCH_S16(16, 768)
+#undef SWB_LAUNCH_S16
         }
         ++db->launches;
     }
@@ -503,7 +533,7 @@ void fill_stats(swb_db* db, uint32_t m, swb_stats* st) {
     st->chunks_claimed = db->last_units ? db->last_units : db->meta.n_local;
     st->rescored_i32 = db->h_counters ? db->h_counters[1] : 0;
     st->cells = static_cast<uint64_t>(m) * db->meta.residues;
-    const uint64_t mpad = (static_cast<uint64_t>(m) + kInterTile - 1) / kInterTile * kInterTile;
+    const uint64_t mpad = (static_cast<uint64_t>(m) + db->last_tile - 1) / db->last_tile * db->last_tile;
     st->padded_cells = mpad * db->meta.padded_rows * kGroupSeqs;
     st->kernel_launches = db->launches;
     auto span = [&](int a, int b) {

@@ -121,7 +121,7 @@ struct WaveParams {
     uint32_t n_units;
     const int8_t* prof8;
     uint32_t pstride;
-    uint32_t n_tiles;             // ceil(m / 32)
+    uint32_t n_tiles;             // ceil(m / T)
     uint2* border0;
     uint2* border1;
     int32_t* slot_scores;         // [n_groups*64], zeroed per search, updated with atomicMax
@@ -142,9 +142,13 @@ struct WaveParams {
 // cooperating warps); the host decides per search (unit_budget in cabi.cu) and the kernel reads the
 // decision back from unit_start.
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+// Polling load of a progress counter.  Relaxed on purpose: an acquire load makes ptxas invalidate the whole
+// L1 (CCTL.IVALL) on every poll.  Ordering is still safe here: the data the counter guards is only ever read
+// with ld.global.cg (served by L2, the point of coherence), those loads are issued after the poll loop's branch
+// has resolved, and the producer's release store made its border rows visible at L2 before the counter.
+__device__ __forceinline__ uint32_t ld_poll(const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -152,9 +156,8 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <bool kSmemProfile>
-__global__ void __launch_bounds__(kInterThreads, 1) wavefront_s16_kernel(WaveParams p) {
-    constexpr int T = kInterTile;
+template <bool kSmemProfile, int T, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p) {
     extern __shared__ __align__(16) uint8_t smem_prof[];
 
     const int8_t* prof;
@@ -187,6 +190,7 @@ __global__ void __launch_bounds__(kInterThreads, 1) wavefront_s16_kernel(WavePar
         }
         const uint32_t g = lo;
         const GroupDesc gd = p.groups[g];
+        const uint32_t rows = gd.n_chunks * kRowsPerChunk;
         const uint32_t u0 = __ldg(p.unit_start + g);
         const bool split = __ldg(p.unit_start + g + 1) - u0 > 1;
         const uint32_t t0 = split ? u - u0 : 0;
@@ -211,22 +215,25 @@ __global__ void __launch_bounds__(kInterThreads, 1) wavefront_s16_kernel(WavePar
             for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
             uint32_t diag_in = NO;
             uint4 cw = gd.n_chunks ? __ldg(gcodes) : make_uint4(0, 0, 0, 0);
-            // inbound border of the row about to be processed; a tile that does not wait on another unit
-            // prefetches across chunk boundaries
-            uint2 bnext = make_uint2(NO, NO);
-            if (!first && !wait && gd.n_chunks) bnext = __ldcg(bin);
+            // inbound border rows are fetched two rows ahead of their use (q0: the row about to be processed,
+            // q1: the one after); a waiting tile stays two chunks behind its producer so that this look-ahead
+            // never reads an unpublished row
+            uint2 q0 = make_uint2(NO, NO), q1 = make_uint2(NO, NO);
 
             for (uint32_t chunk = 0; chunk < gd.n_chunks; ++chunk) {
                 const uint4 cur = cw;
                 if (chunk + 1 < gd.n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
                 const size_t row0 = static_cast<size_t>(chunk) * kRowsPerChunk;
                 if (wait) {
-                    const uint32_t need = static_cast<uint32_t>(row0) + kRowsPerChunk;
+                    const uint32_t need = min(rows, static_cast<uint32_t>(row0) + 2 * kRowsPerChunk);
                     if (lane == 0)
-                        while (ld_acquire(dep) < need) __nanosleep(40);
+                        while (ld_poll(dep) < need) __nanosleep(64);
                     __syncwarp();
                 }
-                if (wait) bnext = __ldcg(bin + row0 * 32);
+                if (!first && chunk == 0) {
+                    q0 = __ldcg(bin);
+                    q1 = __ldcg(bin + 32);     // rows are padded to whole chunks: row 1 always exists
+                }
 #pragma unroll
                 for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
                     const uint32_t wa = r < 4 ? cur.x : cur.y;
@@ -243,13 +250,9 @@ __global__ void __launch_bounds__(kInterThreads, 1) wavefront_s16_kernel(WavePar
                         wB[4 * i] = vb.x, wB[4 * i + 1] = vb.y, wB[4 * i + 2] = vb.z, wB[4 * i + 3] = vb.w;
                     }
                     const size_t row = row0 + r;
-                    const uint2 bi = bnext;
-                    // the next row's inbound border; across a chunk boundary only when this tile does not
-                    // wait on another unit (the next chunk's rows may not have been published yet)
-                    if (!first) {
-                        const bool in_chunk = r + 1 < static_cast<int>(kRowsPerChunk);
-                        if (in_chunk || (!wait && chunk + 1 < gd.n_chunks)) bnext = __ldcg(bin + (row + 1) * 32);
-                    }
+                    const uint2 bi = q0;
+                    q0 = q1;
+                    if (!first && row + 2 < rows) q1 = __ldcg(bin + (row + 2) * 32);
                     uint32_t hl = bi.x;   // Hm of the column left of the tile, this row
                     uint32_t E = bi.y;
                     uint32_t diag = diag_in;
@@ -285,10 +288,7 @@ __global__ void __launch_bounds__(kInterThreads, 1) wavefront_s16_kernel(WavePar
                 }
                 if (publish) {
                     __syncwarp();
-                    if (lane == 0) {
-                        __threadfence();
-                        st_release(pub, static_cast<uint32_t>(row0) + kRowsPerChunk);
-                    }
+                    if (lane == 0) st_release(pub, static_cast<uint32_t>(row0) + kRowsPerChunk);
                 }
             }
         }
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kInterThreads, 1) wavefront_u16_kernel(WavePar
                 if (wait) {
                     const uint32_t need = static_cast<uint32_t>(row0) + kRowsPerChunk;
                     if (lane == 0)
-                        while (ld_acquire(dep) < need) __nanosleep(40);
+                        while (ld_poll(dep) < need) __nanosleep(40);
                     __syncwarp();
                     bnext = __ldcg(bin + row0 * 32);
                 }
