@@ -103,6 +103,7 @@ struct swb_db {
     uint32_t* d_flag_list = nullptr;
     uint32_t* d_counters = nullptr;   // [0] ticket, [1] flag count
     uint32_t* d_unit_start = nullptr;
+    uint8_t* d_group_mode = nullptr;
     uint32_t* d_progress = nullptr;
     size_t progress_cap = 0;
     uint64_t* d_keys = nullptr;
@@ -196,6 +197,16 @@ double unit_budget_fraction() {
     return f;
 }
 
+// A group goes to 8-column tiles when its rows exceed this fraction of a warp's fair share (in row-tiles).
+double narrow_chain_fraction() {
+    static const double f = [] {
+        const char* e = std::getenv("SWB200_NARROW");
+        const double v = e ? std::atof(e) : 0.0;
+        return v > 0.0 ? v : 0.9;
+    }();
+    return f;
+}
+
 QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext) {
     QueryPlan pl;
     pl.m = m;
@@ -233,8 +244,6 @@ QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t
         const std::string v = e ? e : "";
         if (v == "32x384") return std::make_pair(32u, 384u);
         if (v == "48x384") return std::make_pair(48u, 384u);
-        if (v == "16x1024") return std::make_pair(16u, 1024u);
-        if (v == "16x768") return std::make_pair(16u, 768u);
         if (v == "32x512") return std::make_pair(32u, 512u);
         return std::make_pair(static_cast<uint32_t>(kInterTile), static_cast<uint32_t>(kInterThreads));
     }();
@@ -338,7 +347,8 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     // ---- stage matrix + query (+ the unit table of the wavefront kernel) and upload -----------------
     const size_t off_query = 576 * sizeof(int32_t);
     const size_t off_units = (off_query + m + 15) & ~size_t(15);
-    const size_t stage_bytes = off_units + (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t);
+    const size_t off_modes = off_units + (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t);
+    const size_t stage_bytes = off_modes + n_groups;
     swb_status st = ensure_stage(db, stage_bytes);
     if (st != SWB_OK) return st;
     if (m > db->query_cap) {
@@ -351,23 +361,39 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     std::memcpy(db->h_stage, matrix, off_query);
     std::memcpy(db->h_stage + off_query, query, m);
     const uint32_t n_tiles = (m + pl.tile - 1) / pl.tile;
+    const uint32_t n_tiles_narrow = (m + kNarrowTile - 1) / kNarrowTile;
     uint32_t n_units = 0;
+    bool any_narrow = false;
     if (packed) {
-        // Unit policy: a group whose whole (rows x tiles) sweep exceeds the budget -- a fraction of one
-        // warp's fair share of the search -- is split into one unit per tile (a wavefront of warps);
-        // everything else is a single unit scored end to end by one warp.
+        // Unit policy (see kernels.cuh, GroupMode).  Work is counted in row-tiles (one row of one T-column tile).
+        //   single  the default: one warp scores the group's 64 sequences end to end;
+        //   split   the group's whole sweep exceeds `budget`, a fraction of one warp's fair share of the search:
+        //           one unit per tile, so that no unit dominates the makespan;
+        //   narrow  even a split group's per-tile chain (rows x T columns, strictly sequential in one thread,
+        //           ~900 clk per row when the SM empties out, against ~1600 clk per row-tile of saturated
+        //           throughput) would take more than about half the whole search: 8-column tiles cut that
+        //           chain four-fold.  Only the s16 kernel implements it.
         uint32_t* us = reinterpret_cast<uint32_t*>(db->h_stage + off_units);
+        uint8_t* modes = db->h_stage + off_modes;
         const uint64_t total_row_tiles = db->meta.padded_rows * n_tiles;
         const uint64_t warps = static_cast<uint64_t>(db->sm_count) * (pl.threads / 32);
-        const uint64_t budget = std::max<uint64_t>(4096, static_cast<uint64_t>(unit_budget_fraction() * total_row_tiles / warps));
+        const uint64_t fair = total_row_tiles / warps;
+        const uint64_t budget = std::max<uint64_t>(4096, static_cast<uint64_t>(unit_budget_fraction() * fair));
+        const uint64_t narrow_rows = std::max<uint64_t>(2048, static_cast<uint64_t>(narrow_chain_fraction() * fair));
         for (uint32_t g = 0; g < n_groups; ++g) {
             us[g] = n_units;
-            const uint64_t work = static_cast<uint64_t>(db->meta.groups[g].n_chunks) * kRowsPerChunk * n_tiles;
-            n_units += (work > budget && n_tiles > 1) ? n_tiles : 1;
+            const uint64_t rows = static_cast<uint64_t>(db->meta.groups[g].n_chunks) * kRowsPerChunk;
+            uint8_t mode = kGroupSingle;
+            if (rows * n_tiles > budget && n_tiles > 1) mode = kGroupSplit;
+            if (pl.main == kMainS16 && rows > narrow_rows && n_tiles_narrow > 1) mode = kGroupNarrow;
+            modes[g] = mode;
+            any_narrow |= mode == kGroupNarrow;
+            n_units += mode == kGroupSingle ? 1 : (mode == kGroupSplit ? n_tiles : n_tiles_narrow);
         }
         us[n_groups] = n_units;
         SWB_CUDA(cudaMemcpyAsync(db->d_unit_start, us, (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, s));
+        SWB_CUDA(cudaMemcpyAsync(db->d_group_mode, modes, std::max<size_t>(n_groups, 1), cudaMemcpyHostToDevice, s));
         if ((st = ensure_dev(&db->d_progress, &db->progress_cap, n_units, &db->device_bytes)) != SWB_OK) return st;
         SWB_CUDA(cudaMemsetAsync(db->d_progress, 0, static_cast<size_t>(n_units) * sizeof(uint32_t), s));
         db->last_units = n_units;
@@ -408,7 +434,9 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.groups = db->d_groups;
         wp.n_groups = n_groups;
         wp.unit_start = db->d_unit_start;
+        wp.group_mode = db->d_group_mode;
         wp.n_units = n_units;
+        wp.n_tiles_narrow = n_tiles_narrow;
         wp.prof8 = db->d_prof8;
         wp.pstride = pl.pstride;
         wp.n_tiles = n_tiles;
@@ -438,22 +466,25 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
                 wavefront_u16_kernel<false><<<grid, kInterThreads, 0, s>>>(wp);
             }
         } else {
-#define SWB_LAUNCH_S16(TT, TH)                                                                                     \
-    if (pl.tile == TT && pl.threads == TH) {                                                                       \
+#define SWB_LAUNCH_S16_N(TT, TH, NARROW)                                                                           \
+    {                                                                                                              \
         if (in_smem) {                                                                                             \
-            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, TT, TH>,                                      \
+            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, TT, TH, NARROW>,                              \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,                             \
                                           static_cast<int>(db->smem_optin)));                                      \
-            wavefront_s16_kernel<true, TT, TH><<<grid, TH, smem, s>>>(wp);                                         \
+            wavefront_s16_kernel<true, TT, TH, NARROW><<<grid, TH, smem, s>>>(wp);                                 \
         } else {                                                                                                   \
-            wavefront_s16_kernel<false, TT, TH><<<grid, TH, 0, s>>>(wp);                                           \
+            wavefront_s16_kernel<false, TT, TH, NARROW><<<grid, TH, 0, s>>>(wp);                                   \
         }                                                                                                          \
+    }
+#define SWB_LAUNCH_S16(TT, TH)                                                                                     \
+    if (pl.tile == TT && pl.threads == TH) {                                                                       \
+        if (any_narrow) SWB_LAUNCH_S16_N(TT, TH, true) else SWB_LAUNCH_S16_N(TT, TH, false)                        \
     }
             SWB_LAUNCH_S16(32, 512)
             SWB_LAUNCH_S16(32, 384)
             SWB_LAUNCH_S16(48, 384)
-            SWB_LAUNCH_S16(16, 1024)
-            SWB_LAUNCH_S16(16, 768)
+#undef SWB_LAUNCH_S16_N
 #undef SWB_LAUNCH_S16
         }
         ++db->launches;
@@ -570,6 +601,7 @@ swb_status upload_db(swb_db* db) {
     if ((st = dev_alloc(&db->d_flag_list, db->n_slots, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_counters, 4, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_unit_start, m.groups.size() + 1, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_group_mode, m.groups.size() + 1, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_keys, db->n_slots, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_matrix, 576, tally)) != SWB_OK) return st;
     // the bulk host copy is no longer needed
@@ -699,7 +731,7 @@ void swb_db_destroy(swb_db* db) {
         if (db->own_stream) cudaStreamSynchronize(db->own_stream);
         void* ptrs[] = {db->d_codes,      db->d_groups,   db->d_slot_index, db->d_slot_len,    db->d_border0,
                         db->d_border1,    db->d_iborder0, db->d_iborder1,   db->d_slot_scores, db->d_flag_list,
-                        db->d_counters,   db->d_unit_start, db->d_progress, db->d_keys,        db->d_sel[0],
+                        db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_progress, db->d_keys,        db->d_sel[0],
                         db->d_sel[1],     db->d_sort,     db->d_all_scores, db->d_query,       db->d_matrix,
                         db->d_prof8,      db->d_prof8i,   db->d_prof32i};
         for (void* p : ptrs)

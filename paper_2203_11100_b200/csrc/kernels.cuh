@@ -118,7 +118,9 @@ struct WaveParams {
     const GroupDesc* groups;
     uint32_t n_groups;
     const uint32_t* unit_start;   // [n_groups + 1] first unit of each group
+    const uint8_t* group_mode;    // [n_groups] GroupMode
     uint32_t n_units;
+    uint32_t n_tiles_narrow;      // ceil(m / 8): tiles of a kGroupNarrow group
     const int8_t* prof8;
     uint32_t pstride;
     uint32_t n_tiles;             // ceil(m / T)
@@ -156,7 +158,141 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <bool kSmemProfile, int T, int kThreads>
+// One unit: tiles [t0, t1) of `n_tiles` tiles of width T over all rows of group `gd`.
+//   dep  progress counter of the unit to the left (nullptr: none), pub: this unit's counter (nullptr: no consumer)
+//   D    border look-ahead in rows (a power of two <= 8), P: publish progress every P chunks
+template <int T, int D, int P>
+__device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const int8_t* prof, const GroupDesc& gd,
+                                                   uint32_t t0, uint32_t t1, uint32_t n_tiles, const uint32_t* dep,
+                                                   uint32_t* pub, uint32_t lane) {
+    static_assert(T % 8 == 0, "tile width must be a multiple of 8 columns");
+    const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
+    const uint32_t rows = gd.n_chunks * kRowsPerChunk;
+    const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
+    const size_t brow0 = static_cast<size_t>(gd.chunk_base) * kRowsPerChunk * 32 + lane;
+    uint32_t best = 0;
+
+    for (uint32_t tile = t0; tile < t1; ++tile) {
+        const int8_t* ptile = prof + tile * T;
+        const bool first = tile == 0, last = tile + 1 == n_tiles;
+        const bool wait = dep != nullptr && tile == t0;
+        const bool publish = pub != nullptr && tile + 1 == t1;
+        const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + brow0;
+        uint2* bout = ((tile & 1) ? p.border1 : p.border0) + brow0;
+
+        uint32_t Hm[T], F[T];
+#pragma unroll
+        for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
+        uint32_t diag_in = NO;
+        uint4 cw = gd.n_chunks ? __ldg(gcodes) : make_uint4(0, 0, 0, 0);
+        // inbound border rows are fetched D rows ahead of their use (q[i]: row = i mod D); a waiting tile stays
+        // far enough behind its producer that this look-ahead never reads an unpublished row
+        uint2 q[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) q[i] = make_uint2(NO, NO);
+        uint32_t known = 0;   // producer progress observed so far
+
+        for (uint32_t chunk = 0; chunk < gd.n_chunks; ++chunk) {
+            const uint4 cur = cw;
+            if (chunk + 1 < gd.n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
+            const size_t row0 = static_cast<size_t>(chunk) * kRowsPerChunk;
+            if (wait) {
+                const uint32_t need = min(rows, static_cast<uint32_t>(row0) + kRowsPerChunk + D);
+                if (P == 1) {          // the producer publishes every chunk: poll every chunk, keep no state
+                    if (lane == 0)
+                        while (ld_poll(dep) < need) __nanosleep(64);
+                    __syncwarp();
+                } else if (known < need) {
+                    if (lane == 0)
+                        while ((known = ld_poll(dep)) < need) __nanosleep(64);
+                    known = __shfl_sync(0xffffffffu, known, 0);
+                }
+            }
+            if (!first && chunk == 0) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) q[i] = __ldcg(bin + i * 32);   // rows are padded to whole chunks (>= 8)
+            }
+#pragma unroll
+            for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
+                const uint32_t wa = r < 4 ? cur.x : cur.y;
+                const uint32_t wb = r < 4 ? cur.z : cur.w;
+                const uint32_t a1 = (wa >> (8 * (r & 3))) & 0xffu;
+                const uint32_t a2 = (wb >> (8 * (r & 3))) & 0xffu;
+                const int8_t* pa = ptile + a1 * p.pstride;
+                const int8_t* pb = ptile + a2 * p.pstride;
+                uint32_t wA[T / 4], wB[T / 4];
+                if (T % 16 == 0) {
+#pragma unroll
+                    for (int i = 0; i < T / 16; ++i) {
+                        const uint4 va = reinterpret_cast<const uint4*>(pa)[i], vb = reinterpret_cast<const uint4*>(pb)[i];
+                        wA[4 * i] = va.x, wA[4 * i + 1] = va.y, wA[4 * i + 2] = va.z, wA[4 * i + 3] = va.w;
+                        wB[4 * i] = vb.x, wB[4 * i + 1] = vb.y, wB[4 * i + 2] = vb.z, wB[4 * i + 3] = vb.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < T / 8; ++i) {
+                        const uint2 va = reinterpret_cast<const uint2*>(pa)[i], vb = reinterpret_cast<const uint2*>(pb)[i];
+                        wA[2 * i] = va.x, wA[2 * i + 1] = va.y;
+                        wB[2 * i] = vb.x, wB[2 * i + 1] = vb.y;
+                    }
+                }
+                const size_t row = row0 + r;
+                const uint2 bi = q[r % D];
+                if (!first && row + D < rows) q[r % D] = __ldcg(bin + (row + D) * 32);
+                uint32_t hl = bi.x;   // Hm of the column left of the tile, this row
+                uint32_t E = bi.y;
+                uint32_t diag = diag_in;
+                diag_in = hl;
+#pragma unroll
+                for (int k = 0; k < T; k += 2) {
+                    const uint32_t s0 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xC480u : 0xE6A2u);
+                    const uint32_t s1 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xD591u : 0xF7B3u);
+                    // cell k
+                    E = __viaddmax_s16x2(E, NE, hl);
+                    F[k] = __viaddmax_s16x2(F[k], NE, Hm[k]);
+                    const uint32_t d0 = __vadd2(diag, s0);
+                    const uint32_t h0 = __vimax3_s16x2_relu(d0, E, F[k]);
+                    diag = Hm[k];
+                    hl = __vadd2(h0, NO);
+                    Hm[k] = hl;
+                    // cell k+1
+                    E = __viaddmax_s16x2(E, NE, hl);
+                    F[k + 1] = __viaddmax_s16x2(F[k + 1], NE, Hm[k + 1]);
+                    const uint32_t d1 = __vadd2(diag, s1);
+                    const uint32_t h1 = __vimax3_s16x2_relu(d1, E, F[k + 1]);
+                    diag = Hm[k + 1];
+                    hl = __vadd2(h1, NO);
+                    Hm[k + 1] = hl;
+                    // The running maximum is taken over the diagonal terms d, not over H: a cell whose H comes
+                    // from E or F is dominated by an earlier cell (gaps only subtract), so max(H) == max(0, max(d)).
+                    // Giving d this second use also makes the compiler keep the packed add as VIADD.16x2 (FMA
+                    // pipe) + one VIMNMX3 instead of VIADDMNMX + VIMNMX (two ALU-pipe instructions).
+                    best = __vimax3_s16x2(best, d0, d1);
+                }
+                if (!last) bout[row * 32] = make_uint2(hl, E);
+            }
+            if (publish && ((chunk + 1) % P == 0 || chunk + 1 == gd.n_chunks)) {
+                __syncwarp();
+                if (lane == 0) st_release(pub, static_cast<uint32_t>(row0) + kRowsPerChunk);
+            }
+        }
+    }
+    return best;
+}
+
+// Group modes, decided per search by the host (cabi.cu) and uploaded next to unit_start.
+enum GroupMode : uint8_t {
+    kGroupSingle = 0,   // one unit: all tiles of width T, one warp
+    kGroupSplit = 1,    // one unit per tile of width T: a wavefront of warps
+    kGroupNarrow = 2    // one unit per tile of width 8: a wavefront with a 4x shorter per-row chain, for groups whose
+                        // rows x T sequential chain would otherwise outlast the whole search (short query, very
+                        // long sequences)
+};
+constexpr int kNarrowTile = 8;
+
+// kNarrow: compile the 8-column path in.  Searches without narrow groups (all long queries) launch the variant
+// without it, whose register allocation is not disturbed by the second sweep.
+template <bool kSmemProfile, int T, int kThreads, bool kNarrow>
 __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p) {
     extern __shared__ __align__(16) uint8_t smem_prof[];
 
@@ -173,7 +309,6 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
     }
 
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
 
     for (;;) {
         uint32_t u = 0;
@@ -190,108 +325,17 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
         }
         const uint32_t g = lo;
         const GroupDesc gd = p.groups[g];
-        const uint32_t rows = gd.n_chunks * kRowsPerChunk;
         const uint32_t u0 = __ldg(p.unit_start + g);
-        const bool split = __ldg(p.unit_start + g + 1) - u0 > 1;
-        const uint32_t t0 = split ? u - u0 : 0;
-        const uint32_t t1 = split ? t0 + 1 : p.n_tiles;
+        const uint32_t mode = p.group_mode[g];
+        const uint32_t n_tiles = mode == kGroupNarrow ? p.n_tiles_narrow : p.n_tiles;
+        const uint32_t t0 = mode == kGroupSingle ? 0 : u - u0;
+        const uint32_t t1 = mode == kGroupSingle ? n_tiles : t0 + 1;
         const uint32_t* dep = t0 > 0 ? p.progress + (u - 1) : nullptr;
-        uint32_t* pub = t1 < p.n_tiles ? p.progress + u : nullptr;
+        uint32_t* pub = t1 < n_tiles ? p.progress + u : nullptr;
 
-        const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
-        const size_t brow0 = static_cast<size_t>(gd.chunk_base) * kRowsPerChunk * 32 + lane;
-        uint32_t best = 0;
-
-        for (uint32_t tile = t0; tile < t1; ++tile) {
-            const int8_t* ptile = prof + tile * T;
-            const bool first = tile == 0, last = tile + 1 == p.n_tiles;
-            const bool wait = dep != nullptr && tile == t0;
-            const bool publish = pub != nullptr && tile + 1 == t1;
-            const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + brow0;
-            uint2* bout = ((tile & 1) ? p.border1 : p.border0) + brow0;
-
-            uint32_t Hm[T], F[T];
-#pragma unroll
-            for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
-            uint32_t diag_in = NO;
-            uint4 cw = gd.n_chunks ? __ldg(gcodes) : make_uint4(0, 0, 0, 0);
-            // inbound border rows are fetched two rows ahead of their use (q0: the row about to be processed,
-            // q1: the one after); a waiting tile stays two chunks behind its producer so that this look-ahead
-            // never reads an unpublished row
-            uint2 q0 = make_uint2(NO, NO), q1 = make_uint2(NO, NO);
-
-            for (uint32_t chunk = 0; chunk < gd.n_chunks; ++chunk) {
-                const uint4 cur = cw;
-                if (chunk + 1 < gd.n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
-                const size_t row0 = static_cast<size_t>(chunk) * kRowsPerChunk;
-                if (wait) {
-                    const uint32_t need = min(rows, static_cast<uint32_t>(row0) + 2 * kRowsPerChunk);
-                    if (lane == 0)
-                        while (ld_poll(dep) < need) __nanosleep(64);
-                    __syncwarp();
-                }
-                if (!first && chunk == 0) {
-                    q0 = __ldcg(bin);
-                    q1 = __ldcg(bin + 32);     // rows are padded to whole chunks: row 1 always exists
-                }
-#pragma unroll
-                for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
-                    const uint32_t wa = r < 4 ? cur.x : cur.y;
-                    const uint32_t wb = r < 4 ? cur.z : cur.w;
-                    const uint32_t a1 = (wa >> (8 * (r & 3))) & 0xffu;
-                    const uint32_t a2 = (wb >> (8 * (r & 3))) & 0xffu;
-                    const uint4* pa = reinterpret_cast<const uint4*>(ptile + a1 * p.pstride);
-                    const uint4* pb = reinterpret_cast<const uint4*>(ptile + a2 * p.pstride);
-                    uint32_t wA[T / 4], wB[T / 4];
-#pragma unroll
-                    for (int i = 0; i < T / 16; ++i) {
-                        const uint4 va = pa[i], vb = pb[i];
-                        wA[4 * i] = va.x, wA[4 * i + 1] = va.y, wA[4 * i + 2] = va.z, wA[4 * i + 3] = va.w;
-                        wB[4 * i] = vb.x, wB[4 * i + 1] = vb.y, wB[4 * i + 2] = vb.z, wB[4 * i + 3] = vb.w;
-                    }
-                    const size_t row = row0 + r;
-                    const uint2 bi = q0;
-                    q0 = q1;
-                    if (!first && row + 2 < rows) q1 = __ldcg(bin + (row + 2) * 32);
-                    uint32_t hl = bi.x;   // Hm of the column left of the tile, this row
-                    uint32_t E = bi.y;
-                    uint32_t diag = diag_in;
-                    diag_in = hl;
-#pragma unroll
-                    for (int k = 0; k < T; k += 2) {
-                        const uint32_t s0 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xC480u : 0xE6A2u);
-                        const uint32_t s1 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xD591u : 0xF7B3u);
-                        // cell k
-                        E = __viaddmax_s16x2(E, NE, hl);
-                        F[k] = __viaddmax_s16x2(F[k], NE, Hm[k]);
-                        const uint32_t t0 = __vadd2(diag, s0);
-                        const uint32_t h0 = __vimax3_s16x2_relu(t0, E, F[k]);
-                        diag = Hm[k];
-                        hl = __vadd2(h0, NO);
-                        Hm[k] = hl;
-                        // cell k+1
-                        E = __viaddmax_s16x2(E, NE, hl);
-                        F[k + 1] = __viaddmax_s16x2(F[k + 1], NE, Hm[k + 1]);
-                        const uint32_t t1 = __vadd2(diag, s1);
-                        const uint32_t h1 = __vimax3_s16x2_relu(t1, E, F[k + 1]);
-                        diag = Hm[k + 1];
-                        hl = __vadd2(h1, NO);
-                        Hm[k + 1] = hl;
-                        // The running maximum is taken over the diagonal terms t, not over H: a cell whose H
-                        // comes from E or F is dominated by an earlier cell (gaps only subtract), so
-                        // max(H) == max(0, max(t)).  Giving t this second use also makes the compiler keep the
-                        // packed add as VIADD.16x2 (FMA pipe) + one VIMNMX3 instead of VIADDMNMX + VIMNMX
-                        // (two ALU-pipe instructions).
-                        best = __vimax3_s16x2(best, t0, t1);
-                    }
-                    if (!last) bout[row * 32] = make_uint2(hl, E);
-                }
-                if (publish) {
-                    __syncwarp();
-                    if (lane == 0) st_release(pub, static_cast<uint32_t>(row0) + kRowsPerChunk);
-                }
-            }
-        }
+        uint32_t best;
+        if (kNarrow && mode == kGroupNarrow) best = sweep_unit_s16<kNarrowTile, 8, 4>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane);
+        else best = sweep_unit_s16<T, 2, 1>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane);
 
         // halves -> slots (lane, lane+32); the maximum over the group's units
         const int32_t sa = static_cast<int32_t>(best & 0xffffu);
@@ -374,7 +418,7 @@ __global__ void __launch_bounds__(kInterThreads, 1) wavefront_u16_kernel(WavePar
         const uint32_t g = lo;
         const GroupDesc gd = p.groups[g];
         const uint32_t u0 = __ldg(p.unit_start + g);
-        const bool split = __ldg(p.unit_start + g + 1) - u0 > 1;
+        const bool split = p.group_mode[g] != 0;
         const uint32_t t0 = split ? u - u0 : 0;
         const uint32_t t1 = split ? t0 + 1 : p.n_tiles;
         const uint32_t* dep = t0 > 0 ? p.progress + (u - 1) : nullptr;
