@@ -104,6 +104,9 @@ struct swb_db {
     uint32_t* d_counters = nullptr;   // [0] ticket, [1] flag count
     uint32_t* d_unit_start = nullptr;
     uint8_t* d_group_mode = nullptr;
+    uint32_t* d_vstate_off = nullptr;
+    uint4* d_vstate = nullptr;
+    size_t vstate_cap = 0;
     uint32_t* d_progress = nullptr;
     size_t progress_cap = 0;
     uint64_t* d_keys = nullptr;
@@ -192,9 +195,17 @@ double unit_budget_fraction() {
     static const double f = [] {
         const char* e = std::getenv("SWB200_UNIT_BUDGET");
         const double v = e ? std::atof(e) : 0.0;
-        return v > 0.0 ? v : 0.75;
+        return v > 0.0 ? v : 0.0;   // 0: automatic (see score_core)
     }();
     return f;
+}
+
+bool row_blocks_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SWB200_ROWBLOCKS");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
 }
 
 // A group goes to 8-column tiles when its rows exceed this fraction of a warp's fair share (in row-tiles).
@@ -238,17 +249,8 @@ QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t
     const uint64_t reach = static_cast<uint64_t>(top) * std::min<uint64_t>(m, db->meta.max_length);
     pl.may_overflow = reach > static_cast<uint64_t>(pl.limit);
 
-    // register-tile geometry of the s16 kernel (SWB200_TILE = "<columns>x<threads>", for tuning)
-    static const std::pair<uint32_t, uint32_t> geometry = [] {
-        const char* e = std::getenv("SWB200_TILE");
-        const std::string v = e ? e : "";
-        if (v == "32x384") return std::make_pair(32u, 384u);
-        if (v == "48x384") return std::make_pair(48u, 384u);
-        if (v == "32x512") return std::make_pair(32u, 512u);
-        return std::make_pair(static_cast<uint32_t>(kInterTile), static_cast<uint32_t>(kInterThreads));
-    }();
-    pl.tile = pl.main == kMainS16 ? geometry.first : kInterTile;
-    pl.threads = pl.main == kMainS16 ? geometry.second : kInterThreads;
+    pl.tile = kInterTile;
+    pl.threads = kInterThreads;
     // wavefront profile stride: columns padded to whole tiles, then to 16 (mod 128) bytes
     const uint32_t mpad = std::max<uint32_t>(pl.tile, (m + pl.tile - 1) / pl.tile * pl.tile);
     pl.pstride = mpad + ((16 + 128 - (mpad % 128)) % 128);
@@ -347,7 +349,8 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     // ---- stage matrix + query (+ the unit table of the wavefront kernel) and upload -----------------
     const size_t off_query = 576 * sizeof(int32_t);
     const size_t off_units = (off_query + m + 15) & ~size_t(15);
-    const size_t off_modes = off_units + (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t);
+    const size_t off_vsoff = off_units + (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t);
+    const size_t off_modes = off_vsoff + static_cast<size_t>(n_groups) * sizeof(uint32_t);
     const size_t stage_bytes = off_modes + n_groups;
     swb_status st = ensure_stage(db, stage_bytes);
     if (st != SWB_OK) return st;
@@ -363,37 +366,86 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     const uint32_t n_tiles = (m + pl.tile - 1) / pl.tile;
     const uint32_t n_tiles_narrow = (m + kNarrowTile - 1) / kNarrowTile;
     uint32_t n_units = 0;
-    bool any_narrow = false;
+    bool any_narrow = false, any_rowblock = false;
+    uint64_t vstate_slots = 0;
     if (packed) {
-        // Unit policy (see kernels.cuh, GroupMode).  Work is counted in row-tiles (one row of one T-column tile).
-        //   single  the default: one warp scores the group's 64 sequences end to end;
-        //   split   the group's whole sweep exceeds `budget`, a fraction of one warp's fair share of the search:
-        //           one unit per tile, so that no unit dominates the makespan;
-        //   narrow  even a split group's per-tile chain (rows x T columns, strictly sequential in one thread,
-        //           ~900 clk per row when the SM empties out, against ~1600 clk per row-tile of saturated
-        //           throughput) would take more than about half the whole search: 8-column tiles cut that
-        //           chain four-fold.  Only the s16 kernel implements it.
+        // Unit policy (see kernels.cuh, GroupMode).  Work is counted in row-tiles (one row of one T-column tile);
+        // `fair` is one warp's share of the whole search.
+        //   single    the default: one warp scores the group's 64 sequences end to end;
+        //   split     a group whose sweep exceeds `budget` is cut so that no unit dominates the makespan and there
+        //             are enough units for every warp, either
+        //               by tile   (wavefront of warps, each 2 chunks behind its left neighbour:
+        //                          efficiency rows / (rows + 16 (tiles - 1))), or
+        //               by rows   (blocks of rows, each one tile behind the block above:
+        //                          efficiency tiles / (tiles + blocks - 1)),
+        //             whichever wastes less;
+        //   narrow    even a tile-split group's per-tile chain (rows x T columns, strictly sequential in one thread,
+        //             ~900 clk per row when the SM empties out, against ~1600 clk per row-tile of saturated
+        //             throughput) would take more than about half the whole search: 8-column tiles cut that chain
+        //             four-fold.
+        // Row blocks and narrow tiles exist in the s16 kernel only.
         uint32_t* us = reinterpret_cast<uint32_t*>(db->h_stage + off_units);
+        uint32_t* vso = reinterpret_cast<uint32_t*>(db->h_stage + off_vsoff);
         uint8_t* modes = db->h_stage + off_modes;
         const uint64_t total_row_tiles = db->meta.padded_rows * n_tiles;
         const uint64_t warps = static_cast<uint64_t>(db->sm_count) * (pl.threads / 32);
         const uint64_t fair = total_row_tiles / warps;
-        const uint64_t budget = std::max<uint64_t>(4096, static_cast<uint64_t>(unit_budget_fraction() * fair));
+        // With plenty of groups per warp (a whole Swiss-Prot on one GPU: 3.7) only units larger than about
+        // three quarters of a warp's fair share need cutting -- LPT order fills the rest; a small shard with fewer
+        // groups than warps has to be cut finer to give every warp several units.
+        const double auto_fraction = std::min(0.75, std::max(0.08, static_cast<double>(n_groups) / (4.0 * static_cast<double>(warps))));
+        const double fraction = unit_budget_fraction() > 0.0 ? unit_budget_fraction() : auto_fraction;
+        const uint64_t budget = std::max<uint64_t>(2048, static_cast<uint64_t>(fraction * static_cast<double>(fair)));
         const uint64_t narrow_rows = std::max<uint64_t>(2048, static_cast<uint64_t>(narrow_chain_fraction() * fair));
+        const bool s16 = pl.main == kMainS16;
+        // groups are sorted longest first: narrow tiles are needed iff the first group needs them.  The kernel
+        // variant that carries both extra paths spills registers in the common 32-column sweep, so a search that
+        // needs narrow tiles cuts its other large groups by tile rather than by rows.
+        const bool narrow_needed = s16 && n_groups && n_tiles_narrow > 1 &&
+                                   static_cast<uint64_t>(db->meta.groups[0].n_chunks) * kRowsPerChunk > narrow_rows;
+        const bool row_blocks_ok = s16 && row_blocks_enabled() && !narrow_needed;
         for (uint32_t g = 0; g < n_groups; ++g) {
             us[g] = n_units;
-            const uint64_t rows = static_cast<uint64_t>(db->meta.groups[g].n_chunks) * kRowsPerChunk;
+            vso[g] = 0;
+            const uint64_t chunks = db->meta.groups[g].n_chunks;
+            const uint64_t rows = chunks * kRowsPerChunk;
+            const uint64_t work = rows * n_tiles;
             uint8_t mode = kGroupSingle;
-            if (rows * n_tiles > budget && n_tiles > 1) mode = kGroupSplit;
-            if (pl.main == kMainS16 && rows > narrow_rows && n_tiles_narrow > 1) mode = kGroupNarrow;
+            uint32_t units = 1;
+            if (work > budget && n_tiles > 1) {
+                mode = kGroupSplit;
+                units = n_tiles;
+                const double eff_tiles = static_cast<double>(rows) / static_cast<double>(rows + 16 * (n_tiles - 1));
+                // row blocks of at least 2 chunks, about `budget` row-tiles each
+                const uint64_t blocks = std::min<uint64_t>((work + budget - 1) / budget, std::max<uint64_t>(chunks / 2, 1));
+                const double eff_rows = static_cast<double>(n_tiles) / static_cast<double>(n_tiles + blocks - 1);
+                if (row_blocks_ok && blocks >= 2 && eff_rows > eff_tiles) {
+                    mode = kGroupRowBlock;
+                    units = static_cast<uint32_t>(blocks);
+                    vso[g] = static_cast<uint32_t>(vstate_slots);
+                    vstate_slots += n_tiles;
+                    any_rowblock = true;
+                }
+            }
+            if (s16 && rows > narrow_rows && n_tiles_narrow > 1) {
+                if (mode == kGroupRowBlock) vstate_slots -= n_tiles;
+                mode = kGroupNarrow;
+                units = n_tiles_narrow;
+            }
             modes[g] = mode;
             any_narrow |= mode == kGroupNarrow;
-            n_units += mode == kGroupSingle ? 1 : (mode == kGroupSplit ? n_tiles : n_tiles_narrow);
+            n_units += units;
         }
         us[n_groups] = n_units;
         SWB_CUDA(cudaMemcpyAsync(db->d_unit_start, us, (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, s));
         SWB_CUDA(cudaMemcpyAsync(db->d_group_mode, modes, std::max<size_t>(n_groups, 1), cudaMemcpyHostToDevice, s));
+        SWB_CUDA(cudaMemcpyAsync(db->d_vstate_off, vso, std::max<size_t>(n_groups, 1) * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, s));
+        if (any_rowblock) {
+            const size_t need = static_cast<size_t>(vstate_slots) * (kVStateWords / 4) * 32;
+            if ((st = ensure_dev(&db->d_vstate, &db->vstate_cap, need, &db->device_bytes)) != SWB_OK) return st;
+        }
         if ((st = ensure_dev(&db->d_progress, &db->progress_cap, n_units, &db->device_bytes)) != SWB_OK) return st;
         SWB_CUDA(cudaMemsetAsync(db->d_progress, 0, static_cast<size_t>(n_units) * sizeof(uint32_t), s));
         db->last_units = n_units;
@@ -435,6 +487,8 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.n_groups = n_groups;
         wp.unit_start = db->d_unit_start;
         wp.group_mode = db->d_group_mode;
+        wp.vstate_off = db->d_vstate_off;
+        wp.vstate = db->d_vstate;
         wp.n_units = n_units;
         wp.n_tiles_narrow = n_tiles_narrow;
         wp.prof8 = db->d_prof8;
@@ -466,25 +520,23 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
                 wavefront_u16_kernel<false><<<grid, kInterThreads, 0, s>>>(wp);
             }
         } else {
-#define SWB_LAUNCH_S16_N(TT, TH, NARROW)                                                                           \
+#define SWB_LAUNCH_S16(NARROW, RB)                                                                                 \
     {                                                                                                              \
         if (in_smem) {                                                                                             \
-            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, TT, TH, NARROW>,                              \
+            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB>,       \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,                             \
                                           static_cast<int>(db->smem_optin)));                                      \
-            wavefront_s16_kernel<true, TT, TH, NARROW><<<grid, TH, smem, s>>>(wp);                                 \
+            wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB><<<grid, kInterThreads, smem, s>>>(wp); \
         } else {                                                                                                   \
-            wavefront_s16_kernel<false, TT, TH, NARROW><<<grid, TH, 0, s>>>(wp);                                   \
+            wavefront_s16_kernel<false, kInterTile, kInterThreads, NARROW, RB><<<grid, kInterThreads, 0, s>>>(wp); \
         }                                                                                                          \
     }
-#define SWB_LAUNCH_S16(TT, TH)                                                                                     \
-    if (pl.tile == TT && pl.threads == TH) {                                                                       \
-        if (any_narrow) SWB_LAUNCH_S16_N(TT, TH, true) else SWB_LAUNCH_S16_N(TT, TH, false)                        \
-    }
-            SWB_LAUNCH_S16(32, 512)
-            SWB_LAUNCH_S16(32, 384)
-            SWB_LAUNCH_S16(48, 384)
-#undef SWB_LAUNCH_S16_N
+            // the narrow-tile and row-block paths are only compiled into the variants that need them, so that the
+            // plain 32-column sweep keeps its register allocation
+            if (any_narrow && any_rowblock) SWB_LAUNCH_S16(true, true)
+            else if (any_narrow) SWB_LAUNCH_S16(true, false)
+            else if (any_rowblock) SWB_LAUNCH_S16(false, true)
+            else SWB_LAUNCH_S16(false, false)
 #undef SWB_LAUNCH_S16
         }
         ++db->launches;
@@ -602,6 +654,7 @@ swb_status upload_db(swb_db* db) {
     if ((st = dev_alloc(&db->d_counters, 4, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_unit_start, m.groups.size() + 1, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_group_mode, m.groups.size() + 1, tally)) != SWB_OK) return st;
+    if ((st = dev_alloc(&db->d_vstate_off, m.groups.size() + 1, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_keys, db->n_slots, tally)) != SWB_OK) return st;
     if ((st = dev_alloc(&db->d_matrix, 576, tally)) != SWB_OK) return st;
     // the bulk host copy is no longer needed
@@ -731,7 +784,7 @@ void swb_db_destroy(swb_db* db) {
         if (db->own_stream) cudaStreamSynchronize(db->own_stream);
         void* ptrs[] = {db->d_codes,      db->d_groups,   db->d_slot_index, db->d_slot_len,    db->d_border0,
                         db->d_border1,    db->d_iborder0, db->d_iborder1,   db->d_slot_scores, db->d_flag_list,
-                        db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_progress, db->d_keys,        db->d_sel[0],
+                        db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_vstate_off, db->d_vstate, db->d_progress, db->d_keys,        db->d_sel[0],
                         db->d_sel[1],     db->d_sort,     db->d_all_scores, db->d_query,       db->d_matrix,
                         db->d_prof8,      db->d_prof8i,   db->d_prof32i};
         for (void* p : ptrs)

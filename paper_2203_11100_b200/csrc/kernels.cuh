@@ -119,6 +119,8 @@ struct WaveParams {
     uint32_t n_groups;
     const uint32_t* unit_start;   // [n_groups + 1] first unit of each group
     const uint8_t* group_mode;    // [n_groups] GroupMode
+    const uint32_t* vstate_off;   // [n_groups] first vstate slot of a kGroupRowBlock group (slots of one tile each)
+    uint4* vstate;                // register-state hand-over between row blocks
     uint32_t n_units;
     uint32_t n_tiles_narrow;      // ceil(m / 8): tiles of a kGroupNarrow group
     const int8_t* prof8;
@@ -161,13 +163,20 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
 // One unit: tiles [t0, t1) of `n_tiles` tiles of width T over all rows of group `gd`.
 //   dep  progress counter of the unit to the left (nullptr: none), pub: this unit's counter (nullptr: no consumer)
 //   D    border look-ahead in rows (a power of two <= 8), P: publish progress every P chunks
-template <int T, int D, int P>
+//   kRowBlock  the unit is a block of rows [chunk_lo, chunk_hi) swept over ALL tiles; the register state (Hm, F of
+//        the 32 columns, plus the corner value) of every tile is handed from the block above through `vstate`
+//        (one slot of kVStateWords x 32 lanes per tile), and dep / pub count completed TILES instead of rows.
+constexpr uint32_t kVStateWords = 2 * kInterTile + 4;   // Hm + F of the tile's columns, the corner, padded to uint4
+
+template <int T, int D, int P, bool kRowBlock>
 __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const int8_t* prof, const GroupDesc& gd,
                                                    uint32_t t0, uint32_t t1, uint32_t n_tiles, const uint32_t* dep,
-                                                   uint32_t* pub, uint32_t lane) {
+                                                   uint32_t* pub, uint32_t lane, uint32_t chunk_lo, uint32_t chunk_hi,
+                                                   uint4* vstate) {
     static_assert(T % 8 == 0, "tile width must be a multiple of 8 columns");
+    static_assert(!kRowBlock || T == kInterTile, "row blocks hand over exactly kInterTile columns of state");
     const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
-    const uint32_t rows = gd.n_chunks * kRowsPerChunk;
+    const uint32_t rows = chunk_hi * kRowsPerChunk;     // one past the last row this unit touches
     const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
     const size_t brow0 = static_cast<size_t>(gd.chunk_base) * kRowsPerChunk * 32 + lane;
     uint32_t best = 0;
@@ -175,16 +184,31 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
     for (uint32_t tile = t0; tile < t1; ++tile) {
         const int8_t* ptile = prof + tile * T;
         const bool first = tile == 0, last = tile + 1 == n_tiles;
-        const bool wait = dep != nullptr && tile == t0;
-        const bool publish = pub != nullptr && tile + 1 == t1;
+        const bool wait = !kRowBlock && dep != nullptr && tile == t0;
+        const bool publish = !kRowBlock && pub != nullptr && tile + 1 == t1;
         const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + brow0;
         uint2* bout = ((tile & 1) ? p.border1 : p.border0) + brow0;
 
         uint32_t Hm[T], F[T];
-#pragma unroll
-        for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
         uint32_t diag_in = NO;
-        uint4 cw = gd.n_chunks ? __ldg(gcodes) : make_uint4(0, 0, 0, 0);
+        if (kRowBlock && dep != nullptr) {
+            // the block above must have finished this tile; then take over its register state
+            if (lane == 0)
+                while (ld_poll(dep) < tile + 1) __nanosleep(64);
+            __syncwarp();
+            const uint4* slot = vstate + static_cast<size_t>(tile) * (kVStateWords / 4) * 32 + lane;
+#pragma unroll
+            for (int i = 0; i < T / 4; ++i) {
+                const uint4 a = __ldcg(slot + i * 32), b = __ldcg(slot + (T / 4 + i) * 32);
+                Hm[4 * i] = a.x, Hm[4 * i + 1] = a.y, Hm[4 * i + 2] = a.z, Hm[4 * i + 3] = a.w;
+                F[4 * i] = b.x, F[4 * i + 1] = b.y, F[4 * i + 2] = b.z, F[4 * i + 3] = b.w;
+            }
+            diag_in = __ldcg(slot + (2 * T / 4) * 32).x;
+        } else {
+#pragma unroll
+            for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
+        }
+        uint4 cw = chunk_lo < chunk_hi ? __ldg(gcodes + static_cast<size_t>(chunk_lo) * 32) : make_uint4(0, 0, 0, 0);
         // inbound border rows are fetched D rows ahead of their use (q[i]: row = i mod D); a waiting tile stays
         // far enough behind its producer that this look-ahead never reads an unpublished row
         uint2 q[D];
@@ -192,9 +216,9 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
         for (int i = 0; i < D; ++i) q[i] = make_uint2(NO, NO);
         uint32_t known = 0;   // producer progress observed so far
 
-        for (uint32_t chunk = 0; chunk < gd.n_chunks; ++chunk) {
+        for (uint32_t chunk = chunk_lo; chunk < chunk_hi; ++chunk) {
             const uint4 cur = cw;
-            if (chunk + 1 < gd.n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
+            if (chunk + 1 < chunk_hi) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
             const size_t row0 = static_cast<size_t>(chunk) * kRowsPerChunk;
             if (wait) {
                 const uint32_t need = min(rows, static_cast<uint32_t>(row0) + kRowsPerChunk + D);
@@ -208,9 +232,9 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
                     known = __shfl_sync(0xffffffffu, known, 0);
                 }
             }
-            if (!first && chunk == 0) {
+            if (!first && chunk == chunk_lo) {
 #pragma unroll
-                for (int i = 0; i < D; ++i) q[i] = __ldcg(bin + i * 32);   // rows are padded to whole chunks (>= 8)
+                for (int i = 0; i < D; ++i) q[i] = __ldcg(bin + (row0 + i) * 32);   // a chunk has 8 >= D rows
             }
 #pragma unroll
             for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
@@ -271,10 +295,22 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
                 }
                 if (!last) bout[row * 32] = make_uint2(hl, E);
             }
-            if (publish && ((chunk + 1) % P == 0 || chunk + 1 == gd.n_chunks)) {
+            if (publish && ((chunk + 1) % P == 0 || chunk + 1 == chunk_hi)) {
                 __syncwarp();
                 if (lane == 0) st_release(pub, static_cast<uint32_t>(row0) + kRowsPerChunk);
             }
+        }
+        if (kRowBlock && pub != nullptr) {
+            // hand this tile's register state to the block below, then count the tile as done
+            uint4* slot = vstate + static_cast<size_t>(tile) * (kVStateWords / 4) * 32 + lane;
+#pragma unroll
+            for (int i = 0; i < T / 4; ++i) {
+                slot[i * 32] = make_uint4(Hm[4 * i], Hm[4 * i + 1], Hm[4 * i + 2], Hm[4 * i + 3]);
+                slot[(T / 4 + i) * 32] = make_uint4(F[4 * i], F[4 * i + 1], F[4 * i + 2], F[4 * i + 3]);
+            }
+            slot[(2 * T / 4) * 32] = make_uint4(diag_in, 0, 0, 0);
+            __syncwarp();
+            if (lane == 0) st_release(pub, tile + 1);
         }
     }
     return best;
@@ -284,15 +320,18 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
 enum GroupMode : uint8_t {
     kGroupSingle = 0,   // one unit: all tiles of width T, one warp
     kGroupSplit = 1,    // one unit per tile of width T: a wavefront of warps
-    kGroupNarrow = 2    // one unit per tile of width 8: a wavefront with a 4x shorter per-row chain, for groups whose
+    kGroupNarrow = 2,   // one unit per tile of width 8: a wavefront with a 4x shorter per-row chain, for groups whose
                         // rows x T sequential chain would otherwise outlast the whole search (short query, very
                         // long sequences)
+    kGroupRowBlock = 3  // units are blocks of rows, each swept over all tiles one tile behind the block above; the
+                        // efficient split when the query has many tiles and the group few rows (long queries,
+                        // small per-GPU shards)
 };
 constexpr int kNarrowTile = 8;
 
 // kNarrow: compile the 8-column path in.  Searches without narrow groups (all long queries) launch the variant
 // without it, whose register allocation is not disturbed by the second sweep.
-template <bool kSmemProfile, int T, int kThreads, bool kNarrow>
+template <bool kSmemProfile, int T, int kThreads, bool kNarrow, bool kRowBlocks>
 __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p) {
     extern __shared__ __align__(16) uint8_t smem_prof[];
 
@@ -328,14 +367,26 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
         const uint32_t u0 = __ldg(p.unit_start + g);
         const uint32_t mode = p.group_mode[g];
         const uint32_t n_tiles = mode == kGroupNarrow ? p.n_tiles_narrow : p.n_tiles;
-        const uint32_t t0 = mode == kGroupSingle ? 0 : u - u0;
-        const uint32_t t1 = mode == kGroupSingle ? n_tiles : t0 + 1;
-        const uint32_t* dep = t0 > 0 ? p.progress + (u - 1) : nullptr;
-        uint32_t* pub = t1 < n_tiles ? p.progress + u : nullptr;
-
         uint32_t best;
-        if (kNarrow && mode == kGroupNarrow) best = sweep_unit_s16<kNarrowTile, 8, 4>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane);
-        else best = sweep_unit_s16<T, 2, 1>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane);
+        if (kRowBlocks && mode == kGroupRowBlock) {
+            // unit b of nb: chunks [b * per, min((b + 1) * per, n_chunks)), all tiles
+            const uint32_t nb = __ldg(p.unit_start + g + 1) - u0, b = u - u0;
+            const uint32_t per = (gd.n_chunks + nb - 1) / nb;
+            const uint32_t lo_c = min(gd.n_chunks, b * per), hi_c = min(gd.n_chunks, lo_c + per);
+            const uint32_t* dep = b > 0 ? p.progress + (u - 1) : nullptr;
+            uint32_t* pub = b + 1 < nb ? p.progress + u : nullptr;
+            uint4* vs = p.vstate + static_cast<size_t>(p.vstate_off[g]) * (kVStateWords / 4) * 32;
+            best = sweep_unit_s16<T, 2, 1, true>(p, prof, gd, 0, n_tiles, n_tiles, dep, pub, lane, lo_c, hi_c, vs);
+        } else {
+            const uint32_t t0 = mode == kGroupSingle ? 0 : u - u0;
+            const uint32_t t1 = mode == kGroupSingle ? n_tiles : t0 + 1;
+            const uint32_t* dep = t0 > 0 ? p.progress + (u - 1) : nullptr;
+            uint32_t* pub = t1 < n_tiles ? p.progress + u : nullptr;
+            if (kNarrow && mode == kGroupNarrow)
+                best = sweep_unit_s16<kNarrowTile, 8, 4, false>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane, 0, gd.n_chunks, nullptr);
+            else
+                best = sweep_unit_s16<T, 2, 1, false>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane, 0, gd.n_chunks, nullptr);
+        }
 
         // halves -> slots (lane, lane+32); the maximum over the group's units
         const int32_t sa = static_cast<int32_t>(best & 0xffffu);
