@@ -8,7 +8,8 @@ import ctypes as C
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libswb200.so"
+import os
+LIB_PATH = Path(os.environ["SWB200_LIB"]) if os.environ.get("SWB200_LIB") else PKG / "libswb200.so"   # override: tuning only
 
 SWB_OK, SWB_ERR_INVALID, SWB_ERR_RANGE, SWB_ERR_CUDA, SWB_ERR_NCCL, SWB_ERR_UNSUPPORTED, SWB_ERR_INTERNAL = range(7)
 

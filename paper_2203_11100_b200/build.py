@@ -43,7 +43,9 @@ def is_stale() -> bool:
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     if not force and not is_stale():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-ccbin", "/usr/bin/g++", "-o", str(LIB)] + [str(CSRC / s) for s in SOURCES] + ["-ldl", "-lpthread"]
+    extra = [f"-D{k}={os.environ[k]}" for k in ("SWB_INTER_TILE", "SWB_INTER_THREADS") if k in os.environ]   # tuning only
+    out = Path(os.environ.get("SWB_LIB_OUT", str(LIB)))
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-ccbin", "/usr/bin/g++", "-o", str(out)] + [str(CSRC / s) for s in SOURCES] + ["-ldl", "-lpthread"]
     if verbose:
         cmd.insert(1, "-Xptxas")
         cmd.insert(2, "-v")

@@ -58,13 +58,11 @@ inline uint32_t pack16(int32_t v) {
 
 enum { EV_START = 0, EV_UP, EV_SCAN, EV_RESCORE, EV_TOPK, EV_END, EV_COUNT };
 
-enum MainKernel { kMainNone = 0, kMainS16 = 1, kMainU16 = 2 };
+enum MainKernel { kMainNone = 0, kMainS16 = 1 };
 
 struct QueryPlan {
     int main = kMainNone;     // which packed kernel scans the database (none: int32 intra kernel for everything)
     bool wide = false;        // the int32 intra kernel needs the int32 profile (matrix + open outside int8)
-    int32_t c = 0;            // -min(matrix, 0): profile shift of the u16 kernel
-    int32_t bias = 0;         // b' = open + ext + 2c of the u16 kernel
     bool may_overflow = true; // a score above `limit` is possible at all
     int32_t limit = 0;
     int32_t open = 0, ext = 0;
@@ -229,23 +227,12 @@ QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t
     // int8 profile shifted by `open` (s16 kernel and the int8 flavour of the intra kernel)
     const bool fits8 = (lo + open >= -128) && (hi + open <= 127) && (open <= 127);
     pl.wide = !fits8;
-    // uint8 profile shifted by c (u16 kernel): bytes must stay below 128 (PRMT zero-extends through the sign)
-    pl.c = std::max(0, -lo);
-    pl.bias = open + ext + 2 * pl.c;
-    const bool fitsu = (hi + pl.c <= 127) && (pl.bias <= 8192);
-    static const int forced = [] {
+    static const bool force_intra_env = [] {
         const char* e = std::getenv("SWB200_KERNEL");
-        if (e && std::string(e) == "s16") return static_cast<int>(kMainS16);
-        if (e && std::string(e) == "u16") return static_cast<int>(kMainU16);
-        if (e && std::string(e) == "intra") return -1;
-        return static_cast<int>(kMainNone);
+        return e && std::string(e) == "intra";
     }();
-    if (forced == -1 || db->force_intra) pl.main = kMainNone;
-    else if (forced == kMainU16 && fitsu) pl.main = kMainU16;
-    else if (fits8) pl.main = kMainS16;      // default: measured faster (VIADD.16x2 already runs on the FMA pipe)
-    else if (fitsu) pl.main = kMainU16;
-    else pl.main = kMainNone;
-    pl.limit = pl.main == kMainU16 ? 65535 - pl.bias - top : 32767 - top;
+    pl.main = (fits8 && !db->force_intra && !force_intra_env) ? kMainS16 : kMainNone;
+    pl.limit = 32767 - top;
     const uint64_t reach = static_cast<uint64_t>(top) * std::min<uint64_t>(m, db->meta.max_length);
     pl.may_overflow = reach > static_cast<uint64_t>(pl.limit);
 
@@ -459,7 +446,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     pp.query = db->d_query;
     pp.matrix = db->d_matrix;
     pp.m = m;
-    pp.shift_main = pl.main == kMainU16 ? pl.c : open;
+    pp.shift_main = open;
     pp.shift_intra = open;
     pp.pstride = pl.pstride;
     pp.intra_t = pl.intra_t;
@@ -501,25 +488,11 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.ticket = db->d_counters;
         wp.neg_open2 = pack16(-open);
         wp.neg_ext2 = pack16(-ext);
-        wp.init2 = pack16(pl.bias - open);
-        wp.open_mc2 = pack16(open - pl.c);
-        wp.bias_mc2 = pack16(pl.bias - pl.c);
-        wp.neg_open_word = 0u - static_cast<uint32_t>(open) * 0x10001u;
-        wp.one = 1;
-        wp.bias = pl.bias;
         const size_t smem = prof_elems;
         const uint32_t warps_per_cta = pl.threads / 32;
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(db->sm_count, (n_units + warps_per_cta - 1) / warps_per_cta));
         const bool in_smem = smem <= db->smem_optin;
-        if (pl.main == kMainU16) {
-            if (in_smem) {
-                SWB_CUDA(cudaFuncSetAttribute(wavefront_u16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(db->smem_optin)));
-                wavefront_u16_kernel<true><<<grid, kInterThreads, smem, s>>>(wp);
-            } else {
-                wavefront_u16_kernel<false><<<grid, kInterThreads, 0, s>>>(wp);
-            }
-        } else {
+        {
 #define SWB_LAUNCH_S16(NARROW, RB)                                                                                 \
     {                                                                                                              \
         if (in_smem) {                                                                                             \

@@ -28,8 +28,14 @@
 namespace swb {
 
 constexpr int kProfRows = 25;        // 24 symbols + the pad row
-constexpr int kInterTile = 32;       // query columns held in registers per pass (inter-task)
-constexpr int kInterThreads = 512;   // persistent CTA: 16 warps, one per SMSP x4
+#ifndef SWB_INTER_TILE
+#define SWB_INTER_TILE 32
+#endif
+#ifndef SWB_INTER_THREADS
+#define SWB_INTER_THREADS 512
+#endif
+constexpr int kInterTile = SWB_INTER_TILE;        // query columns held in registers per pass (multiple of 8)
+constexpr int kInterThreads = SWB_INTER_THREADS;  // persistent CTA: 16 warps, four per SMSP
 constexpr int kIntraDelta = 64;      // step offset between neighbouring warps of an intra-task CTA
 constexpr int kIntraRing = 128;      // rows of border ring buffer between neighbouring warps
 constexpr int kIntraMaxWarps = 8;
@@ -133,13 +139,6 @@ struct WaveParams {
     uint32_t* ticket;
     uint32_t neg_open2;           // (-open, -open) packed
     uint32_t neg_ext2;            // (-extend, -extend) packed
-    // wavefront_u16_kernel only (biased unsigned domain, see there)
-    uint32_t init2;               // (b' - open) packed: Xm / E / F of the matrix edge
-    uint32_t open_mc2;            // (open - c) packed
-    uint32_t bias_mc2;            // (b' - c) packed
-    uint32_t neg_open_word;       // -(open * 65537): subtracts open from both halves with one 32-bit add
-    uint32_t one;                 // 1, opaque to the compiler: keeps the two adds on the FMA pipe as IMAD
-    int32_t bias;                 // b'
 };
 
 // A group is either one unit (all tiles, one warp) or n_tiles units (one tile each, a wavefront of
@@ -394,185 +393,6 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
         const uint32_t slot_a = gd.first_slot + lane;
         if (sa) atomicMax(p.slot_scores + slot_a, sa);
         if (sb) atomicMax(p.slot_scores + slot_a + 32, sb);
-    }
-}
-
-// ------------------------------------------------------------------------------------------------
-// wavefront_u16_kernel: the same tile-wavefront, re-balanced across the two integer pipes.
-//
-// ncu on wavefront_s16_kernel shows the ALU (DPX) pipe 84 % busy and the FMA pipe 10 %: the kernel
-// is bound by 6.5 ALU instructions per two cells.  The FMA pipe issues IMAD at the same rate and
-// in parallel (pipe_rate_kernel: 18.5 + 18.5 T/s), but a 32-bit add is only a correct *packed*
-// add when no carry crosses bit 16.  This variant makes that true by construction:
-//
-//   * every stored quantity is biased by b' = open + ext + 2c (c = -min(matrix, 0)) and treated as
-//     unsigned, so both halves are always >= 0 and < 65536: a 32-bit add of two such words, or of a
-//     word and a constant whose halves keep the result in range, never carries across;
-//   * the zero floor of the recurrence is applied to the diagonal input only.  With X the
-//     un-floored cell value, max(X, 0) = H holds for every cell (a gap opened from a floored zero
-//     can never exceed -open <= 0, so feeding un-floored X into E and F changes nothing that
-//     survives the floor), which removes the need for a "relu at b'" instruction:
-//
-//       D  = max(Xm_diag + (open - c), b' - c)        VIADDMNMX.U16x2      ALU   [= max(X_diag,0) + b' - c]
-//       t  = D + p                                    IMAD                 FMA   [p = sub + c >= 0, profile byte]
-//       E  = max(E - ext, Xm_left)                    VIADDMNMX.U16x2      ALU
-//       F  = max(F - ext, Xm_up)                      VIADDMNMX.U16x2      ALU
-//       X  = max(t, E, F)                             VIMNMX3.U16x2        ALU
-//       Xm = X - open                                 IMAD (x*1 + const)   FMA
-//       best = max(best, X0, X1)                      VIMNMX3.U16x2        ALU, per two cells
-//       p  = pack(byte_A, byte_B)                     PRMT                 ALU
-//
-//   5.5 ALU + 2 FMA instructions per two cells instead of 6.5 ALU.  The unsigned domain also
-//   doubles the trusted range: limit = 65535 - b' - max(matrix).
-// Everything else (units, tickets, borders, flags) is identical to wavefront_s16_kernel.
-// ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t imad_add(uint32_t a, uint32_t one, uint32_t c) {
-    uint32_t d;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(one), "r"(c));
-    return d;
-}
-
-template <bool kSmemProfile>
-__global__ void __launch_bounds__(kInterThreads, 1) wavefront_u16_kernel(WaveParams p) {
-    constexpr int T = kInterTile;
-    extern __shared__ __align__(16) uint8_t smem_prof[];
-
-    const int8_t* prof;
-    if (kSmemProfile) {
-        const uint32_t n16 = kProfRows * p.pstride / 16;
-        const uint4* src = reinterpret_cast<const uint4*>(p.prof8);
-        uint4* dst = reinterpret_cast<uint4*>(smem_prof);
-        for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
-        __syncthreads();
-        prof = reinterpret_cast<const int8_t*>(smem_prof);
-    } else {
-        prof = p.prof8;
-    }
-
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t INIT = p.init2, NE = p.neg_ext2, OMC = p.open_mc2, BMC = p.bias_mc2;
-    const uint32_t NOW = p.neg_open_word, ONE = p.one;
-    const uint32_t BIAS2 = static_cast<uint32_t>(p.bias) * 0x10001u;
-
-    for (;;) {
-        uint32_t u = 0;
-        if (lane == 0) u = atomicAdd(p.ticket, 1u);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= p.n_units) break;
-
-        uint32_t lo = 0, hi = p.n_groups;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(p.unit_start + mid) <= u) lo = mid;
-            else hi = mid;
-        }
-        const uint32_t g = lo;
-        const GroupDesc gd = p.groups[g];
-        const uint32_t u0 = __ldg(p.unit_start + g);
-        const bool split = p.group_mode[g] != 0;
-        const uint32_t t0 = split ? u - u0 : 0;
-        const uint32_t t1 = split ? t0 + 1 : p.n_tiles;
-        const uint32_t* dep = t0 > 0 ? p.progress + (u - 1) : nullptr;
-        uint32_t* pub = t1 < p.n_tiles ? p.progress + u : nullptr;
-
-        const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
-        const size_t brow0 = static_cast<size_t>(gd.chunk_base) * kRowsPerChunk * 32 + lane;
-        uint32_t best = BIAS2;
-
-        for (uint32_t tile = t0; tile < t1; ++tile) {
-            const int8_t* ptile = prof + tile * T;
-            const bool first = tile == 0, last = tile + 1 == p.n_tiles;
-            const bool wait = dep != nullptr && tile == t0;
-            const bool publish = pub != nullptr && tile + 1 == t1;
-            const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + brow0;
-            uint2* bout = ((tile & 1) ? p.border1 : p.border0) + brow0;
-
-            uint32_t Xm[T], F[T];
-#pragma unroll
-            for (int k = 0; k < T; ++k) Xm[k] = INIT, F[k] = INIT;
-            uint32_t diag_in = INIT;
-            uint4 cw = gd.n_chunks ? __ldg(gcodes) : make_uint4(0, 0, 0, 0);
-            // inbound border of the row about to be processed; for a tile that does not wait on another
-            // unit the prefetch runs across chunk boundaries
-            uint2 bnext = make_uint2(INIT, INIT);
-            if (!first && !wait && gd.n_chunks) bnext = __ldcg(bin);
-
-            for (uint32_t chunk = 0; chunk < gd.n_chunks; ++chunk) {
-                const uint4 cur = cw;
-                if (chunk + 1 < gd.n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
-                const size_t row0 = static_cast<size_t>(chunk) * kRowsPerChunk;
-                if (wait) {
-                    const uint32_t need = static_cast<uint32_t>(row0) + kRowsPerChunk;
-                    if (lane == 0)
-                        while (ld_poll(dep) < need) __nanosleep(40);
-                    __syncwarp();
-                    bnext = __ldcg(bin + row0 * 32);
-                }
-#pragma unroll
-                for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
-                    const uint32_t wa = r < 4 ? cur.x : cur.y;
-                    const uint32_t wb = r < 4 ? cur.z : cur.w;
-                    const uint32_t a1 = (wa >> (8 * (r & 3))) & 0xffu;
-                    const uint32_t a2 = (wb >> (8 * (r & 3))) & 0xffu;
-                    const uint4* pa = reinterpret_cast<const uint4*>(ptile + a1 * p.pstride);
-                    const uint4* pb = reinterpret_cast<const uint4*>(ptile + a2 * p.pstride);
-                    uint32_t wA[T / 4], wB[T / 4];
-#pragma unroll
-                    for (int i = 0; i < T / 16; ++i) {
-                        const uint4 va = pa[i], vb = pb[i];
-                        wA[4 * i] = va.x, wA[4 * i + 1] = va.y, wA[4 * i + 2] = va.z, wA[4 * i + 3] = va.w;
-                        wB[4 * i] = vb.x, wB[4 * i + 1] = vb.y, wB[4 * i + 2] = vb.z, wB[4 * i + 3] = vb.w;
-                    }
-                    const size_t row = row0 + r;
-                    const uint2 bi = bnext;
-                    if (!first) {
-                        const bool in_chunk = r + 1 < static_cast<int>(kRowsPerChunk);
-                        if (in_chunk || (!wait && chunk + 1 < gd.n_chunks)) bnext = __ldcg(bin + (row + 1) * 32);
-                    }
-                    uint32_t xl = bi.x;   // Xm of the column left of the tile, this row
-                    uint32_t E = bi.y;
-                    uint32_t diag = diag_in;
-                    diag_in = xl;
-#pragma unroll
-                    for (int k = 0; k < T; k += 2) {
-                        // profile bytes are < 128, so the "sign" bytes PRMT replicates are zero
-                        const uint32_t p0 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xC480u : 0xE6A2u);
-                        const uint32_t p1 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xD591u : 0xF7B3u);
-                        // cell k
-                        E = __viaddmax_u16x2(E, NE, xl);
-                        F[k] = __viaddmax_u16x2(F[k], NE, Xm[k]);
-                        const uint32_t d0 = __viaddmax_u16x2(diag, OMC, BMC);
-                        const uint32_t x0 = __vimax3_u16x2(imad_add(d0, ONE, p0), E, F[k]);
-                        diag = Xm[k];
-                        xl = imad_add(x0, ONE, NOW);
-                        Xm[k] = xl;
-                        // cell k+1
-                        E = __viaddmax_u16x2(E, NE, xl);
-                        F[k + 1] = __viaddmax_u16x2(F[k + 1], NE, Xm[k + 1]);
-                        const uint32_t d1 = __viaddmax_u16x2(diag, OMC, BMC);
-                        const uint32_t x1 = __vimax3_u16x2(imad_add(d1, ONE, p1), E, F[k + 1]);
-                        diag = Xm[k + 1];
-                        xl = imad_add(x1, ONE, NOW);
-                        Xm[k + 1] = xl;
-                        best = __vimax3_u16x2(best, x0, x1);
-                    }
-                    if (!last) bout[row * 32] = make_uint2(xl, E);
-                }
-                if (publish) {
-                    __syncwarp();
-                    if (lane == 0) {
-                        __threadfence();
-                        st_release(pub, static_cast<uint32_t>(row0) + kRowsPerChunk);
-                    }
-                }
-            }
-        }
-
-        const int32_t sa = static_cast<int32_t>(best & 0xffffu) - p.bias;
-        const int32_t sb = static_cast<int32_t>(best >> 16) - p.bias;
-        const uint32_t slot_a = gd.first_slot + lane;
-        if (sa > 0) atomicMax(p.slot_scores + slot_a, sa);
-        if (sb > 0) atomicMax(p.slot_scores + slot_a + 32, sb);
     }
 }
 
