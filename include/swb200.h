@@ -168,6 +168,26 @@ swb_status swb_score_pair(const uint8_t* query, uint32_t query_len, const uint8_
                           uint32_t subject_len, const int32_t* matrix, int32_t gap_open,
                           int32_t gap_extend, uint64_t chunk_width, int32_t device, int32_t* score);
 
+/* sw_align_traceback (align.hpp:254-353) on the GPU: optimal local alignment of one pair with its edit script.
+ * Outside the measured scoring path but on by default in run_search (scheduler.hpp:27,246-249).
+ *   memory_cap   as in the reference: if (m+1)*(n+1) bytes exceed it (or overflow), the result is score-only with
+ *                capped = 1 and no operations
+ *   ops          receives the edit script, first operation first, one byte each with the numbering of EditOp
+ *                (align.hpp:236): 0 match, 1 substitute, 2 insert, 3 del; at most ops_capacity bytes are written,
+ *                out->n_ops is the true length (<= m + n)
+ * Same tie-breaking as the reference, so scripts are identical, not merely equally good. */
+typedef struct swb_alignment {
+    uint64_t query_begin, query_end;     /* half-open */
+    uint64_t subject_begin, subject_end; /* half-open */
+    uint64_t n_ops;
+    int32_t score;
+    int32_t capped;
+} swb_alignment;
+swb_status swb_align_traceback(const uint8_t* query, uint32_t query_len, const uint8_t* subject,
+                               uint32_t subject_len, const int32_t* matrix, int32_t gap_open,
+                               int32_t gap_extend, uint64_t memory_cap, int32_t device,
+                               swb_alignment* out, uint8_t* ops, uint64_t ops_capacity);
+
 /* ---- several GPUs, one process (the C++ drop-in's multi-GPU mode) ------------------------------
  * The database is dealt by residue count over `n_devices` GPUs; each search runs all shards
  * concurrently, then the per-shard top-k keys are exchanged with one ncclAllGather and merged.

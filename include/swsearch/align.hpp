@@ -5,8 +5,9 @@
 //     sw_score_scalar     align.hpp:69-78    -> swb_score_pair   (intra-task warp-shuffle kernel, int32)
 //     sw_score_batch      align.hpp:91-159   -> swb_score_batch  (packed int16 DPX kernel + int32 re-run)
 //     sw_score_wavefront  align.hpp:166-229  -> swb_score_pair
-// The traceback (align.hpp:254-353) runs after scoring on at most top_k hits and is outside the measured path
-// (SPEC.md:403); it stays host C++ here, written to reproduce the reference's edit scripts decision by decision.
+//     sw_align_traceback  align.hpp:254-353  -> swb_align_traceback (direction-matrix fill + backward walk on the GPU;
+//                                               runs after scoring on at most top_k hits, outside the measured path,
+//                                               SPEC.md:403, but on by default)
 #pragma once
 
 #include <algorithm>
@@ -108,101 +109,34 @@ struct Alignment {
     bool capped = false;
 };
 
-/// Traceback over a full (|query|+1) x (|subject|+1) byte matrix (host code, outside the measured path).
-/// Tie-breaking follows the reference exactly: inside a cell zero < diagonal < horizontal gap < vertical gap wins
-/// only on strict improvement in that order; a gap that is as good opened as extended counts as opened; the first
-/// best cell in (subject row, query column) order is the end point.
+/// Optimal local alignment with its edit script, computed on the GPU (swb_align_traceback): an anti-diagonal
+/// fill that writes one direction byte per cell, then a backward walk.  The matrix needs (|query|+1)*(|subject|+1)
+/// bytes by the reference's accounting; pairs beyond `memory_cap` come back score-only with `capped` set.
+/// Tie-breaking follows the reference exactly, so the scripts are identical: inside a cell zero, diagonal, gap along
+/// the query, gap along the subject win in that order only on strict improvement; a gap that is as good opened as
+/// extended counts as opened; the first best cell in (subject row, query column) order is the end point.
 inline Alignment sw_align_traceback(const EncodedSequence& query, const EncodedSequence& subject,
                                     const ScoringMatrix& matrix, const GapModel& gaps,
                                     std::size_t memory_cap = std::size_t{256} << 20) {
     Alignment result;
     const std::size_t m = query.length(), n = subject.length();
     if (m == 0 || n == 0) return result;
+    for (std::uint8_t code : subject.codes)
+        if (code >= ScoringMatrix::size) throw std::out_of_range("subject code outside matrix alphabet");
 
-    const std::size_t width = m + 1;
-    const std::size_t bytes = width * (n + 1);
-    const bool overflowed = bytes / width != n + 1;
-    if (overflowed || bytes > memory_cap) {
-        result.score = sw_score_scalar(query, subject, matrix, gaps);
-        result.capped = true;
-        return result;
-    }
-
-    // one byte per cell: low two bits = where H came from; two flags = "this gap cell extends a longer gap"
-    constexpr std::uint8_t kFromNone = 0, kFromDiag = 1, kFromGapQ = 2, kFromGapS = 3;   // GapQ: along the query
-    constexpr std::uint8_t kMaskFrom = 3, kGapQExtends = 4, kGapSExtends = 8;
-    std::vector<std::uint8_t> trace(bytes, kFromNone);
-
-    const std::int32_t open = gaps.open(), extend = gaps.extend();
-    std::vector<std::int32_t> h_row(width, 0), gap_s(width, detail::kNegInf);
-    std::int32_t top = 0;
-    std::size_t top_row = 0, top_col = 0;
-
-    for (std::size_t row = 1; row <= n; ++row) {
-        const std::int32_t* scores = matrix.row(subject.codes[row - 1]);
-        std::uint8_t* trace_row = trace.data() + row * width;
-        std::int32_t corner = 0;                 // H of (row-1, col-1)
-        std::int32_t gap_q = detail::kNegInf;    // gap running along the query in this row
-        for (std::size_t col = 1; col <= m; ++col) {
-            std::uint8_t flags = 0;
-            const std::int32_t q_opened = h_row[col - 1] - open, q_extended = gap_q - extend;
-            if (q_extended > q_opened) flags |= kGapQExtends;
-            gap_q = std::max(q_opened, q_extended);
-            const std::int32_t s_opened = h_row[col] - open, s_extended = gap_s[col] - extend;
-            if (s_extended > s_opened) flags |= kGapSExtends;
-            gap_s[col] = std::max(s_opened, s_extended);
-
-            std::int32_t value = 0;
-            std::uint8_t from = kFromNone;
-            const std::int32_t paired = corner + scores[query.codes[col - 1]];
-            if (paired > value) value = paired, from = kFromDiag;
-            if (gap_q > value) value = gap_q, from = kFromGapQ;
-            if (gap_s[col] > value) value = gap_s[col], from = kFromGapS;
-
-            trace_row[col] = static_cast<std::uint8_t>(flags | from);
-            corner = h_row[col];
-            h_row[col] = value;
-            if (value > top) top = value, top_row = row, top_col = col;
-        }
-    }
-
-    result.score = {top};
-    if (top == 0) return result;
-
-    enum class In { cell, gap_q, gap_s } where = In::cell;
-    std::size_t row = top_row, col = top_col;
-    std::vector<EditOp> backwards;
-    for (bool walking = true; walking;) {
-        const std::uint8_t here = trace[row * width + col];
-        switch (where) {
-        case In::cell:
-            switch (here & kMaskFrom) {
-            case kFromNone: walking = false; break;
-            case kFromDiag:
-                backwards.push_back(query.codes[col - 1] == subject.codes[row - 1] ? EditOp::match : EditOp::substitute);
-                --row, --col;
-                break;
-            case kFromGapQ: where = In::gap_q; break;
-            default: where = In::gap_s; break;
-            }
-            break;
-        case In::gap_q:
-            backwards.push_back(EditOp::del);
-            --col;
-            if (!(here & kGapQExtends)) where = In::cell;
-            break;
-        case In::gap_s:
-            backwards.push_back(EditOp::insert);
-            --row;
-            if (!(here & kGapSExtends)) where = In::cell;
-            break;
-        }
-    }
-    result.ops.assign(backwards.rbegin(), backwards.rend());
-    result.query_begin = col;
-    result.query_end = top_col;
-    result.subject_begin = row;
-    result.subject_end = top_row;
+    swb_alignment raw{};
+    std::vector<std::uint8_t> script(m + n);
+    gpu::check(swb_align_traceback(query.codes.data(), static_cast<std::uint32_t>(m), subject.codes.data(),
+                                   static_cast<std::uint32_t>(n), gpu::matrix_table(matrix), gaps.open(), gaps.extend(),
+                                   memory_cap, gpu::devices().front(), &raw, script.data(), script.size()));
+    result.score = {raw.score};
+    result.capped = raw.capped != 0;
+    result.query_begin = raw.query_begin;
+    result.query_end = raw.query_end;
+    result.subject_begin = raw.subject_begin;
+    result.subject_end = raw.subject_end;
+    result.ops.resize(raw.n_ops);
+    for (std::size_t i = 0; i < result.ops.size(); ++i) result.ops[i] = static_cast<EditOp>(script[i]);
     return result;
 }
 

@@ -49,6 +49,11 @@ class SwbDbInfo(C.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_ if "reserved" not in name}
 
 
+class SwbAlignment(C.Structure):
+    _fields_ = [("query_begin", C.c_uint64), ("query_end", C.c_uint64), ("subject_begin", C.c_uint64),
+                ("subject_end", C.c_uint64), ("n_ops", C.c_uint64), ("score", C.c_int32), ("capped", C.c_int32)]
+
+
 class SwbPipeRates(C.Structure):
     _fields_ = [
         ("viaddmnmx_s16x2", C.c_double), ("vimnmx3_s16x2", C.c_double), ("viadd_16x2", C.c_double),
@@ -83,6 +88,8 @@ SIGNATURES = {
                                   C.c_int32, C.c_int32, i32p]),
     "swb_score_pair": (C.c_int, [u8p, C.c_uint32, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint64,
                                  C.c_int32, i32p]),
+    "swb_align_traceback": (C.c_int, [u8p, C.c_uint32, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint64,
+                                      C.c_int32, C.POINTER(SwbAlignment), u8p, C.c_uint64]),
     "swb_mdb_create_flat": (C.c_int, [u8p, u64p, C.c_uint32, C.c_uint64, i32p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "swb_mdb_create": (C.c_int, [C.POINTER(u8p), u32p, C.c_uint32, C.c_uint64, i32p, C.c_uint32,
                                  C.POINTER(C.c_void_p)]),

@@ -1005,6 +1005,132 @@ swb_status swb_score_pair(const uint8_t* query, uint32_t query_len, const uint8_
     return SWB_OK;
 }
 
+swb_status swb_align_traceback(const uint8_t* query, uint32_t query_len, const uint8_t* subject, uint32_t subject_len,
+                               const int32_t* matrix, int32_t gap_open, int32_t gap_extend, uint64_t memory_cap,
+                               int32_t device, swb_alignment* out, uint8_t* ops, uint64_t ops_capacity) {
+    if (!out) return fail(SWB_ERR_INVALID, "out is null");
+    if (subject_len && !subject) return fail(SWB_ERR_INVALID, "subject is null");
+    swb_status st = check_scoring_args(query, query_len, matrix, gap_open, gap_extend);
+    if (st != SWB_OK) return st;
+    std::memset(out, 0, sizeof(*out));
+    const uint64_t m = query_len, n = subject_len;
+    if (m == 0 || n == 0) return SWB_OK;                                  // align.hpp:260
+    // the reference's budget test (align.hpp:262-267), on its (m+1) x (n+1) byte matrix
+    const uint64_t cells = (m + 1) * (n + 1);
+    if (cells / (m + 1) != n + 1 || cells > memory_cap) {
+        int32_t score = 0;
+        st = swb_score_pair(query, query_len, subject, subject_len, matrix, gap_open, gap_extend, 1, device, &score);
+        if (st != SWB_OK) return st;
+        out->score = score;
+        out->capped = 1;
+        return SWB_OK;
+    }
+
+    swb_db* db = nullptr;
+    const uint8_t* ptrs[1] = {subject};
+    const uint32_t ls[1] = {subject_len};
+    st = swb_db_create(ptrs, ls, 1, 0, device, 0, 1, &db);
+    if (st != SWB_OK) return st;
+    db->force_intra = true;           // (the transient handle is private to this call: no locking needed)
+    DeviceGuard guard(db->device);
+    cudaStream_t s = db->stream;
+
+    uint8_t* d_dir = nullptr;
+    uint8_t* d_ops = nullptr;
+    int32_t* d_result = nullptr;
+    uint2* d_b0 = nullptr;
+    uint2* d_b1 = nullptr;
+    int8_t* d_prof8 = nullptr;
+    int32_t* d_prof32 = nullptr;
+    uint8_t* d_query = nullptr;
+    int32_t* d_matrix = nullptr;
+    auto cleanup = [&] {
+        for (void* ptr : {static_cast<void*>(d_dir), static_cast<void*>(d_ops), static_cast<void*>(d_result),
+                          static_cast<void*>(d_b0), static_cast<void*>(d_b1), static_cast<void*>(d_prof8),
+                          static_cast<void*>(d_prof32), static_cast<void*>(d_query), static_cast<void*>(d_matrix)})
+            if (ptr) cudaFree(ptr);
+    };
+    int32_t result[6] = {0, 0, 0, 0, 0, 0};
+    std::vector<uint8_t> reversed;
+    st = [&]() -> swb_status {
+        const QueryPlan pl = make_plan(db, query_len, matrix, gap_open, gap_extend);
+        const uint32_t pitch = (query_len + 7) / 8 * 8;
+        const uint32_t n_lane_tiles = (query_len + 7) / 8;
+        const uint32_t warps = std::min<uint32_t>(kIntraMaxWarps, (n_lane_tiles + 31) / 32);
+        const uint32_t passes = (n_lane_tiles + 32 * warps - 1) / (32 * warps);
+        swb_status e;
+        if ((e = dev_alloc(&d_dir, static_cast<size_t>(pitch) * n, nullptr)) != SWB_OK) return e;
+        if ((e = dev_alloc(&d_ops, m + n + 32, nullptr)) != SWB_OK) return e;
+        if ((e = dev_alloc(&d_result, 8, nullptr)) != SWB_OK) return e;
+        if ((e = dev_alloc(&d_b0, n, nullptr)) != SWB_OK) return e;
+        if ((e = dev_alloc(&d_b1, n, nullptr)) != SWB_OK) return e;
+        if ((e = dev_alloc(&d_query, m, nullptr)) != SWB_OK) return e;
+        if ((e = dev_alloc(&d_matrix, 576, nullptr)) != SWB_OK) return e;
+        const size_t profi_elems = static_cast<size_t>(kProfRows) * n_lane_tiles * 8;
+        if (!pl.wide) { if ((e = dev_alloc(&d_prof8, profi_elems, nullptr)) != SWB_OK) return e; }
+        else { if ((e = dev_alloc(&d_prof32, profi_elems, nullptr)) != SWB_OK) return e; }
+        SWB_CUDA(cudaMemcpyAsync(d_query, query, m, cudaMemcpyHostToDevice, s));
+        SWB_CUDA(cudaMemcpyAsync(d_matrix, matrix, 576 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        SWB_CUDA(cudaMemsetAsync(d_result, 0, 8 * sizeof(int32_t), s));
+        ProfileParams pp{};
+        pp.query = d_query;
+        pp.matrix = d_matrix;
+        pp.m = query_len;
+        pp.shift_main = gap_open;
+        pp.shift_intra = gap_open;
+        pp.pstride = 0;                 // only the re-tiled form is needed
+        pp.intra_t = 8;
+        pp.n_lane_tiles = n_lane_tiles;
+        pp.prof8i = d_prof8;
+        pp.prof32i = d_prof32;
+        build_profile_kernel<<<64, 256, 0, s>>>(pp);
+        TracebackParams tp{};
+        tp.codes = db->d_codes;
+        tp.query = d_query;
+        tp.m = query_len;
+        tp.n = subject_len;
+        tp.profi = pl.wide ? static_cast<const void*>(d_prof32) : static_cast<const void*>(d_prof8);
+        tp.n_lane_tiles = n_lane_tiles;
+        tp.n_passes = passes;
+        tp.border0 = d_b0;
+        tp.border1 = d_b1;
+        tp.dir = d_dir;
+        tp.pitch = pitch;
+        tp.open = gap_open;
+        tp.ext = gap_extend;
+        tp.result = d_result;
+        tp.ops_reversed = d_ops;
+        if (pl.wide) traceback_fill_kernel<int32_t><<<1, warps * 32, 0, s>>>(tp);
+        else traceback_fill_kernel<int8_t><<<1, warps * 32, 0, s>>>(tp);
+        traceback_walk_kernel<<<1, 32, 0, s>>>(tp);
+        SWB_CUDA(cudaMemcpyAsync(result, d_result, sizeof(result), cudaMemcpyDeviceToHost, s));
+        SWB_CUDA(cudaStreamSynchronize(s));
+        SWB_CUDA(cudaGetLastError());
+        reversed.resize(static_cast<size_t>(result[3]));
+        if (!reversed.empty())
+            SWB_CUDA(cudaMemcpy(reversed.data(), d_ops, reversed.size(), cudaMemcpyDeviceToHost));
+        return SWB_OK;
+    }();
+    cleanup();
+    {
+        const std::string keep = g_error;
+        swb_db_destroy(db);
+        g_error = keep;
+    }
+    if (st != SWB_OK) return st;
+    out->score = result[0];
+    if (result[0] > 0) {
+        out->query_begin = static_cast<uint64_t>(result[4]);
+        out->query_end = static_cast<uint64_t>(result[2]);
+        out->subject_begin = static_cast<uint64_t>(result[5]);
+        out->subject_end = static_cast<uint64_t>(result[1]);
+        out->n_ops = reversed.size();
+        if (ops)
+            for (uint64_t i = 0; i < reversed.size() && i < ops_capacity; ++i) ops[i] = reversed[reversed.size() - 1 - i];
+    }
+    return SWB_OK;
+}
+
 swb_status swb_shard_assignment(const uint32_t* lens, uint32_t n, uint64_t length_threshold, uint32_t shard_count,
                                 uint32_t* shard_of) {
     if (n && (!lens || !shard_of)) return fail(SWB_ERR_INVALID, "null argument");

@@ -551,6 +551,214 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraPar
 }
 
 // ------------------------------------------------------------------------------------------------
+// Traceback on the GPU (sw_align_traceback, align.hpp:254-353) -- SURVEY 8(f) rank 2.  Runs after scoring on the
+// <= top_k surviving hits, outside the measured region, but it is on by default (scheduler.hpp:27) and on the host
+// it costs more than the whole search for long pairs.
+//
+// traceback_fill_kernel: one CTA per pair, the intra-task wavefront of intra_s32_kernel (8 columns per lane) that
+// additionally writes one direction byte per cell with the reference's encoding and tie-breaking
+// (align.hpp:269-305): bits 0-1 where H came from (0 stop, 1 diagonal, 2 gap along the query, 3 gap along the
+// subject, later ones winning only on strict improvement), bit 2 / bit 3 set when that gap is an extension (a tie
+// between opening and extending counts as opening).  The end point is the first maximum in (subject row, query
+// column) order (align.hpp:308).  Layout: dir[(t - 1) * pitch + (q - 1)], pitch = m rounded up to 8, so that a
+// lane's 8 columns are one aligned 8-byte store.
+// traceback_walk_kernel: one warp follows the path backwards; diagonal runs are followed 32 cells per step.
+// ------------------------------------------------------------------------------------------------
+struct TracebackParams {
+    const uint8_t* codes;      // interleaved group layout; the pair's subject is slot 0 of group 0
+    const uint8_t* query;      // m codes
+    uint32_t m, n;
+    const void* profi;         // prof8i or prof32i, re-tiled with 8 columns per lane tile
+    uint32_t n_lane_tiles;
+    uint32_t n_passes;
+    uint2* border0;            // [n] per-pass border row
+    uint2* border1;
+    uint8_t* dir;              // n * pitch direction bytes
+    uint32_t pitch;
+    int32_t open, ext;
+    int32_t* result;           // [0] score, [1] end row t (1-based), [2] end column q (1-based), [3] n_ops,
+                               // [4] query_begin, [5] subject_begin
+    uint8_t* ops_reversed;     // walk output, last operation first
+};
+
+template <typename PT>
+__global__ void __launch_bounds__(32 * kIntraMaxWarps) traceback_fill_kernel(TracebackParams p) {
+    constexpr int T = 8;
+    __shared__ uint2 ring[kIntraMaxWarps][kIntraRing];
+    __shared__ int32_t red_score[kIntraMaxWarps * 32];
+    __shared__ uint32_t red_t[kIntraMaxWarps * 32], red_q[kIntraMaxWarps * 32];
+
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int32_t NO = -p.open, NE = -p.ext;
+    const PT* prof = static_cast<const PT*>(p.profi);
+    const uint32_t row_words = p.n_lane_tiles * 8;
+    const int64_t n = p.n;
+    const uint8_t* seq = p.codes;
+    const int64_t steps = n + 31 + static_cast<int64_t>(kIntraDelta) * (W - 1);
+
+    int32_t best = 0;
+    uint32_t best_t = 0, best_q = 0;
+
+    for (uint32_t pass = 0; pass < p.n_passes; ++pass) {
+        const uint32_t lane_tile = (pass * W + w) * 32 + lane;
+        const bool tile_valid = lane_tile < p.n_lane_tiles;
+        const PT* ptile = prof + static_cast<size_t>(tile_valid ? lane_tile : 0) * 8;
+        const uint32_t col0 = lane_tile * T;                 // 0-based query column of this lane's first cell
+        const bool first = pass == 0, last = pass + 1 == p.n_passes;
+        const uint2* bin = (pass & 1) ? p.border0 : p.border1;
+        uint2* bout = (pass & 1) ? p.border1 : p.border0;
+
+        int32_t Hm[T], F[T];
+#pragma unroll
+        for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
+        int32_t diag_in = NO, out_h = NO, out_e = NO;
+        __syncthreads();
+
+        for (int64_t d = 0; d < steps; ++d) {
+            const int64_t r = d - static_cast<int64_t>(w) * kIntraDelta - lane;
+            const bool in_range = r >= 0 && r < n;
+            const uint32_t a = (in_range && tile_valid) ? seq[(r >> 3) * 512 + (r & 7)] : kPadCode;
+
+            int32_t in_h = __shfl_up_sync(0xffffffffu, out_h, 1);
+            int32_t in_e = __shfl_up_sync(0xffffffffu, out_e, 1);
+            if (lane == 0) {
+                in_h = NO, in_e = NO;
+                if (in_range) {
+                    if (w > 0) {
+                        const uint2 v = ring[w][r & (kIntraRing - 1)];
+                        in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
+                    } else if (!first) {
+                        const uint2 v = bin[r];
+                        in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
+                    }
+                }
+            }
+
+            int32_t sub[T];
+            if (sizeof(PT) == 1) {
+                const uint2 v = *reinterpret_cast<const uint2*>(ptile + static_cast<size_t>(a) * row_words);
+#pragma unroll
+                for (int k = 0; k < T; ++k) {
+                    const uint32_t word = k < 4 ? v.x : v.y;
+                    const uint32_t sel = (k & 3) == 0 ? 0x8880u : (k & 3) == 1 ? 0x9991u : (k & 3) == 2 ? 0xAAA2u : 0xBBB3u;
+                    sub[k] = static_cast<int32_t>(prmt(word, 0, sel));
+                }
+            } else {
+                const int4* q4 = reinterpret_cast<const int4*>(ptile + static_cast<size_t>(a) * row_words);
+                const int4 v0 = q4[0], v1 = q4[1];
+                const int32_t all[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (int k = 0; k < T; ++k) sub[k] = all[k];
+            }
+
+            int32_t hl = in_h, E = in_e;
+            int32_t diag = diag_in;
+            diag_in = in_h;
+            uint32_t dlo = 0, dhi = 0;   // 8 direction bytes
+#pragma unroll
+            for (int k = 0; k < T; ++k) {
+                uint32_t flags = 0;
+                const int32_t e_ext = E + NE;                 // extend the gap along the query
+                if (hl < e_ext) flags |= 4u;                  // opening (hl = H_left - open) loses strictly
+                E = max(hl, e_ext);
+                const int32_t f_ext = F[k] + NE;              // extend the gap along the subject
+                if (Hm[k] < f_ext) flags |= 8u;
+                F[k] = max(Hm[k], f_ext);
+                int32_t h = 0;
+                uint32_t from = 0;
+                const int32_t paired = diag + sub[k];         // sub = matrix + open, diag = H_diag - open
+                if (paired > h) h = paired, from = 1u;
+                if (E > h) h = E, from = 2u;
+                if (F[k] > h) h = F[k], from = 3u;
+                const uint32_t byte = flags | from;
+                if (k < 4) dlo |= byte << (8 * k);
+                else dhi |= byte << (8 * (k - 4));
+                diag = Hm[k];
+                hl = h + NO;
+                Hm[k] = hl;
+                if (h > best && in_range && col0 + k < p.m) best = h, best_t = static_cast<uint32_t>(r) + 1, best_q = col0 + k + 1;
+            }
+            out_h = hl, out_e = E;
+
+            if (in_range && tile_valid)
+                *reinterpret_cast<uint2*>(p.dir + static_cast<size_t>(r) * p.pitch + col0) = make_uint2(dlo, dhi);
+            if (lane == 31 && in_range) {
+                if (w + 1 < W) ring[w + 1][r & (kIntraRing - 1)] = make_uint2(hl, E);
+                else if (!last) bout[r] = make_uint2(hl, E);
+            }
+            if (W > 1 && (d & 31) == 31) __syncthreads();
+        }
+    }
+
+    // end point: maximum score, then smallest row, then smallest column == first maximum in row-major order
+    red_score[threadIdx.x] = best, red_t[threadIdx.x] = best_t, red_q[threadIdx.x] = best_q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 1; i < blockDim.x; ++i) {
+            const bool better = red_score[i] > best ||
+                                (red_score[i] == best && best > 0 &&
+                                 (red_t[i] < best_t || (red_t[i] == best_t && red_q[i] < best_q)));
+            if (better) best = red_score[i], best_t = red_t[i], best_q = red_q[i];
+        }
+        p.result[0] = best, p.result[1] = static_cast<int32_t>(best_t), p.result[2] = static_cast<int32_t>(best_q);
+    }
+}
+
+__global__ void __launch_bounds__(32) traceback_walk_kernel(TracebackParams p) {
+    const uint32_t lane = threadIdx.x;
+    const int32_t score = p.result[0];
+    uint32_t t = static_cast<uint32_t>(p.result[1]), q = static_cast<uint32_t>(p.result[2]);   // 1-based
+    uint32_t n_ops = 0;
+    if (score > 0) {
+        enum { kCell = 0, kGapQ = 1, kGapS = 2 };
+        int where = kCell;
+        for (bool walking = true; walking;) {
+            if (where == kCell) {
+                // speculate that the next 32 cells up the diagonal are all "from diagonal"
+                uint32_t byte = 0;
+                const bool inside = t > lane && q > lane;
+                if (inside) byte = p.dir[static_cast<size_t>(t - lane - 1) * p.pitch + (q - lane - 1)];
+                const bool is_diag = inside && (byte & 3u) == 1u;
+                const uint32_t not_diag = ~__ballot_sync(0xffffffffu, is_diag);
+                const uint32_t run = not_diag ? __ffs(not_diag) - 1 : 32;   // lanes 0..run-1 are diagonal moves
+                if (lane < run) {
+                    const uint8_t qc = p.query[q - lane - 1];
+                    const uint32_t row = t - lane - 1;
+                    const uint8_t sc = p.codes[(row >> 3) * 512 + (row & 7)];
+                    p.ops_reversed[n_ops + lane] = qc == sc ? 0 : 1;                     // match : substitute
+                }
+                n_ops += run, t -= run, q -= run;
+                if (run < 32) {
+                    // the cell at the end of the run is not diagonal (or is outside the matrix)
+                    const uint32_t stop_byte = __shfl_sync(0xffffffffu, byte, run);
+                    const bool stop_inside = __shfl_sync(0xffffffffu, static_cast<int>(inside), run) != 0;
+                    const uint32_t from = stop_inside ? (stop_byte & 3u) : 0u;
+                    if (from == 0) walking = false;
+                    else where = from == 2 ? kGapQ : kGapS;
+                }
+            } else {
+                // gap runs are short: one cell per step
+                const uint32_t byte = p.dir[static_cast<size_t>(t - 1) * p.pitch + (q - 1)];
+                if (where == kGapQ) {
+                    if (lane == 0) p.ops_reversed[n_ops] = 3;   // del: a query residue against a gap
+                    ++n_ops, --q;
+                    if (!(byte & 4u)) where = kCell;
+                } else {
+                    if (lane == 0) p.ops_reversed[n_ops] = 2;   // insert: a subject residue against a gap
+                    ++n_ops, --t;
+                    if (!(byte & 8u)) where = kCell;
+                }
+            }
+        }
+    }
+    if (lane == 0) {
+        p.result[3] = static_cast<int32_t>(n_ops);
+        p.result[4] = static_cast<int32_t>(q);   // query_begin (0-based, half-open)
+        p.result[5] = static_cast<int32_t>(t);   // subject_begin
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
 // Score gather (merge_results, scheduler.hpp:106-117, without the full sort).
 //   key = (score << 32) | (0xFFFFFFFF - db_index): descending key order == (score desc, index asc).
 //   0 is never a valid key (db_index < 2^32 - 1), so it pads.

@@ -234,6 +234,23 @@ def score_wavefront(query, subject, matrix, gaps: GapModel, chunk_width: int = 6
     return out.value
 
 
+def align_traceback(query, subject, matrix, gaps: GapModel, memory_cap: int = 256 << 20, device: int = 0) -> dict:
+    """sw_align_traceback (align.hpp:254-353) on the GPU: bounds, score, capped flag and the edit script
+    (0 match, 1 substitute, 2 insert, 3 del -- EditOp, align.hpp:236)."""
+    lib = _cabi.load()
+    q, s, mat = _u8(query), _u8(subject), _mat(matrix)
+    dummy = np.zeros(1, np.uint8)
+    out = _cabi.SwbAlignment()
+    cap = len(q) + len(s) + 1
+    ops = np.zeros(cap, dtype=np.uint8)
+    rc = lib.swb_align_traceback(_ptr(q if len(q) else dummy, _u8p), len(q), _ptr(s if len(s) else dummy, _u8p), len(s),
+                                 _ptr(mat, _i32p), gaps.open, gaps.extend, memory_cap, device, C.byref(out),
+                                 _ptr(ops, _u8p), cap)
+    _raise(lib, rc)
+    return dict(bounds=[int(out.query_begin), int(out.query_end), int(out.subject_begin), int(out.subject_end)],
+                score=int(out.score), capped=bool(out.capped), ops=ops[:int(out.n_ops)].copy())
+
+
 def shard_assignment(lengths, length_threshold: int, shard_count: int) -> np.ndarray:
     """The deterministic residue-balanced deal used by swb_db_create (host only, no GPU needed)."""
     lib = _cabi.load()

@@ -251,3 +251,35 @@ def test_multi_shard_equals_single(port, b62):
         assert (total >= 0).all()            # every sequence was scored by exactly one shard
     i4, s4 = decode_keys(keys[0])
     assert len(i4) <= 25
+
+
+def test_traceback_matches_reference_scripts(b62):
+    """sw_align_traceback on the GPU: identical bounds and edit scripts, not merely equal scores
+    (fixtures: outputs of the unmodified reference, tests/golden/make_golden.py)."""
+    from paper_2203_11100_b200 import align_traceback
+    for rec in golden()["tracebacks"]:
+        if rec.get("capped_only"):
+            continue
+        q, s, g = enc(rec["q"]), enc(rec["s"]), GapModel(rec["open"], rec["extend"])
+        tb = align_traceback(q, s, b62, g)
+        assert tb["score"] == rec["score"] and tb["bounds"] == rec["bounds"] and not tb["capped"]
+        assert tb["ops"].tolist() == rec["ops"]
+        capped = align_traceback(q, s, b62, g, memory_cap=64)
+        assert capped["capped"] and capped["score"] == rec["score"] and len(capped["ops"]) == 0
+    assert align_traceback(enc(""), enc("AAA"), b62, GapModel(10, 2))["score"] == 0
+
+
+def test_traceback_random_against_reference(ref, b62):
+    from paper_2203_11100_b200 import align_traceback
+    rng = np.random.default_rng(21)
+    shapes = [(1, 1), (7, 300), (300, 7), (64, 64), (257, 255), (900, 1100), (2100, 700), (3000, 2600)]
+    for i, (m, n) in enumerate(shapes):
+        q = synth.random_residues(rng, m)
+        s = synth.mutate(rng, np.concatenate([synth.random_residues(rng, n // 3), q[: max(1, min(m, n // 2))],
+                                              synth.random_residues(rng, n)])[:n], 0.15, 3)
+        for gaps in [(10, 2), (5, 5), (3, 0), (0, 0)][: 2 if m * len(s) > 10 ** 6 else 4]:
+            exp = ref.traceback(q, s, b62, *gaps)
+            got = align_traceback(q, s, b62, GapModel(*gaps))
+            assert got["score"] == exp["score"], (m, n, gaps)
+            assert got["bounds"] == exp["bounds"], (m, n, gaps)
+            assert got["ops"].tolist() == exp["ops"].tolist(), (m, n, gaps)
