@@ -116,6 +116,12 @@ swb_status swb_db_create_flat(const uint8_t* codes, const uint64_t* offsets, uin
                               uint64_t length_threshold, int32_t device, uint32_t shard_rank,
                               uint32_t shard_count, swb_db** out);
 
+/* On-disk packed database: the shard exactly as it sits in HBM -- sorted, grouped,
+ * interleaved, with its index tables -- so that a later process skips parsing, sorting and packing.
+ * Little-endian, versioned; swb_db_load rejects files of another version or with a damaged header. */
+swb_status swb_db_save(swb_db* db, const char* path);
+swb_status swb_db_load(const char* path, int32_t device, swb_db** out);
+
 void swb_db_destroy(swb_db* db);
 swb_status swb_db_info_get(const swb_db* db, swb_db_info* info);
 

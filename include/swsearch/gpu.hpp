@@ -76,16 +76,19 @@ struct Fingerprint {
     }
 };
 
+// O(1) per call (it runs on every run_search): the element count, the address of the sequence array and a
+// sample of 64 sequences (length, first and last residue, address of the residues).
 inline Fingerprint fingerprint(const SequenceDatabase& db) {
     Fingerprint f;
     f.count = db.sequences.size();
     f.storage = db.sequences.data();
+    f.residues = db.total_residues;
     const std::size_t stride = f.count / 64 + 1;
-    for (std::size_t i = 0; i < f.count; ++i) {
+    for (std::size_t i = 0; i < f.count; i += stride) {
         const auto& codes = db.sequences[i].codes;
-        f.residues += codes.size();
-        if (i % stride == 0 && !codes.empty())
-            f.sample = f.sample * 1099511628211ull + codes.front() * 31u + codes.back() * 7u + codes.size();
+        f.sample = f.sample * 1099511628211ull + codes.size() * 131u +
+                   static_cast<std::uint64_t>(reinterpret_cast<std::uintptr_t>(codes.data()));
+        if (!codes.empty()) f.sample = f.sample * 31u + codes.front() * 7u + codes.back();
     }
     return f;
 }

@@ -76,6 +76,8 @@ SIGNATURES = {
     "swb_db_create_flat": (C.c_int, [u8p, u64p, C.c_uint32, C.c_uint64, C.c_int32, C.c_uint32, C.c_uint32,
                                      C.POINTER(C.c_void_p)]),
     "swb_db_destroy": (None, [C.c_void_p]),
+    "swb_db_save": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "swb_db_load": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),
     "swb_db_info_get": (C.c_int, [C.c_void_p, C.POINTER(SwbDbInfo)]),
     "swb_db_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "swb_search": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32,

@@ -212,8 +212,10 @@ swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len
                 return;
             }
             DeviceGuard guard(db->device);
-            // zero-padded send buffer (a shard may hold fewer than k sequences)
-            cudaError_t e = cudaMemcpyAsync(mdb->d_send[r], host.data(), k * sizeof(uint64_t), cudaMemcpyHostToDevice, db->stream);
+            // the shard's keys are already on its device; only a shard holding fewer than k sequences goes
+            // through the zero-padded host copy
+            cudaError_t e = dkeys ? cudaMemcpyAsync(mdb->d_send[r], dkeys, k * sizeof(uint64_t), cudaMemcpyDeviceToDevice, db->stream)
+                                  : cudaMemcpyAsync(mdb->d_send[r], host.data(), k * sizeof(uint64_t), cudaMemcpyHostToDevice, db->stream);
             if (e == cudaSuccess) e = cudaStreamSynchronize(db->stream);
             if (e != cudaSuccess) {
                 sts[r] = SWB_ERR_CUDA;

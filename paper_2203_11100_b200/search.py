@@ -101,6 +101,20 @@ class Database:
         codes = np.concatenate([_u8(s) for s in seqs]) if len(seqs) and offsets[-1] else np.zeros(0, np.uint8)
         return cls(codes, offsets, **kw)
 
+    @classmethod
+    def load(cls, path: str, device: int = 0):
+        """Open a packed database written by save(): no parsing, sorting or packing."""
+        self = cls.__new__(cls)
+        self._lib = _cabi.load()
+        self._h = C.c_void_p()
+        _raise(self._lib, self._lib.swb_db_load(str(path).encode(), device, C.byref(self._h)))
+        self.device = device
+        self.n_total = self.info()["n_total"]
+        return self
+
+    def save(self, path: str):
+        _raise(self._lib, self._lib.swb_db_save(self._h, str(path).encode()))
+
     def close(self):
         if self._h:
             self._lib.swb_db_destroy(self._h)

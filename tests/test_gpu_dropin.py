@@ -29,3 +29,31 @@ def test_dropin_output_equals_reference_binary(lib):
     if not REF.exists():
         pytest.skip("oracle/_ref/dropin_ref did not travel")
     assert _run(MINE) == _run(REF)
+
+
+def test_cli_search_and_bench(lib, tmp_path, port):
+    """The CLI on the GPU: ranked hits equal the oracle's, bench emits the SPEC's CSV."""
+    import numpy as np
+    from oracle import pyoracle as po
+    from paper_2203_11100_b200 import synth
+    cli = ROOT / "tests" / "cpp" / "_build" / "swsearch"
+    rng = np.random.default_rng(31)
+    letters = lambda codes: "".join(synth.ALPHABET[c] for c in codes)
+    q = synth.random_residues(rng, 120)
+    seqs = [synth.random_residues(rng, int(rng.integers(1, 300))) for _ in range(80)]
+    seqs[13] = synth.mutate(rng, q, 0.1, 1)
+    (tmp_path / "q.fa").write_text(">query one\n" + letters(q) + "\n")
+    (tmp_path / "db.fa").write_text("".join(f">s{i}\n{letters(s)}\n" for i, s in enumerate(seqs)))
+    out = subprocess.run([str(cli), "search", "-q", str(tmp_path / "q.fa"), "-d", str(tmp_path / "db.fa"), "--top-k", "5"],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    ei, es, _ = port.run_search(q, po.FlatDb.from_list(seqs), synth.blosum62(), 10, 2, top_k=5)
+    rows = [l.split("\t") for l in out.stdout.splitlines() if l.startswith("  ") and "\t" in l]
+    assert [r[1] for r in rows] == [f"s{i}" for i in ei] and [int(r[2]) for r in rows] == es.tolist()
+    assert "q[" in rows[0][3]
+    csv = subprocess.run([str(cli), "bench", "-q", str(tmp_path / "q.fa"), "-d", str(tmp_path / "db.fa"), "--repetitions", "3"],
+                         capture_output=True, text=True, timeout=600)
+    assert csv.returncode == 0, csv.stderr
+    lines = csv.stdout.splitlines()
+    assert lines[0] == "query_id,query_length,repetitions,mean_gcups,min_gcups,max_gcups,stddev_gcups"
+    assert lines[1].startswith("0,120,3,") and len(lines) == 2

@@ -283,3 +283,25 @@ def test_traceback_random_against_reference(ref, b62):
             assert got["score"] == exp["score"], (m, n, gaps)
             assert got["bounds"] == exp["bounds"], (m, n, gaps)
             assert got["ops"].tolist() == exp["ops"].tolist(), (m, n, gaps)
+
+
+def test_packed_database_file_round_trip(tmp_path, b62):
+    qs, sdb = synth.config1()
+    g = GapModel(10, 2)
+    path = tmp_path / "config1.swb"
+    with Database(sdb.codes, sdb.offsets, shard_rank=1, shard_count=3) as db:
+        i1, s1, _ = db.search(qs[0], b62, g, 30)
+        info1 = db.info()
+        db.save(path)
+    with Database.load(path) as db2:
+        i2, s2, _ = db2.search(qs[0], b62, g, 30)
+        info2 = db2.info()
+    assert (i1 == i2).all() and (s1 == s2).all()
+    for key in ("n_total", "n_local", "n_short", "n_long", "n_groups", "residues", "shard_rank", "shard_count", "max_length"):
+        assert info1[key] == info2[key]
+    bad = tmp_path / "bad.swb"
+    bad.write_bytes(path.read_bytes()[:100])
+    with pytest.raises(ValueError):
+        Database.load(bad)
+    with pytest.raises(ValueError):
+        Database.load(tmp_path / "missing.swb")

@@ -108,3 +108,38 @@ def test_synth_is_deterministic_and_shaped():
     assert synth.QUERY_LENGTHS[0] == 144 and synth.QUERY_LENGTHS[-1] == 5478 and len(synth.QUERY_LENGTHS) == 20
     # the GCUPS identity of SPEC.md:370
     assert abs(144 * synth.SWISSPROT_RESIDUES / 1.0 / 1e9 - 29.4009) < 1e-3
+
+
+def _cpp_build():
+    import subprocess
+    subprocess.check_call(["make", "-C", str(ROOT / "tests" / "cpp"), "all"], stdout=subprocess.DEVNULL)
+    return ROOT / "tests" / "cpp" / "_build"
+
+
+def test_bench_header_spec_examples(lib):
+    """swsearch/bench.hpp: GCUPS formula, measurement_error, CSV schema."""
+    import subprocess
+    out = subprocess.run([str(_cpp_build() / "bench_unit")], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "bench_unit: ok" in out.stdout
+
+
+def test_cli_usage_and_exit_codes(lib, tmp_path):
+    """tools/swsearch_cli.cpp: validation before any file is opened, stats output, exit codes."""
+    import subprocess
+    cli = str(_cpp_build() / "swsearch")
+    run = lambda *a: subprocess.run([cli, *a], capture_output=True, text=True)
+    assert run("--help").returncode == 0 and run("--help").stdout.startswith("usage: swsearch")
+    assert run("search").returncode == 2                                   # no db -> usage error
+    assert run("search", "-d", "x.fa").returncode == 2                     # no query
+    assert run("bench", "-d", "x.fa", "-q", "y.fa", "--repetitions", "abc").returncode == 2
+    assert run("frobnicate", "-d", "x.fa").returncode == 2
+    assert run("sweep", "-d", "x.fa", "-q", "y.fa").returncode == 2        # --values missing
+    assert run("stats", "-d", str(tmp_path / "missing.fa")).returncode == 3
+    fa = tmp_path / "db.fa"
+    fa.write_text(">a first\nARNDARND\n>b\n\n>c\nWWWWWWWWWWWWWWWWWWW\n")
+    out = run("stats", "-d", str(fa))
+    assert out.returncode == 0 and out.stdout == "3 sequences, 27 residues, max 19\n"
+    bad = tmp_path / "bad.fa"
+    bad.write_text("ACGT\n")
+    assert run("stats", "-d", str(bad)).returncode == 4                    # format error
