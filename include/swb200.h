@@ -194,6 +194,15 @@ swb_status swb_align_traceback(const uint8_t* query, uint32_t query_len, const u
                                int32_t gap_extend, uint64_t memory_cap, int32_t device,
                                swb_alignment* out, uint8_t* ops, uint64_t ops_capacity);
 
+/* Tracebacks for hits of a search, straight from the resident database (no subject upload): all pairs are filled
+ * in one launch (one CTA each) and walked in another.  hits[i].db_index must belong to this shard; hits[i].score
+ * is returned as the score of capped pairs.  ops receives the scripts back to back: hit i's operations start at
+ * ops[ops_offset[i]] and may use up to ops_offset[i+1] - ops_offset[i] bytes (query_len + subject length is
+ * always enough). */
+swb_status swb_db_align_hits(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
+                             int32_t gap_open, int32_t gap_extend, const swb_hit* hits, uint32_t n_hits,
+                             uint64_t memory_cap, swb_alignment* out, uint8_t* ops, const uint64_t* ops_offset);
+
 /* ---- several GPUs, one process (the C++ drop-in's multi-GPU mode) ------------------------------
  * The database is dealt by residue count over `n_devices` GPUs; each search runs all shards
  * concurrently, then the per-shard top-k keys are exchanged with one ncclAllGather and merged.
@@ -208,6 +217,10 @@ void swb_mdb_destroy(swb_mdb* mdb);
 swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len,
                           const int32_t* matrix, int32_t gap_open, int32_t gap_extend,
                           uint32_t top_k, swb_hit* hits, uint32_t* n_hits, swb_stats* stats);
+/* swb_db_align_hits routed to the shards that own the hits. */
+swb_status swb_mdb_align_hits(swb_mdb* mdb, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
+                              int32_t gap_open, int32_t gap_extend, const swb_hit* hits, uint32_t n_hits,
+                              uint64_t memory_cap, swb_alignment* out, uint8_t* ops, const uint64_t* ops_offset);
 uint32_t swb_mdb_shard_count(const swb_mdb* mdb);
 swb_db* swb_mdb_shard(swb_mdb* mdb, uint32_t i);
 

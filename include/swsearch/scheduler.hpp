@@ -169,9 +169,32 @@ inline RankedResults run_search(const EncodedSequence& query, const SequenceData
         }
     }
 
-    if (config.compute_alignments)
-        for (Hit& hit : results.hits)
-            hit.alignment = sw_align_traceback(query, db.sequences[hit.db_index], matrix, gaps, config.traceback_memory_cap);
+    if (config.compute_alignments && !results.hits.empty()) {
+        // all surviving hits are traced back on the GPU in one go, straight from the resident database
+        const std::size_t count = results.hits.size();
+        std::vector<swb_hit> raw_hits(count);
+        std::vector<std::uint64_t> offsets(count + 1, 0);
+        for (std::size_t i = 0; i < count; ++i) {
+            raw_hits[i] = swb_hit{results.hits[i].db_index, results.hits[i].score.value};
+            offsets[i + 1] = offsets[i] + query.length() + db.sequences[results.hits[i].db_index].length();
+        }
+        std::vector<swb_alignment> raw(count);
+        std::vector<std::uint8_t> scripts(std::max<std::uint64_t>(offsets[count], 1));
+        gpu::check(swb_mdb_align_hits(resident, query.codes.data(), static_cast<std::uint32_t>(query.length()),
+                                      gpu::matrix_table(matrix), gaps.open(), gaps.extend(), raw_hits.data(),
+                                      static_cast<std::uint32_t>(count), config.traceback_memory_cap, raw.data(),
+                                      scripts.data(), offsets.data()));
+        for (std::size_t i = 0; i < count; ++i) {
+            Alignment a;
+            a.score = {raw[i].score};
+            a.capped = raw[i].capped != 0;
+            a.query_begin = raw[i].query_begin, a.query_end = raw[i].query_end;
+            a.subject_begin = raw[i].subject_begin, a.subject_end = raw[i].subject_end;
+            a.ops.resize(raw[i].n_ops);
+            for (std::size_t k = 0; k < a.ops.size(); ++k) a.ops[k] = static_cast<EditOp>(scripts[offsets[i] + k]);
+            results.hits[i].alignment = std::move(a);
+        }
+    }
     return results;
 }
 

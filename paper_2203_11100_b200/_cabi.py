@@ -92,6 +92,10 @@ SIGNATURES = {
                                  C.c_int32, i32p]),
     "swb_align_traceback": (C.c_int, [u8p, C.c_uint32, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint64,
                                       C.c_int32, C.POINTER(SwbAlignment), u8p, C.c_uint64]),
+    "swb_db_align_hits": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.POINTER(SwbHit), C.c_uint32,
+                                    C.c_uint64, C.POINTER(SwbAlignment), u8p, u64p]),
+    "swb_mdb_align_hits": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.POINTER(SwbHit), C.c_uint32,
+                                     C.c_uint64, C.POINTER(SwbAlignment), u8p, u64p]),
     "swb_mdb_create_flat": (C.c_int, [u8p, u64p, C.c_uint32, C.c_uint64, i32p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "swb_mdb_create": (C.c_int, [C.POINTER(u8p), u32p, C.c_uint32, C.c_uint64, i32p, C.c_uint32,
                                  C.POINTER(C.c_void_p)]),

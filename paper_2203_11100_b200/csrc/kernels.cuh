@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraPar
 // <= top_k surviving hits, outside the measured region, but it is on by default (scheduler.hpp:27) and on the host
 // it costs more than the whole search for long pairs.
 //
-// traceback_fill_kernel: one CTA per pair, the intra-task wavefront of intra_s32_kernel (8 columns per lane) that
+// traceback_fill_kernel: one CTA per pair (all pairs of a search in one launch), the intra-task wavefront of intra_s32_kernel (8 columns per lane) that
 // additionally writes one direction byte per cell with the reference's encoding and tie-breaking
 // (align.hpp:269-305): bits 0-1 where H came from (0 stop, 1 diagonal, 2 gap along the query, 3 gap along the
 // subject, later ones winning only on strict improvement), bit 2 / bit 3 set when that gap is an extension (a tie
@@ -564,20 +564,30 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraPar
 // lane's 8 columns are one aligned 8-byte store.
 // traceback_walk_kernel: one warp follows the path backwards; diagonal runs are followed 32 cells per step.
 // ------------------------------------------------------------------------------------------------
+struct TracebackJob {
+    uint64_t codes_off;   // byte offset of the subject's first residue in the interleaved layout
+    uint64_t dir_off;     // byte offset of this pair's direction matrix
+    uint64_t border_off;  // element offset of this pair's per-pass border rows
+    uint64_t ops_off;     // byte offset of this pair's (reversed) edit script
+    uint32_t n;           // subject length
+    uint32_t result_off;  // index of this pair's 8-int result record
+};
+
 struct TracebackParams {
-    const uint8_t* codes;      // interleaved group layout; the pair's subject is slot 0 of group 0
+    const uint8_t* codes;      // interleaved group layout of the resident database
     const uint8_t* query;      // m codes
-    uint32_t m, n;
+    const TracebackJob* jobs;  // one per CTA
+    uint32_t m;
     const void* profi;         // prof8i or prof32i, re-tiled with 8 columns per lane tile
     uint32_t n_lane_tiles;
     uint32_t n_passes;
-    uint2* border0;            // [n] per-pass border row
+    uint2* border0;
     uint2* border1;
-    uint8_t* dir;              // n * pitch direction bytes
-    uint32_t pitch;
+    uint8_t* dir;
+    uint32_t pitch;            // m rounded up to 8
     int32_t open, ext;
-    int32_t* result;           // [0] score, [1] end row t (1-based), [2] end column q (1-based), [3] n_ops,
-                               // [4] query_begin, [5] subject_begin
+    int32_t* result;           // per job: [0] score, [1] end row t (1-based), [2] end column q (1-based), [3] n_ops,
+                               //          [4] query_begin, [5] subject_begin
     uint8_t* ops_reversed;     // walk output, last operation first
 };
 
@@ -592,8 +602,10 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) traceback_fill_kernel(Tra
     const int32_t NO = -p.open, NE = -p.ext;
     const PT* prof = static_cast<const PT*>(p.profi);
     const uint32_t row_words = p.n_lane_tiles * 8;
-    const int64_t n = p.n;
-    const uint8_t* seq = p.codes;
+    const TracebackJob job = p.jobs[blockIdx.x];
+    const int64_t n = job.n;
+    const uint8_t* seq = p.codes + job.codes_off;
+    uint8_t* const dir = p.dir + job.dir_off;
     const int64_t steps = n + 31 + static_cast<int64_t>(kIntraDelta) * (W - 1);
 
     int32_t best = 0;
@@ -605,8 +617,8 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) traceback_fill_kernel(Tra
         const PT* ptile = prof + static_cast<size_t>(tile_valid ? lane_tile : 0) * 8;
         const uint32_t col0 = lane_tile * T;                 // 0-based query column of this lane's first cell
         const bool first = pass == 0, last = pass + 1 == p.n_passes;
-        const uint2* bin = (pass & 1) ? p.border0 : p.border1;
-        uint2* bout = (pass & 1) ? p.border1 : p.border0;
+        const uint2* bin = ((pass & 1) ? p.border0 : p.border1) + job.border_off;
+        uint2* bout = ((pass & 1) ? p.border1 : p.border0) + job.border_off;
 
         int32_t Hm[T], F[T];
 #pragma unroll
@@ -681,7 +693,7 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) traceback_fill_kernel(Tra
             out_h = hl, out_e = E;
 
             if (in_range && tile_valid)
-                *reinterpret_cast<uint2*>(p.dir + static_cast<size_t>(r) * p.pitch + col0) = make_uint2(dlo, dhi);
+                *reinterpret_cast<uint2*>(dir + static_cast<size_t>(r) * p.pitch + col0) = make_uint2(dlo, dhi);
             if (lane == 31 && in_range) {
                 if (w + 1 < W) ring[w + 1][r & (kIntraRing - 1)] = make_uint2(hl, E);
                 else if (!last) bout[r] = make_uint2(hl, E);
@@ -700,14 +712,20 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) traceback_fill_kernel(Tra
                                  (red_t[i] < best_t || (red_t[i] == best_t && red_q[i] < best_q)));
             if (better) best = red_score[i], best_t = red_t[i], best_q = red_q[i];
         }
-        p.result[0] = best, p.result[1] = static_cast<int32_t>(best_t), p.result[2] = static_cast<int32_t>(best_q);
+        int32_t* result = p.result + static_cast<size_t>(job.result_off) * 8;
+        result[0] = best, result[1] = static_cast<int32_t>(best_t), result[2] = static_cast<int32_t>(best_q);
     }
 }
 
 __global__ void __launch_bounds__(32) traceback_walk_kernel(TracebackParams p) {
     const uint32_t lane = threadIdx.x;
-    const int32_t score = p.result[0];
-    uint32_t t = static_cast<uint32_t>(p.result[1]), q = static_cast<uint32_t>(p.result[2]);   // 1-based
+    const TracebackJob job = p.jobs[blockIdx.x];
+    int32_t* const result = p.result + static_cast<size_t>(job.result_off) * 8;
+    const uint8_t* const dir = p.dir + job.dir_off;
+    const uint8_t* const seq = p.codes + job.codes_off;
+    uint8_t* const ops = p.ops_reversed + job.ops_off;
+    const int32_t score = result[0];
+    uint32_t t = static_cast<uint32_t>(result[1]), q = static_cast<uint32_t>(result[2]);   // 1-based
     uint32_t n_ops = 0;
     if (score > 0) {
         enum { kCell = 0, kGapQ = 1, kGapS = 2 };
@@ -717,15 +735,15 @@ __global__ void __launch_bounds__(32) traceback_walk_kernel(TracebackParams p) {
                 // speculate that the next 32 cells up the diagonal are all "from diagonal"
                 uint32_t byte = 0;
                 const bool inside = t > lane && q > lane;
-                if (inside) byte = p.dir[static_cast<size_t>(t - lane - 1) * p.pitch + (q - lane - 1)];
+                if (inside) byte = dir[static_cast<size_t>(t - lane - 1) * p.pitch + (q - lane - 1)];
                 const bool is_diag = inside && (byte & 3u) == 1u;
                 const uint32_t not_diag = ~__ballot_sync(0xffffffffu, is_diag);
                 const uint32_t run = not_diag ? __ffs(not_diag) - 1 : 32;   // lanes 0..run-1 are diagonal moves
                 if (lane < run) {
                     const uint8_t qc = p.query[q - lane - 1];
                     const uint32_t row = t - lane - 1;
-                    const uint8_t sc = p.codes[(row >> 3) * 512 + (row & 7)];
-                    p.ops_reversed[n_ops + lane] = qc == sc ? 0 : 1;                     // match : substitute
+                    const uint8_t sc = seq[(row >> 3) * 512 + (row & 7)];
+                    ops[n_ops + lane] = qc == sc ? 0 : 1;                                // match : substitute
                 }
                 n_ops += run, t -= run, q -= run;
                 if (run < 32) {
@@ -738,13 +756,13 @@ __global__ void __launch_bounds__(32) traceback_walk_kernel(TracebackParams p) {
                 }
             } else {
                 // gap runs are short: one cell per step
-                const uint32_t byte = p.dir[static_cast<size_t>(t - 1) * p.pitch + (q - 1)];
+                const uint32_t byte = dir[static_cast<size_t>(t - 1) * p.pitch + (q - 1)];
                 if (where == kGapQ) {
-                    if (lane == 0) p.ops_reversed[n_ops] = 3;   // del: a query residue against a gap
+                    if (lane == 0) ops[n_ops] = 3;   // del: a query residue against a gap
                     ++n_ops, --q;
                     if (!(byte & 4u)) where = kCell;
                 } else {
-                    if (lane == 0) p.ops_reversed[n_ops] = 2;   // insert: a subject residue against a gap
+                    if (lane == 0) ops[n_ops] = 2;   // insert: a subject residue against a gap
                     ++n_ops, --t;
                     if (!(byte & 8u)) where = kCell;
                 }
@@ -752,9 +770,9 @@ __global__ void __launch_bounds__(32) traceback_walk_kernel(TracebackParams p) {
         }
     }
     if (lane == 0) {
-        p.result[3] = static_cast<int32_t>(n_ops);
-        p.result[4] = static_cast<int32_t>(q);   // query_begin (0-based, half-open)
-        p.result[5] = static_cast<int32_t>(t);   // subject_begin
+        result[3] = static_cast<int32_t>(n_ops);
+        result[4] = static_cast<int32_t>(q);   // query_begin (0-based, half-open)
+        result[5] = static_cast<int32_t>(t);   // subject_begin
     }
 }
 

@@ -173,6 +173,51 @@ void swb_mdb_destroy(swb_mdb* mdb) {
     delete mdb;
 }
 
+swb_status swb_mdb_align_hits(swb_mdb* mdb, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
+                              int32_t gap_open, int32_t gap_extend, const swb_hit* hits, uint32_t n_hits,
+                              uint64_t memory_cap, swb_alignment* out, uint8_t* ops, const uint64_t* ops_offset) {
+    if (!mdb) return fail(SWB_ERR_INVALID, "mdb is null");
+    if (n_hits && (!hits || !out || !ops_offset)) return fail(SWB_ERR_INVALID, "null argument");
+    const size_t G = mdb->shards.size();
+    if (G == 1)
+        return swb_db_align_hits(mdb->shards[0], query, query_len, matrix, gap_open, gap_extend, hits, n_hits, memory_cap,
+                                 out, ops, ops_offset);
+    // route every hit to the shard that holds it
+    for (size_t r = 0; r < G; ++r) {
+        swb_db* db = mdb->shards[r];
+        {
+            std::lock_guard<std::mutex> lock(db->mu);
+            if (db->slot_of.empty() && db->meta.n_total) {
+                db->slot_of.assign(db->meta.n_total, kNoSequence);
+                for (uint32_t slot = 0; slot < db->meta.slot_index.size(); ++slot)
+                    if (db->meta.slot_index[slot] != kNoSequence) db->slot_of[db->meta.slot_index[slot]] = slot;
+            }
+        }
+        std::vector<swb_hit> mine;
+        std::vector<uint32_t> where;
+        std::vector<uint64_t> offs(1, 0);
+        for (uint32_t i = 0; i < n_hits; ++i) {
+            if (hits[i].db_index < db->meta.n_total && db->slot_of[hits[i].db_index] != kNoSequence) {
+                mine.push_back(hits[i]);
+                where.push_back(i);
+                offs.push_back(offs.back() + (ops_offset[i + 1] - ops_offset[i]));
+            }
+        }
+        if (mine.empty()) continue;
+        std::vector<swb_alignment> part(mine.size());
+        std::vector<uint8_t> part_ops(std::max<uint64_t>(offs.back(), 1));
+        const swb_status st = swb_db_align_hits(db, query, query_len, matrix, gap_open, gap_extend, mine.data(),
+                                                static_cast<uint32_t>(mine.size()), memory_cap, part.data(),
+                                                ops ? part_ops.data() : nullptr, offs.data());
+        if (st != SWB_OK) return st;
+        for (size_t j = 0; j < mine.size(); ++j) {
+            out[where[j]] = part[j];
+            if (ops) std::memcpy(ops + ops_offset[where[j]], part_ops.data() + offs[j], std::min<uint64_t>(part[j].n_ops, offs[j + 1] - offs[j]));
+        }
+    }
+    return SWB_OK;
+}
+
 uint32_t swb_mdb_shard_count(const swb_mdb* mdb) { return mdb ? static_cast<uint32_t>(mdb->shards.size()) : 0; }
 
 swb_db* swb_mdb_shard(swb_mdb* mdb, uint32_t i) {

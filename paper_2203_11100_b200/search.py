@@ -164,6 +164,12 @@ class Database:
         _raise(self._lib, rc)
         return keys[:top_k], dptr.value, st.as_dict()
 
+    def align_hits(self, query, matrix, gaps: GapModel, index, score, subject_lengths, memory_cap: int = 256 << 20):
+        """Tracebacks of search hits straight from the resident database (swb_db_align_hits): a list of dicts
+        like align_traceback()'s, one per hit."""
+        return _align_hits(self._lib.swb_db_align_hits, self._lib, self._h, query, matrix, gaps, index, score,
+                           subject_lengths, memory_cap)
+
     def score_all(self, query, matrix, gaps: GapModel, out: np.ndarray | None = None):
         """Scores of all n_total sequences in db order (other shards' entries untouched)."""
         q, mat = _u8(query), _mat(matrix)
@@ -174,6 +180,30 @@ class Database:
                                      _ptr(out, _i32p), C.byref(st))
         _raise(self._lib, rc)
         return out[:self.n_total], st.as_dict()
+
+
+def _align_hits(fn, lib, handle, query, matrix, gaps, index, score, subject_lengths, memory_cap):
+    q, mat = _u8(query), _mat(matrix)
+    n = len(index)
+    hits = (_cabi.SwbHit * max(1, n))()
+    for i in range(n):
+        hits[i].db_index = int(index[i])
+        hits[i].score = int(score[i])
+    offsets = np.zeros(n + 1, dtype=np.uint64)
+    np.cumsum(np.asarray(subject_lengths, dtype=np.uint64) + np.uint64(len(q)), out=offsets[1:])
+    ops = np.zeros(max(1, int(offsets[-1])), dtype=np.uint8)
+    out = (_cabi.SwbAlignment * max(1, n))()
+    dummy = np.zeros(1, np.uint8)
+    rc = fn(handle, _ptr(q if len(q) else dummy, _u8p), len(q), _ptr(mat, _i32p), gaps.open, gaps.extend, hits, n,
+            memory_cap, out, _ptr(ops, _u8p), _ptr(offsets, _u64p))
+    _raise(lib, rc)
+    res = []
+    for i in range(n):
+        a = out[i]
+        res.append(dict(bounds=[int(a.query_begin), int(a.query_end), int(a.subject_begin), int(a.subject_end)],
+                        score=int(a.score), capped=bool(a.capped),
+                        ops=ops[int(offsets[i]):int(offsets[i]) + int(a.n_ops)].copy()))
+    return res
 
 
 def merge_keys(keys, top_k: int, device: int = 0):
@@ -320,3 +350,7 @@ class MultiGpuDatabase:
         idx = np.array([hits[i].db_index for i in range(n.value)], dtype=np.uint32)
         sc = np.array([hits[i].score for i in range(n.value)], dtype=np.int32)
         return idx, sc, st.as_dict()
+
+    def align_hits(self, query, matrix, gaps: GapModel, index, score, subject_lengths, memory_cap: int = 256 << 20):
+        return _align_hits(self._lib.swb_mdb_align_hits, self._lib, self._h, query, matrix, gaps, index, score,
+                           subject_lengths, memory_cap)

@@ -305,3 +305,27 @@ def test_packed_database_file_round_trip(tmp_path, b62):
         Database.load(bad)
     with pytest.raises(ValueError):
         Database.load(tmp_path / "missing.swb")
+
+
+def test_batched_traceback_of_search_hits(ref, b62):
+    """run_search's default (compute_alignments = true, scheduler.hpp:246-249): every hit's alignment equals the
+    reference's sw_align_traceback, for one shard and for several."""
+    qs, sdb = synth.config1()
+    g = GapModel(10, 2)
+    q = qs[0]
+    lens = sdb.lengths()
+    with Database(sdb.codes, sdb.offsets) as db:
+        idx, sc, _ = db.search(q, b62, g, 12)
+        got = db.align_hits(q, b62, g, idx, sc, lens[idx])
+        capped = db.align_hits(q, b62, g, idx[:3], sc[:3], lens[idx[:3]], memory_cap=1000)
+    assert all(c["capped"] and c["score"] == int(s) and len(c["ops"]) == 0 for c, s in zip(capped, sc[:3]))
+    for i, a in zip(idx, got):
+        exp = ref.traceback(q, sdb.seq(int(i)), b62, 10, 2)
+        assert a["score"] == exp["score"] and a["bounds"] == exp["bounds"] and a["ops"].tolist() == exp["ops"].tolist()
+    mdb = MultiGpuDatabase(sdb.codes, sdb.offsets, [0, 0, 0])
+    i2, s2, _ = mdb.search(q, b62, g, 12)
+    got2 = mdb.align_hits(q, b62, g, i2, s2, lens[i2])
+    mdb.close()
+    assert (i2 == idx).all()
+    for a, b in zip(got, got2):
+        assert a["bounds"] == b["bounds"] and a["ops"].tolist() == b["ops"].tolist() and a["score"] == b["score"]
