@@ -843,18 +843,4 @@ __global__ void bitonic_step_kernel(uint64_t* keys, uint64_t n_pow2, uint64_t si
     }
 }
 
-__global__ void keys_to_hits_kernel(const uint64_t* keys, uint32_t k, uint32_t* out_index, int32_t* out_score,
-                                    uint32_t* out_count) {
-    uint32_t cnt = 0;
-    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
-        const uint64_t key = keys[i];
-        if (key) {
-            out_index[i] = 0xFFFFFFFFu - static_cast<uint32_t>(key & 0xFFFFFFFFu);
-            out_score[i] = static_cast<int32_t>(key >> 32);
-            ++cnt;
-        }
-    }
-    if (cnt) atomicAdd(out_count, cnt);
-}
-
 }  // namespace swb
