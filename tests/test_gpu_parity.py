@@ -329,3 +329,50 @@ def test_batched_traceback_of_search_hits(ref, b62):
     assert (i2 == idx).all()
     for a, b in zip(got, got2):
         assert a["bounds"] == b["bounds"] and a["ops"].tolist() == b["ops"].tolist() and a["score"] == b["score"]
+
+
+def test_kernel_equivalence_property(port, b62):
+    """>= 1000 random pairs, lengths 1-500: scalar == batch (every lane width) == wavefront,
+    exact integers.  Here: oracle scalar vs the packed DPX kernel (score_batch) vs the intra-task kernel."""
+    rng = np.random.default_rng(41)
+    checked = 0
+    for lane_width in (1, 4, 8, 16, 32, 64):
+        for _ in range(4):
+            q = synth.random_residues(rng, int(rng.integers(1, 501)))
+            subs = [synth.random_residues(rng, int(rng.integers(1, 501))) for _ in range(lane_width)]
+            if rng.random() < 0.5:
+                subs[0] = synth.mutate(rng, q, 0.2, 2)
+            go = int(rng.integers(0, 14)); ge = int(rng.integers(0, go + 1))
+            got = score_batch(q, subs, lane_width, b62, GapModel(go, ge))
+            exp = [port.score_scalar(q, s, b62, go, ge) for s in subs]
+            assert got.tolist() == exp
+            checked += lane_width
+    # one big batch brings the total past 1000 pairs
+    q = synth.random_residues(rng, 333)
+    subs = [synth.random_residues(rng, int(rng.integers(1, 501))) for _ in range(600)]
+    assert score_batch(q, subs, 600, b62, GapModel(10, 2)).tolist() == [port.score_scalar(q, s, b62, 10, 2) for s in subs]
+    checked += 600
+    assert checked >= 1000
+    for _ in range(12):
+        q = synth.random_residues(rng, int(rng.integers(1, 501)))
+        s = synth.random_residues(rng, int(rng.integers(1, 501)))
+        assert score_wavefront(q, s, b62, GapModel(10, 2), int(rng.choice([1, 4, 64, len(q)]))) == port.score_scalar(q, s, b62, 10, 2)
+
+
+def test_config5_shape_blosum50_with_overflow(port):
+    """BASELINE config 5 at reduced size: BLOSUM50, gap 12/2, a query long enough that its planted copies leave
+    the int16 range and must come back exact from the int32 re-run."""
+    b50 = synth.blosum50()
+    queries = synth.make_queries([300, 8000], seed=55)
+    sdb = synth.make_database(1500, target_residues=450_000, max_len=9000, queries=queries, seed=55)
+    g = GapModel(12, 2)
+    with Database(sdb.codes, sdb.offsets) as db:
+        for qi, q in enumerate(queries):
+            got, st = db.score_all(q, b50, g)
+            idx, sc, _ = db.search(q, b50, g, 10)
+            assert idx[0] == sdb.planted[qi][0]
+            sample = np.unique(np.concatenate([np.array(sdb.planted[qi]), np.arange(0, sdb.n, 97)]))
+            exp = port.score_all(q, po.FlatDb.from_list([sdb.seq(int(i)) for i in sample]), b50, 12, 2)
+            assert (got[sample] == exp).all()
+            if qi == 1:
+                assert st["rescored_i32"] >= 1 and sc[0] > 32767
