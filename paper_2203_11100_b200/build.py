@@ -15,7 +15,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libswb200.so"
 SOURCES = ["cabi.cu", "pack.cpp"]
-HEADERS = ["kernels.cuh", "pipe_rates.cuh", "pack.hpp", "multi.inl"]
+HEADERS = ["kernels.cuh", "pipe_rates.cuh", "pack.hpp", "plan.inl", "handle.inl", "scan.inl", "persist.inl", "pairs.inl", "pipe.inl",
+           "multi.inl"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,339 @@
+// scan.inl -- one search on one shard: upload, profile, unit table, packed scan, int32 re-run, top-k select.
+// Included by cabi.cu inside its anonymous namespace.
+
+template <int T, typename PT>
+void launch_intra(const IntraParams& ip, uint32_t ctas, uint32_t warps, cudaStream_t s) {
+    intra_s32_kernel<T, PT><<<ctas, warps * 32, 0, s>>>(ip);
+}
+
+template <typename PT>
+void launch_intra_t(uint32_t t, const IntraParams& ip, uint32_t ctas, uint32_t warps, cudaStream_t s) {
+    switch (t) {
+        case 4: launch_intra<4, PT>(ip, ctas, warps, s); break;
+        case 5: launch_intra<5, PT>(ip, ctas, warps, s); break;
+        case 6: launch_intra<6, PT>(ip, ctas, warps, s); break;
+        case 7: launch_intra<7, PT>(ip, ctas, warps, s); break;
+        default: launch_intra<8, PT>(ip, ctas, warps, s); break;
+    }
+}
+
+// Launch the int32 intra-task kernel over `list` (nullptr = every slot).
+swb_status run_intra(swb_db* db, const QueryPlan& pl, const uint32_t* list, cudaStream_t s) {
+    swb_status st;
+    if (!db->intra_ctas) {
+        // per-CTA border rows are only touched when the query needs more than one pass, but the
+        // allocation is sized once for the worst case
+        const uint64_t rows = std::max<uint32_t>(db->max_rows, 1);
+        uint64_t ctas = (512ull << 20) / (rows * 16);
+        ctas = std::min<uint64_t>(static_cast<uint64_t>(db->sm_count) * 8, std::max<uint64_t>(8, ctas));
+        ctas = std::min<uint64_t>(ctas, std::max<uint32_t>(db->n_slots, 1));
+        if ((st = dev_alloc(&db->d_iborder0, rows * ctas, &db->device_bytes)) != SWB_OK) return st;
+        if ((st = dev_alloc(&db->d_iborder1, rows * ctas, &db->device_bytes)) != SWB_OK) return st;
+        db->intra_ctas = static_cast<uint32_t>(ctas);
+    }
+    IntraParams ip{};
+    ip.codes = db->d_codes;
+    ip.groups = db->d_groups;
+    ip.slot_len = db->d_slot_len;
+    ip.list = list;
+    ip.list_count = db->d_counters + 1;
+    ip.n_slots = db->n_slots;
+    ip.profi = pl.wide ? static_cast<const void*>(db->d_prof32i) : static_cast<const void*>(db->d_prof8i);
+    ip.n_lane_tiles = pl.n_lane_tiles;
+    ip.n_passes = pl.intra_passes;
+    ip.border0 = db->d_iborder0;
+    ip.border1 = db->d_iborder1;
+    ip.border_rows = std::max<uint32_t>(db->max_rows, 1);
+    ip.slot_scores = db->d_slot_scores;
+    ip.open = pl.open;
+    ip.ext = pl.ext;
+    if (pl.wide) launch_intra_t<int32_t>(pl.intra_t, ip, db->intra_ctas, pl.intra_w, s);
+    else launch_intra_t<int8_t>(pl.intra_t, ip, db->intra_ctas, pl.intra_w, s);
+    ++db->launches;
+    return SWB_OK;
+}
+
+// Scores every local sequence; results land in d_slot_scores.  Asynchronous on db->stream.
+swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_t* matrix, int32_t open,
+                      int32_t ext) {
+    cudaStream_t s = db->stream;
+    const QueryPlan pl = make_plan(db, m, matrix, open, ext);
+    db->launches = 0;
+    db->last_units = 0;
+    db->last_tile = pl.tile;
+    SWB_CUDA(cudaEventRecord(db->ev[EV_START], s));
+    SWB_CUDA(cudaMemsetAsync(db->d_slot_scores, 0, std::max<size_t>(db->n_slots, 1) * sizeof(int32_t), s));
+    SWB_CUDA(cudaMemsetAsync(db->d_counters, 0, 4 * sizeof(uint32_t), s));
+
+    if (m == 0 || db->meta.n_local == 0) {
+        // empty query: every score is 0 (align.hpp:45,100,172)
+        for (int e = EV_UP; e <= EV_RESCORE; ++e) SWB_CUDA(cudaEventRecord(db->ev[e], s));
+        return SWB_OK;
+    }
+
+    const uint32_t n_groups = static_cast<uint32_t>(db->meta.groups.size());
+    const bool packed = pl.main != kMainNone;
+
+    // ---- stage matrix + query (+ the unit table of the wavefront kernel) and upload -----------------
+    const size_t off_query = 576 * sizeof(int32_t);
+    const size_t off_units = (off_query + m + 15) & ~size_t(15);
+    const size_t off_vsoff = off_units + (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t);
+    const size_t off_modes = off_vsoff + static_cast<size_t>(n_groups) * sizeof(uint32_t);
+    const size_t stage_bytes = off_modes + n_groups;
+    swb_status st = ensure_stage(db, stage_bytes);
+    if (st != SWB_OK) return st;
+    if (m > db->query_cap) {
+        if (db->d_query) cudaFree(db->d_query);
+        db->d_query = nullptr;
+        st = dev_alloc(&db->d_query, static_cast<size_t>(m) * 2, &db->device_bytes);
+        if (st != SWB_OK) return st;
+        db->query_cap = m * 2;
+    }
+    std::memcpy(db->h_stage, matrix, off_query);
+    std::memcpy(db->h_stage + off_query, query, m);
+    const uint32_t n_tiles = (m + pl.tile - 1) / pl.tile;
+    const uint32_t n_tiles_narrow = (m + kNarrowTile - 1) / kNarrowTile;
+    uint32_t n_units = 0;
+    bool any_narrow = false, any_rowblock = false;
+    uint64_t vstate_slots = 0;
+    if (packed) {
+        // Unit policy (see kernels.cuh, GroupMode).  Work is counted in row-tiles (one row of one T-column tile);
+        // `fair` is one warp's share of the whole search.
+        //   single    the default: one warp scores the group's 64 sequences end to end;
+        //   split     a group whose sweep exceeds `budget` is cut so that no unit dominates the makespan and there
+        //             are enough units for every warp, either
+        //               by tile   (wavefront of warps, each 2 chunks behind its left neighbour:
+        //                          efficiency rows / (rows + 16 (tiles - 1))), or
+        //               by rows   (blocks of rows, each one tile behind the block above:
+        //                          efficiency tiles / (tiles + blocks - 1)),
+        //             whichever wastes less;
+        //   narrow    even a tile-split group's per-tile chain (rows x T columns, strictly sequential in one thread,
+        //             ~900 clk per row when the SM empties out, against ~1600 clk per row-tile of saturated
+        //             throughput) would take more than about half the whole search: 8-column tiles cut that chain
+        //             four-fold.
+        // Row blocks and narrow tiles exist in the s16 kernel only.
+        uint32_t* us = reinterpret_cast<uint32_t*>(db->h_stage + off_units);
+        uint32_t* vso = reinterpret_cast<uint32_t*>(db->h_stage + off_vsoff);
+        uint8_t* modes = db->h_stage + off_modes;
+        const uint64_t total_row_tiles = db->meta.padded_rows * n_tiles;
+        const uint64_t warps = static_cast<uint64_t>(db->sm_count) * (pl.threads / 32);
+        const uint64_t fair = total_row_tiles / warps;
+        // With plenty of groups per warp (a whole Swiss-Prot on one GPU: 3.7) only units larger than about
+        // three quarters of a warp's fair share need cutting -- LPT order fills the rest; a small shard with fewer
+        // groups than warps has to be cut finer to give every warp several units.
+        const double auto_fraction = std::min(0.75, std::max(0.08, static_cast<double>(n_groups) / (4.0 * static_cast<double>(warps))));
+        const double fraction = unit_budget_fraction() > 0.0 ? unit_budget_fraction() : auto_fraction;
+        const uint64_t budget = std::max<uint64_t>(2048, static_cast<uint64_t>(fraction * static_cast<double>(fair)));
+        const uint64_t narrow_rows = std::max<uint64_t>(2048, static_cast<uint64_t>(narrow_chain_fraction() * fair));
+        const bool s16 = pl.main == kMainS16;
+        // groups are sorted longest first: narrow tiles are needed iff the first group needs them.  The kernel
+        // variant that carries both extra paths spills registers in the common 32-column sweep, so a search that
+        // needs narrow tiles cuts its other large groups by tile rather than by rows.
+        const bool narrow_needed = s16 && n_groups && n_tiles_narrow > 1 &&
+                                   static_cast<uint64_t>(db->meta.groups[0].n_chunks) * kRowsPerChunk > narrow_rows;
+        const bool row_blocks_ok = s16 && row_blocks_enabled() && !narrow_needed;
+        for (uint32_t g = 0; g < n_groups; ++g) {
+            us[g] = n_units;
+            vso[g] = 0;
+            const uint64_t chunks = db->meta.groups[g].n_chunks;
+            const uint64_t rows = chunks * kRowsPerChunk;
+            const uint64_t work = rows * n_tiles;
+            uint8_t mode = kGroupSingle;
+            uint32_t units = 1;
+            if (work > budget && n_tiles > 1) {
+                mode = kGroupSplit;
+                units = n_tiles;
+                const double eff_tiles = static_cast<double>(rows) / static_cast<double>(rows + 16 * (n_tiles - 1));
+                // row blocks of at least 2 chunks, about `budget` row-tiles each
+                const uint64_t blocks = std::min<uint64_t>((work + budget - 1) / budget, std::max<uint64_t>(chunks / 2, 1));
+                const double eff_rows = static_cast<double>(n_tiles) / static_cast<double>(n_tiles + blocks - 1);
+                if (row_blocks_ok && blocks >= 2 && eff_rows > eff_tiles) {
+                    mode = kGroupRowBlock;
+                    units = static_cast<uint32_t>(blocks);
+                    vso[g] = static_cast<uint32_t>(vstate_slots);
+                    vstate_slots += n_tiles;
+                    any_rowblock = true;
+                }
+            }
+            if (s16 && rows > narrow_rows && n_tiles_narrow > 1) {
+                if (mode == kGroupRowBlock) vstate_slots -= n_tiles;
+                mode = kGroupNarrow;
+                units = n_tiles_narrow;
+            }
+            modes[g] = mode;
+            any_narrow |= mode == kGroupNarrow;
+            n_units += units;
+        }
+        us[n_groups] = n_units;
+        SWB_CUDA(cudaMemcpyAsync(db->d_unit_start, us, (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, s));
+        SWB_CUDA(cudaMemcpyAsync(db->d_group_mode, modes, std::max<size_t>(n_groups, 1), cudaMemcpyHostToDevice, s));
+        SWB_CUDA(cudaMemcpyAsync(db->d_vstate_off, vso, std::max<size_t>(n_groups, 1) * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, s));
+        if (any_rowblock) {
+            const size_t need = static_cast<size_t>(vstate_slots) * (kVStateWords / 4) * 32;
+            if ((st = ensure_dev(&db->d_vstate, &db->vstate_cap, need, &db->device_bytes)) != SWB_OK) return st;
+        }
+        if ((st = ensure_dev(&db->d_progress, &db->progress_cap, n_units, &db->device_bytes)) != SWB_OK) return st;
+        SWB_CUDA(cudaMemsetAsync(db->d_progress, 0, static_cast<size_t>(n_units) * sizeof(uint32_t), s));
+        db->last_units = n_units;
+    }
+    SWB_CUDA(cudaMemcpyAsync(db->d_matrix, db->h_stage, off_query, cudaMemcpyHostToDevice, s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_query, db->h_stage + off_query, m, cudaMemcpyHostToDevice, s));
+
+    const size_t prof_elems = static_cast<size_t>(kProfRows) * pl.pstride;
+    const size_t profi_elems = static_cast<size_t>(kProfRows) * pl.n_lane_tiles * 8;
+    ProfileParams pp{};
+    pp.query = db->d_query;
+    pp.matrix = db->d_matrix;
+    pp.m = m;
+    pp.shift_main = open;
+    pp.shift_intra = open;
+    pp.pstride = pl.pstride;
+    pp.intra_t = pl.intra_t;
+    pp.n_lane_tiles = pl.n_lane_tiles;
+    if (packed) {
+        if ((st = ensure_dev(&db->d_prof8, &db->prof8_cap, prof_elems, &db->device_bytes)) != SWB_OK) return st;
+        pp.prof8 = db->d_prof8;
+    }
+    if (!pl.wide) {
+        if ((st = ensure_dev(&db->d_prof8i, &db->prof8i_cap, profi_elems, &db->device_bytes)) != SWB_OK) return st;
+        pp.prof8i = db->d_prof8i;
+    } else {
+        if ((st = ensure_dev(&db->d_prof32i, &db->prof32i_cap, profi_elems, &db->device_bytes)) != SWB_OK) return st;
+        pp.prof32i = db->d_prof32i;
+    }
+    build_profile_kernel<<<64, 256, 0, s>>>(pp);
+    ++db->launches;
+    SWB_CUDA(cudaEventRecord(db->ev[EV_UP], s));
+
+    // ---- the scan ------------------------------------------------------------------------------------
+    if (packed) {
+        WaveParams wp{};
+        wp.codes = reinterpret_cast<const uint4*>(db->d_codes);
+        wp.groups = db->d_groups;
+        wp.n_groups = n_groups;
+        wp.unit_start = db->d_unit_start;
+        wp.group_mode = db->d_group_mode;
+        wp.vstate_off = db->d_vstate_off;
+        wp.vstate = db->d_vstate;
+        wp.n_units = n_units;
+        wp.n_tiles_narrow = n_tiles_narrow;
+        wp.prof8 = db->d_prof8;
+        wp.pstride = pl.pstride;
+        wp.n_tiles = n_tiles;
+        wp.border0 = db->d_border0;
+        wp.border1 = db->d_border1;
+        wp.slot_scores = db->d_slot_scores;
+        wp.progress = db->d_progress;
+        wp.ticket = db->d_counters;
+        wp.neg_open2 = pack16(-open);
+        wp.neg_ext2 = pack16(-ext);
+        const size_t smem = prof_elems;
+        const uint32_t warps_per_cta = pl.threads / 32;
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(db->sm_count, (n_units + warps_per_cta - 1) / warps_per_cta));
+        const bool in_smem = smem <= db->smem_optin;
+        {
+#define SWB_LAUNCH_S16(NARROW, RB)                                                                                 \
+    {                                                                                                              \
+        if (in_smem) {                                                                                             \
+            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB>,       \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,                             \
+                                          static_cast<int>(db->smem_optin)));                                      \
+            wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB><<<grid, kInterThreads, smem, s>>>(wp); \
+        } else {                                                                                                   \
+            wavefront_s16_kernel<false, kInterTile, kInterThreads, NARROW, RB><<<grid, kInterThreads, 0, s>>>(wp); \
+        }                                                                                                          \
+    }
+            // the narrow-tile and row-block paths are only compiled into the variants that need them, so that the
+            // plain 32-column sweep keeps its register allocation
+            if (any_narrow && any_rowblock) SWB_LAUNCH_S16(true, true)
+            else if (any_narrow) SWB_LAUNCH_S16(true, false)
+            else if (any_rowblock) SWB_LAUNCH_S16(false, true)
+            else SWB_LAUNCH_S16(false, false)
+#undef SWB_LAUNCH_S16
+        }
+        ++db->launches;
+    }
+    SWB_CUDA(cudaEventRecord(db->ev[EV_SCAN], s));
+
+    // ---- int32: re-run of lanes above the trust limit, or everything when the packed path is out ----
+    if (!packed) {
+        if ((st = run_intra(db, pl, nullptr, s)) != SWB_OK) return st;
+    } else if (pl.may_overflow) {
+        collect_flagged_kernel<<<std::max(1u, std::min(1024u, (db->n_slots + 255) / 256)), 256, 0, s>>>(
+            db->d_slot_scores, db->n_slots, pl.limit, db->d_flag_list, db->d_counters + 1);
+        ++db->launches;
+        if ((st = run_intra(db, pl, db->d_flag_list, s)) != SWB_OK) return st;
+    }
+    SWB_CUDA(cudaEventRecord(db->ev[EV_RESCORE], s));
+    SWB_CUDA(cudaGetLastError());
+    return SWB_OK;
+}
+
+// Descending top-k of n device keys; result pointer (k entries, zero padded) in *out.
+swb_status select_topk(swb_db* db, const uint64_t* d_in, uint64_t n, uint32_t k, const uint64_t** out) {
+    cudaStream_t s = db->stream;
+    swb_status st;
+    if (k <= kSelectMaxK) {
+        const uint64_t first_blocks = std::max<uint64_t>(1, (n + kSelectSlice - 1) / kSelectSlice);
+        const size_t need = static_cast<size_t>(first_blocks) * k;
+        if (need > db->sel_cap) {
+            for (auto& p : db->d_sel) {
+                if (p) cudaFree(p);
+                p = nullptr;
+            }
+            for (auto& p : db->d_sel)
+                if ((st = dev_alloc(&p, need, &db->device_bytes)) != SWB_OK) return st;
+            db->sel_cap = need;
+        }
+        const uint64_t* in = d_in;
+        int which = 0;
+        for (;;) {
+            const uint64_t blocks = std::max<uint64_t>(1, (n + kSelectSlice - 1) / kSelectSlice);
+            select_topk_kernel<<<static_cast<unsigned>(blocks), kSelectThreads, 0, s>>>(in, n, k, db->d_sel[which]);
+            ++db->launches;
+            in = db->d_sel[which];
+            n = blocks * k;
+            which ^= 1;
+            if (blocks == 1) break;
+        }
+        *out = in;
+        return SWB_OK;
+    }
+    // k > 1024: full bitonic sort of the zero-padded key array
+    uint64_t pow2 = 2;
+    while (pow2 < n) pow2 <<= 1;
+    if (pow2 > db->sort_cap) {
+        if (db->d_sort) cudaFree(db->d_sort);
+        db->d_sort = nullptr;
+        if ((st = dev_alloc(&db->d_sort, pow2, &db->device_bytes)) != SWB_OK) return st;
+        db->sort_cap = pow2;
+    }
+    SWB_CUDA(cudaMemsetAsync(db->d_sort, 0, pow2 * sizeof(uint64_t), s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_sort, d_in, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(4096, std::max<uint64_t>(1, pow2 / 2 / 256)));
+    for (uint64_t size = 2; size <= pow2; size <<= 1)
+        for (uint64_t stride = size >> 1; stride > 0; stride >>= 1) {
+            bitonic_step_kernel<<<grid, 256, 0, s>>>(db->d_sort, pow2, size, stride);
+            ++db->launches;
+        }
+    *out = db->d_sort;
+    return SWB_OK;
+}
+
+swb_status search_keys_locked(swb_db* db, const uint8_t* query, uint32_t m, const int32_t* matrix,
+                              int32_t open, int32_t ext, uint32_t top_k, const uint64_t** d_out) {
+    swb_status st = score_core(db, query, m, matrix, open, ext);
+    if (st != SWB_OK) return st;
+    cudaStream_t s = db->stream;
+    if (db->n_slots) {
+        build_keys_kernel<<<std::max(1u, std::min(1024u, (db->n_slots + 255) / 256)), 256, 0, s>>>(
+            db->d_slot_scores, db->d_slot_index, db->n_slots, db->d_keys);
+        ++db->launches;
+    }
+    st = select_topk(db, db->d_keys, db->n_slots, top_k, d_out);
+    if (st != SWB_OK) return st;
+    SWB_CUDA(cudaEventRecord(db->ev[EV_TOPK], s));
+    return SWB_OK;
+}
