@@ -138,6 +138,16 @@ swb_status swb_search(swb_db* db, const uint8_t* query, uint32_t query_len, cons
                       int32_t gap_open, int32_t gap_extend, uint32_t top_k, swb_hit* hits,
                       uint32_t* n_hits, swb_stats* stats);
 
+/* Several queries against the shard, pipelined: every query's upload, scan and select are
+ * issued back to back on the handle's stream and the call synchronises once, so host preparation and launch
+ * latency of query q+1 overlap the scan of query q.  Results are identical to n_queries calls of swb_search.
+ *   hits          n_queries x top_k entries; query q's hits start at hits[q * top_k]
+ *   n_hits        n_queries counts
+ *   ms_per_query  optional: device time of each query (CUDA events) */
+swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint32_t* query_lens,
+                           uint32_t n_queries, const int32_t* matrix, int32_t gap_open, int32_t gap_extend,
+                           uint32_t top_k, swb_hit* hits, uint32_t* n_hits, float* ms_per_query);
+
 /* As swb_search, but returns the shard's top_k as packed 64-bit keys
  *   key = (uint64(score) << 32) | (0xFFFFFFFF - db_index)
  * in descending key order, padded with 0 up to top_k entries (0 is never a valid key).  A plain

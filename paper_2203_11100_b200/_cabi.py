@@ -82,6 +82,8 @@ SIGNATURES = {
     "swb_db_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "swb_search": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32,
                              C.POINTER(SwbHit), u32p, C.POINTER(SwbStats)]),
+    "swb_search_many": (C.c_int, [C.c_void_p, C.POINTER(u8p), u32p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32,
+                                  C.POINTER(SwbHit), u32p, C.POINTER(C.c_float)]),
     "swb_search_keys": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32, u64p,
                                   C.POINTER(C.c_void_p), C.POINTER(SwbStats)]),
     "swb_merge_keys": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.c_int32, C.c_uint32, C.POINTER(SwbHit), u32p]),

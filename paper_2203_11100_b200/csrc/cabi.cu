@@ -133,6 +133,8 @@ struct swb_db {
 
     uint8_t* h_stage = nullptr;   // pinned: matrix + query + unit table up, keys down
     size_t stage_cap = 0;
+    size_t stage_base = 0;        // offset of the current query's staging area (swb_search_many pipelines several)
+    std::vector<cudaEvent_t> many_events;   // per-query start/end events of swb_search_many
     uint32_t* h_counters = nullptr;   // pinned copy of d_counters
     cudaEvent_t ev[EV_COUNT] = {};
     uint32_t launches = 0;
@@ -263,6 +265,7 @@ void swb_db_destroy(swb_db* db) {
         if (db->h_counters) cudaFreeHost(db->h_counters);
         for (auto& ev : db->ev)
             if (ev) cudaEventDestroy(ev);
+        for (auto& ev : db->many_events) cudaEventDestroy(ev);
         if (db->own_stream) cudaStreamDestroy(db->own_stream);
     }
     delete db;
@@ -326,6 +329,69 @@ swb_status swb_search_keys(swb_db* db, const uint8_t* query, uint32_t query_len,
     }
     if (device_keys) *device_keys = (k_eff == top_k) ? const_cast<uint64_t*>(d_top) : nullptr;
     fill_stats(db, query_len, stats);
+    return SWB_OK;
+}
+
+swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint32_t* query_lens, uint32_t n_queries,
+                           const int32_t* matrix, int32_t gap_open, int32_t gap_extend, uint32_t top_k, swb_hit* hits,
+                           uint32_t* n_hits, float* ms_per_query) {
+    if (!db) return fail(SWB_ERR_INVALID, "db is null");
+    if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
+    if (n_queries && (!queries || !query_lens || !hits || !n_hits)) return fail(SWB_ERR_INVALID, "null argument");
+    swb_status st;
+    for (uint32_t q = 0; q < n_queries; ++q)
+        if ((st = check_scoring_args(queries[q], query_lens[q], matrix, gap_open, gap_extend)) != SWB_OK) return st;
+    if (n_queries == 0) return SWB_OK;
+    std::lock_guard<std::mutex> lock(db->mu);
+    DeviceGuard guard(db->device);
+    cudaStream_t s = db->stream;
+    const uint64_t n_keys = db->meta.n_local;
+    const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint64_t>(n_keys, 1)));
+    const size_t n_groups = db->meta.groups.size();
+
+    // one staging area per query (inputs up, keys + counters down), sized up front: the pinned buffer must not
+    // move while copies are in flight
+    std::vector<size_t> in_off(n_queries), out_off(n_queries);
+    size_t total = 0;
+    for (uint32_t q = 0; q < n_queries; ++q) {
+        in_off[q] = total;
+        total += (576 * sizeof(int32_t) + query_lens[q] + 64 + (n_groups + 1) * 9 + 255) & ~size_t(255);
+        out_off[q] = total;
+        total += (static_cast<size_t>(k_eff) * sizeof(uint64_t) + 16 + 255) & ~size_t(255);
+    }
+    if ((st = ensure_stage(db, total)) != SWB_OK) return st;
+    while (db->many_events.size() < 2 * static_cast<size_t>(n_queries)) {
+        cudaEvent_t ev;
+        SWB_CUDA(cudaEventCreate(&ev));
+        db->many_events.push_back(ev);
+    }
+    // queries are issued back to back on the stream: the host prepares query q+1 (unit table, launches) while the
+    // GPU still scans query q, and nothing synchronises until the last one is in flight
+    for (uint32_t q = 0; q < n_queries && st == SWB_OK; ++q) {
+        db->stage_base = in_off[q];
+        cudaEventRecord(db->many_events[2 * q], s);
+        const uint64_t* d_top = nullptr;
+        st = search_keys_locked(db, queries[q], query_lens[q], matrix, gap_open, gap_extend, k_eff, &d_top);
+        if (st != SWB_OK) break;
+        if (cudaMemcpyAsync(db->h_stage + out_off[q], d_top, static_cast<size_t>(k_eff) * sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            st = fail(SWB_ERR_CUDA, "cudaMemcpyAsync failed");
+        cudaEventRecord(db->many_events[2 * q + 1], s);
+    }
+    db->stage_base = 0;
+    const cudaError_t sync = cudaStreamSynchronize(s);
+    if (st != SWB_OK) return st;
+    if (sync != cudaSuccess) return fail(SWB_ERR_CUDA, cudaGetErrorString(sync));
+    for (uint32_t q = 0; q < n_queries; ++q) {
+        const uint64_t* keys = reinterpret_cast<const uint64_t*>(db->h_stage + out_off[q]);
+        uint32_t cnt = 0;
+        for (uint32_t i = 0; i < k_eff && keys[i]; ++i, ++cnt) {
+            hits[static_cast<size_t>(q) * top_k + cnt].db_index = 0xFFFFFFFFu - static_cast<uint32_t>(keys[i] & 0xFFFFFFFFu);
+            hits[static_cast<size_t>(q) * top_k + cnt].score = static_cast<int32_t>(keys[i] >> 32);
+        }
+        n_hits[q] = cnt;
+        if (ms_per_query) cudaEventElapsedTime(&ms_per_query[q], db->many_events[2 * q], db->many_events[2 * q + 1]);
+    }
     return SWB_OK;
 }
 

@@ -80,8 +80,9 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     const size_t off_vsoff = off_units + (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t);
     const size_t off_modes = off_vsoff + static_cast<size_t>(n_groups) * sizeof(uint32_t);
     const size_t stage_bytes = off_modes + n_groups;
-    swb_status st = ensure_stage(db, stage_bytes);
+    swb_status st = ensure_stage(db, db->stage_base + stage_bytes);   // a no-op inside swb_search_many (pre-sized)
     if (st != SWB_OK) return st;
+    uint8_t* const stage = db->h_stage + db->stage_base;
     if (m > db->query_cap) {
         if (db->d_query) cudaFree(db->d_query);
         db->d_query = nullptr;
@@ -89,8 +90,8 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         if (st != SWB_OK) return st;
         db->query_cap = m * 2;
     }
-    std::memcpy(db->h_stage, matrix, off_query);
-    std::memcpy(db->h_stage + off_query, query, m);
+    std::memcpy(stage, matrix, off_query);
+    std::memcpy(stage + off_query, query, m);
     const uint32_t n_tiles = (m + pl.tile - 1) / pl.tile;
     const uint32_t n_tiles_narrow = (m + kNarrowTile - 1) / kNarrowTile;
     uint32_t n_units = 0;
@@ -112,9 +113,9 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         //             throughput) would take more than about half the whole search: 8-column tiles cut that chain
         //             four-fold.
         // Row blocks and narrow tiles exist in the s16 kernel only.
-        uint32_t* us = reinterpret_cast<uint32_t*>(db->h_stage + off_units);
-        uint32_t* vso = reinterpret_cast<uint32_t*>(db->h_stage + off_vsoff);
-        uint8_t* modes = db->h_stage + off_modes;
+        uint32_t* us = reinterpret_cast<uint32_t*>(stage + off_units);
+        uint32_t* vso = reinterpret_cast<uint32_t*>(stage + off_vsoff);
+        uint8_t* modes = stage + off_modes;
         const uint64_t total_row_tiles = db->meta.padded_rows * n_tiles;
         const uint64_t warps = static_cast<uint64_t>(db->sm_count) * (pl.threads / 32);
         const uint64_t fair = total_row_tiles / warps;
@@ -178,8 +179,8 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         SWB_CUDA(cudaMemsetAsync(db->d_progress, 0, static_cast<size_t>(n_units) * sizeof(uint32_t), s));
         db->last_units = n_units;
     }
-    SWB_CUDA(cudaMemcpyAsync(db->d_matrix, db->h_stage, off_query, cudaMemcpyHostToDevice, s));
-    SWB_CUDA(cudaMemcpyAsync(db->d_query, db->h_stage + off_query, m, cudaMemcpyHostToDevice, s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_matrix, stage, off_query, cudaMemcpyHostToDevice, s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_query, stage + off_query, m, cudaMemcpyHostToDevice, s));
 
     const size_t prof_elems = static_cast<size_t>(kProfRows) * pl.pstride;
     const size_t profi_elems = static_cast<size_t>(kProfRows) * pl.n_lane_tiles * 8;

@@ -376,3 +376,20 @@ def test_config5_shape_blosum50_with_overflow(port):
             assert (got[sample] == exp).all()
             if qi == 1:
                 assert st["rescored_i32"] >= 1 and sc[0] > 32767
+
+
+def test_pipelined_multi_query_equals_one_by_one(b62):
+    """swb_search_many: same ranked lists as separate searches, for queries of very different lengths (different
+    kernel variants, re-run on/off) issued back to back."""
+    rng = np.random.default_rng(61)
+    qs, sdb = synth.config1()
+    queries = [qs[0], synth.random_residues(rng, 7), sdb.seq(sdb.planted[0][1]), synth.random_residues(rng, 1500),
+               enc(""), synth.random_residues(rng, 3300)]
+    g = GapModel(10, 2)
+    with Database(sdb.codes, sdb.offsets) as db:
+        single = [db.search(q, b62, g, 15)[:2] for q in queries]
+        many, ms = db.search_many(queries, b62, g, 15)
+        again, _ = db.search_many(queries[::-1], b62, g, 15)
+    for (i1, s1), (i2, s2), (i3, s3) in zip(single, many, again[::-1]):
+        assert (i1 == i2).all() and (s1 == s2).all() and (i1 == i3).all() and (s1 == s3).all()
+    assert (ms > 0).all()
