@@ -128,11 +128,24 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         const uint64_t narrow_rows = std::max<uint64_t>(2048, static_cast<uint64_t>(narrow_chain_fraction() * fair));
         const bool s16 = pl.main == kMainS16;
         // groups are sorted longest first: narrow tiles are needed iff the first group needs them.  The kernel
-        // variant that carries both extra paths spills registers in the common 32-column sweep, so a search that
-        // needs narrow tiles cuts its other large groups by tile rather than by rows.
+        // variant that carries both extra paths spills registers in the common 32-column sweep (about 12 % slower),
+        // so a search that needs narrow tiles cuts its other large groups by rows only if cutting them by tile
+        // instead would waste more than that (small shards, long queries).
         const bool narrow_needed = s16 && n_groups && n_tiles_narrow > 1 &&
                                    static_cast<uint64_t>(db->meta.groups[0].n_chunks) * kRowsPerChunk > narrow_rows;
-        const bool row_blocks_ok = s16 && row_blocks_enabled() && !narrow_needed;
+        bool row_blocks_ok = s16 && row_blocks_enabled();
+        if (row_blocks_ok && narrow_needed) {
+            double wasted = 0.0;   // extra warp time of tile-splitting where row blocks would have been chosen
+            for (uint32_t g = 0; g < n_groups; ++g) {
+                const uint64_t chunks = db->meta.groups[g].n_chunks, rows = chunks * kRowsPerChunk, work = rows * n_tiles;
+                if (work <= budget || n_tiles < 2 || rows > narrow_rows) continue;
+                const double eff_tiles = static_cast<double>(rows) / static_cast<double>(rows + 16 * (n_tiles - 1));
+                const uint64_t blocks = std::min<uint64_t>((work + budget - 1) / budget, std::max<uint64_t>(chunks / 2, 1));
+                const double eff_rows = static_cast<double>(n_tiles) / static_cast<double>(n_tiles + blocks - 1);
+                if (blocks >= 2 && eff_rows > eff_tiles) wasted += static_cast<double>(work) * (1.0 / eff_tiles - 1.0 / eff_rows);
+            }
+            row_blocks_ok = wasted > 0.12 * static_cast<double>(total_row_tiles);
+        }
         for (uint32_t g = 0; g < n_groups; ++g) {
             us[g] = n_units;
             vso[g] = 0;

@@ -393,3 +393,24 @@ def test_pipelined_multi_query_equals_one_by_one(b62):
     for (i1, s1), (i2, s2), (i3, s3) in zip(single, many, again[::-1]):
         assert (i1 == i2).all() and (s1 == s2).all() and (i1 == i3).all() and (s1 == s3).all()
     assert (ms > 0).all()
+
+
+def test_concurrent_callers_on_one_database(b62):
+    """run_search "may be called concurrently from many threads on the same db": calls on one handle
+    are serialised inside the library and every caller gets the single-threaded answer."""
+    import threading
+    qs, sdb = synth.config1()
+    rng = np.random.default_rng(71)
+    queries = [qs[0]] + [synth.random_residues(rng, int(rng.integers(20, 400))) for _ in range(5)]
+    g = GapModel(10, 2)
+    with Database(sdb.codes, sdb.offsets) as db:
+        expected = [db.search(q, b62, g, 10)[:2] for q in queries]
+        results = [None] * 12
+        def worker(slot):
+            results[slot] = db.search(queries[slot % len(queries)], b62, g, 10)[:2]
+        threads = [threading.Thread(target=worker, args=(i,)) for i in range(12)]
+        [t.start() for t in threads]
+        [t.join() for t in threads]
+    for slot, (idx, sc) in enumerate(results):
+        ei, es = expected[slot % len(queries)]
+        assert (idx == ei).all() and (sc == es).all()
