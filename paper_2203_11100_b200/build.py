@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libswb200.so"
 SOURCES = ["cabi.cu", "pack.cpp"]
-HEADERS = ["kernels.cuh", "pipe_rates.cuh", "pack.hpp", "plan.inl", "handle.inl", "scan.inl", "persist.inl", "pairs.inl", "pipe.inl",
+HEADERS = ["kernels.cuh", "pipeline.cuh", "pipe_rates.cuh", "pack.hpp", "plan.inl", "handle.inl", "scan.inl", "persist.inl", "pairs.inl", "pipe.inl",
            "multi.inl"]
 
 NVCC_FLAGS = [
@@ -44,7 +44,7 @@ def is_stale() -> bool:
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     if not force and not is_stale():
         return LIB
-    extra = [f"-D{k}={os.environ[k]}" for k in ("SWB_INTER_TILE", "SWB_INTER_THREADS") if k in os.environ]   # tuning only
+    extra = [f"-D{k}={os.environ[k]}" for k in ("SWB_INTER_TILE", "SWB_INTER_THREADS", "SWB_PIPE_STATS") if k in os.environ]   # tuning only
     out = Path(os.environ.get("SWB_LIB_OUT", str(LIB)))
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-ccbin", "/usr/bin/g++", "-o", str(out)] + [str(CSRC / s) for s in SOURCES] + ["-ldl", "-lpthread"]
     if verbose:

@@ -30,6 +30,7 @@
 
 #include "../../include/swb200.h"
 #include "kernels.cuh"
+#include "pipeline.cuh"
 #include "pack.hpp"
 #include "pipe_rates.cuh"
 

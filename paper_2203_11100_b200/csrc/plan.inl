@@ -29,6 +29,39 @@ double narrow_chain_fraction() {
     return f;
 }
 
+// The on-chip tile pipeline (pipeline.cuh) scans the database unless SWB200_PIPE=0.
+bool pipe_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SWB200_PIPE");
+        return e && std::string(e) == "1";
+    }();
+    return on;
+}
+
+uint32_t pipe_lag_div() {
+    static const uint32_t d = [] {
+        const char* e = std::getenv("SWB200_PIPE_LAGDIV");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 1 ? static_cast<uint32_t>(v) : 20u;
+    }();
+    return d;
+}
+
+// Capacity of each border ring (chunks, a power of two) that fits next to the profile; < 2: the pipeline cannot run.
+uint32_t pipe_ring_chunks(const swb_db* db, size_t prof_elems) {
+    static const uint32_t cap = [] {
+        const char* e = std::getenv("SWB200_PIPE_RING");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 2 ? static_cast<uint32_t>(v) : 4u;
+    }();
+    const size_t fixed = ((prof_elems + 255) & ~size_t(255)) + sizeof(PipeCtl);
+    if (fixed >= db->smem_optin) return 0;
+    const size_t room = (db->smem_optin - fixed) / (static_cast<size_t>(kPipeWarps) * kPipeChunkBytes);
+    uint32_t c = 1;
+    while (c * 2 <= room && c * 2 <= cap) c *= 2;
+    return room >= 1 ? c : 0;
+}
+
 QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext) {
     QueryPlan pl;
     pl.m = m;

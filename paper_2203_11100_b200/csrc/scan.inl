@@ -222,7 +222,51 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     SWB_CUDA(cudaEventRecord(db->ev[EV_UP], s));
 
     // ---- the scan ------------------------------------------------------------------------------------
-    if (packed) {
+    if (packed && pipe_enabled() && pipe_ring_chunks(db, prof_elems) >= 2) {
+        PipeParams qp{};
+        qp.codes = reinterpret_cast<const uint4*>(db->d_codes);
+        qp.groups = db->d_groups;
+        qp.group_first = 0;
+        qp.n_items = n_groups;
+        qp.prof8 = db->d_prof8;
+        qp.pstride = pl.pstride;
+        qp.prof_bytes = static_cast<uint32_t>((prof_elems + 255) & ~size_t(255));
+        qp.n_tiles = n_tiles;
+        qp.ring_chunks = pipe_ring_chunks(db, prof_elems);
+        qp.border = db->d_border0;
+        qp.lag_div = pipe_lag_div();
+        qp.slot_scores = db->d_slot_scores;
+        qp.ticket = db->d_counters;
+        qp.neg_open2 = pack16(-open);
+        qp.neg_ext2 = pack16(-ext);
+        const size_t smem = qp.prof_bytes + sizeof(PipeCtl) + static_cast<size_t>(kPipeWarps) * qp.ring_chunks * kPipeChunkBytes;
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(db->sm_count, n_groups));
+        SWB_CUDA(cudaFuncSetAttribute(pipeline_s16_kernel<kInterTile, kInterThreads>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(db->smem_optin)));
+#ifdef SWB_PIPE_STATS
+        static unsigned long long* d_stats = nullptr;   // debug builds only: where do the pipeline's warps wait?
+        if (!d_stats) cudaMalloc(&d_stats, sizeof(unsigned long long) * 4 * kPipeWarps * 1024);
+        cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4 * kPipeWarps * 1024, s);
+        qp.stats = d_stats;
+#endif
+        pipeline_s16_kernel<kInterTile, kInterThreads><<<grid, kInterThreads, smem, s>>>(qp);
+        ++db->launches;
+#ifdef SWB_PIPE_STATS
+        {
+            std::vector<unsigned long long> h(static_cast<size_t>(grid) * kPipeWarps * 4);
+            cudaStreamSynchronize(s);
+            cudaMemcpy(h.data(), d_stats, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+            double tot[kPipeWarps][4] = {};
+            for (uint32_t c = 0; c < grid; ++c)
+                for (uint32_t w = 0; w < kPipeWarps; ++w)
+                    for (int k = 0; k < 4; ++k) tot[w][k] += static_cast<double>(h[(static_cast<size_t>(c) * kPipeWarps + w) * 4 + k]);
+            std::fprintf(stderr, "pipe stats m=%u tiles=%u ring=%u: warp  wait_in%%  wait_out%%  item%%  (of the warp's lifetime)\n", m, n_tiles, qp.ring_chunks);
+            for (uint32_t w = 0; w < kPipeWarps; ++w)
+                std::fprintf(stderr, "   %2u  %6.2f  %6.2f  %6.2f   life %.2f ms\n", w, 100 * tot[w][0] / tot[w][3], 100 * tot[w][1] / tot[w][3],
+                             100 * tot[w][2] / tot[w][3], tot[w][3] / grid / 1.9e6);
+        }
+#endif
+    } else if (packed) {
         WaveParams wp{};
         wp.codes = reinterpret_cast<const uint4*>(db->d_codes);
         wp.groups = db->d_groups;
