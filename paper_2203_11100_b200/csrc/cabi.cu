@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -88,6 +89,9 @@ struct QueryPlan {
 struct swb_db {
     int device = 0;
     cudaStream_t own_stream = nullptr, stream = nullptr;
+    cudaStream_t side_stream = nullptr;   // the pipeline kernel, next to the wavefront kernel on `stream`
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool pipe_attr_set = false;
     int sm_count = 0;
     size_t smem_optin = 0;
     std::mutex mu;
@@ -255,6 +259,7 @@ void swb_db_destroy(swb_db* db) {
     {
         DeviceGuard guard(db->device);
         if (db->own_stream) cudaStreamSynchronize(db->own_stream);
+        if (db->side_stream) cudaStreamSynchronize(db->side_stream);
         void* ptrs[] = {db->d_codes,      db->d_groups,   db->d_slot_index, db->d_slot_len,    db->d_border0,
                         db->d_border1,    db->d_iborder0, db->d_iborder1,   db->d_slot_scores, db->d_flag_list,
                         db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_vstate_off, db->d_vstate, db->d_progress, db->d_keys,        db->d_sel[0],
@@ -268,6 +273,9 @@ void swb_db_destroy(swb_db* db) {
             if (ev) cudaEventDestroy(ev);
         for (auto& ev : db->many_events) cudaEventDestroy(ev);
         if (db->own_stream) cudaStreamDestroy(db->own_stream);
+        if (db->side_stream) cudaStreamDestroy(db->side_stream);
+        if (db->ev_fork) cudaEventDestroy(db->ev_fork);
+        if (db->ev_join) cudaEventDestroy(db->ev_join);
     }
     delete db;
 }

@@ -60,6 +60,11 @@ swb_status init_handle_resources(swb_db* db) {
     if (cudaStreamCreateWithFlags(&db->own_stream, cudaStreamNonBlocking) != cudaSuccess)
         return fail(SWB_ERR_CUDA, "cudaStreamCreate failed");
     db->stream = db->own_stream;
+    if (cudaStreamCreateWithFlags(&db->side_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(SWB_ERR_CUDA, "cudaStreamCreate failed");
+    if (cudaEventCreateWithFlags(&db->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&db->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return fail(SWB_ERR_CUDA, "cudaEventCreate failed");
     for (auto& ev : db->ev)
         if (cudaEventCreate(&ev) != cudaSuccess) return fail(SWB_ERR_CUDA, "cudaEventCreate failed");
     if (cudaMallocHost(reinterpret_cast<void**>(&db->h_counters), 4 * sizeof(uint32_t)) != cudaSuccess)

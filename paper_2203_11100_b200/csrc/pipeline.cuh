@@ -149,7 +149,10 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
     // not finish it with every ring downstream full), so this one link goes through the database-shaped border
     // array in global memory: unbounded, flow-controlled by its head counter only.  It carries 1/16 of the
     // border rows and is read back one pass later from L2.
-    const bool wrap_in = warp == 0, wrap_out = next == 0;
+    // Queries of at most 16 tiles never put two tiles of one group on the same warp, so there the cycle cannot
+    // close and all 16 links are rings.
+    const bool wrap = p.n_tiles > kPipeWarps;
+    const bool wrap_in = wrap && warp == 0, wrap_out = wrap && next == 0;
     const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
     const uint32_t ring_mask = p.ring_chunks - 1;
     const uint32_t ring_bytes = p.ring_chunks * kPipeChunkBytes;
@@ -178,8 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
         uint8_t* gborder = reinterpret_cast<uint8_t*>(p.border + gd.chunk_base * kRowsPerChunk * 32 + lane);
         const uint8_t* gstage = reinterpret_cast<const uint8_t*>(p.border + gd.chunk_base * kRowsPerChunk * 32) + lane * 16;
         const uint32_t in_end = in_pos + gd.n_chunks;
-        const uint32_t lag = p.n_tiles <= kPipeWarps ? p.ring_chunks - 1
-                                                     : max(1u, min(p.ring_chunks - 1, gd.n_chunks / p.lag_div));
+        const uint32_t lag = max(1u, min(p.ring_chunks - 1, gd.n_chunks / p.lag_div));
 
         uint32_t Hm[T], F[T];
 #pragma unroll
@@ -198,7 +200,11 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
                     // the other.  Its inbound rows come from global memory, so they are staged into its (otherwise
                     // unused) ring with cp.async one chunk ahead and read from shared memory like everyone else's.
                     if (staged == in_pos) {
-                        SWB_STAT(w_in, while (lds_acquire(&ctl->head[0]) <= staged) __nanosleep(20));
+                        // nothing in flight (start of a slot, or the producer is close): wait until two chunks are
+                        // published, so that from here on the next chunk can always be requested while this one is
+                        // being consumed
+                        const uint32_t need = min(in_pos + 2, in_end);
+                        SWB_STAT(w_in, while (lds_acquire(&ctl->head[0]) < need) __nanosleep(20));
                         stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
                                     gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
                         ++staged;

@@ -33,16 +33,46 @@ double narrow_chain_fraction() {
 bool pipe_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("SWB200_PIPE");
-        return e && std::string(e) == "1";
+        return !(e && std::string(e) == "0");
     }();
     return on;
+}
+
+double env_number(const char* name, double fallback) {
+    const char* e = std::getenv(name);
+    const double v = e ? std::atof(e) : 0.0;
+    return v > 0.0 ? v : fallback;
+}
+
+// Queries with fewer tiles than this stay with the wavefront kernel.
+uint32_t pipe_min_tiles() {
+    static const uint32_t v = static_cast<uint32_t>(env_number("SWB200_PIPE_MINTILES", 9));
+    return v;
+}
+
+// The pipeline is used when max_rows <= this factor x a warp's fair share of the search (row-tiles).
+double pipe_chain_factor() {
+    static const double v = env_number("SWB200_PIPE_CHAIN", 1.2);
+    return v;
+}
+
+// A group taller than this fraction of a CTA's fair share of rows stays with the wavefront kernel.
+double pipe_tall_fraction() {
+    static const double v = env_number("SWB200_PIPE_TALL", 0.35);
+    return v;
+}
+
+// SMs for the wavefront kernel = its share of the rows x this margin.
+double pipe_wave_margin() {
+    static const double v = env_number("SWB200_PIPE_WAVE_MARGIN", 1.25);
+    return v;
 }
 
 uint32_t pipe_lag_div() {
     static const uint32_t d = [] {
         const char* e = std::getenv("SWB200_PIPE_LAGDIV");
         const int v = e ? std::atoi(e) : 0;
-        return v >= 1 ? static_cast<uint32_t>(v) : 20u;
+        return v >= 1 ? static_cast<uint32_t>(v) : 24u;
     }();
     return d;
 }

@@ -95,6 +95,10 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     const uint32_t n_tiles = (m + pl.tile - 1) / pl.tile;
     const uint32_t n_tiles_narrow = (m + kNarrowTile - 1) / kNarrowTile;
     uint32_t n_units = 0;
+    uint32_t pipe_first = n_groups;   // groups [pipe_first, n_groups) go through the on-chip pipeline
+    uint32_t wave_sms = static_cast<uint32_t>(db->sm_count);   // SMs the wavefront kernel gets
+    const size_t prof_elems = static_cast<size_t>(kProfRows) * pl.pstride;
+    const uint32_t pipe_rings = pipe_ring_chunks(db, prof_elems);
     bool any_narrow = false, any_rowblock = false;
     uint64_t vstate_slots = 0;
     if (packed) {
@@ -116,13 +120,48 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         uint32_t* us = reinterpret_cast<uint32_t*>(stage + off_units);
         uint32_t* vso = reinterpret_cast<uint32_t*>(stage + off_vsoff);
         uint8_t* modes = stage + off_modes;
-        const uint64_t total_row_tiles = db->meta.padded_rows * n_tiles;
-        const uint64_t warps = static_cast<uint64_t>(db->sm_count) * (pl.threads / 32);
+        // Division of labour between the two scan kernels (pipeline.cuh).  The on-chip pipeline gives a group one
+        // CTA, so a group whose rows x tiles exceed about a third of a CTA's fair share of the search (or whose
+        // chain of rows would outlast it) would unbalance it: those few tall groups at the head of the sorted list
+        // stay with the wavefront kernel, which spreads a group over warps of many SMs, and run next to the
+        // pipeline on `wave_sms` SMs of their own.  Short queries (few tiles: little border traffic to save,
+        // chains too short to keep 16 warps in step) and small databases stay with the wavefront kernel entirely.
+        pipe_first = n_groups;
+        wave_sms = static_cast<uint32_t>(db->sm_count);
+        uint64_t wave_row_tiles = db->meta.padded_rows * n_tiles;
+        // While the longest group's chain of rows (sequential in one thread per tile) is what bounds the search,
+        // the wavefront kernel needs every SM it can get for it: the pipeline only takes over once a warp's fair
+        // share of the whole search (in row-tiles) has grown to about the longest group's rows.
+        const double fair_all = static_cast<double>(wave_row_tiles) / (static_cast<double>(db->sm_count) * (pl.threads / 32));
+        const bool chain_bound = static_cast<double>(db->max_rows) > pipe_chain_factor() * fair_all;
+        if (pl.main == kMainS16 && pipe_enabled() && pipe_rings >= 2 && n_tiles >= pipe_min_tiles() && !chain_bound &&
+            n_groups >= 2 * static_cast<uint32_t>(db->sm_count)) {
+            const uint64_t fair_cta = db->meta.padded_rows / static_cast<uint64_t>(db->sm_count);   // rows per CTA
+            const uint64_t tall = std::max<uint64_t>(256, static_cast<uint64_t>(pipe_tall_fraction() * static_cast<double>(fair_cta)));
+            uint32_t g = 0;
+            uint64_t rows_wave = 0;
+            while (g < n_groups && static_cast<uint64_t>(db->meta.groups[g].n_chunks) * kRowsPerChunk > tall) {
+                rows_wave += static_cast<uint64_t>(db->meta.groups[g].n_chunks) * kRowsPerChunk;
+                ++g;
+            }
+            pipe_first = g;
+            if (g == 0) {
+                wave_sms = 0;
+            } else {
+                const double share = static_cast<double>(rows_wave) / static_cast<double>(db->meta.padded_rows);
+                wave_sms = static_cast<uint32_t>(std::ceil(share * pipe_wave_margin() * db->sm_count));
+                wave_sms = std::max<uint32_t>(1, std::min<uint32_t>(wave_sms, static_cast<uint32_t>(db->sm_count) - 1));
+            }
+            wave_row_tiles = rows_wave * n_tiles;
+        }
+        const uint32_t n_wave_groups = pipe_first;   // the wavefront kernel's groups: [0, pipe_first)
+        const uint64_t total_row_tiles = wave_row_tiles;
+        const uint64_t warps = static_cast<uint64_t>(std::max<uint32_t>(wave_sms, 1)) * (pl.threads / 32);
         const uint64_t fair = total_row_tiles / warps;
         // With plenty of groups per warp (a whole Swiss-Prot on one GPU: 3.7) only units larger than about
         // three quarters of a warp's fair share need cutting -- LPT order fills the rest; a small shard with fewer
         // groups than warps has to be cut finer to give every warp several units.
-        const double auto_fraction = std::min(0.75, std::max(0.08, static_cast<double>(n_groups) / (4.0 * static_cast<double>(warps))));
+        const double auto_fraction = std::min(0.75, std::max(0.08, static_cast<double>(n_wave_groups) / (4.0 * static_cast<double>(warps))));
         const double fraction = unit_budget_fraction() > 0.0 ? unit_budget_fraction() : auto_fraction;
         const uint64_t budget = std::max<uint64_t>(2048, static_cast<uint64_t>(fraction * static_cast<double>(fair)));
         const uint64_t narrow_rows = std::max<uint64_t>(2048, static_cast<uint64_t>(narrow_chain_fraction() * fair));
@@ -131,12 +170,12 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         // variant that carries both extra paths spills registers in the common 32-column sweep (about 12 % slower),
         // so a search that needs narrow tiles cuts its other large groups by rows only if cutting them by tile
         // instead would waste more than that (small shards, long queries).
-        const bool narrow_needed = s16 && n_groups && n_tiles_narrow > 1 &&
+        const bool narrow_needed = s16 && n_wave_groups && n_tiles_narrow > 1 &&
                                    static_cast<uint64_t>(db->meta.groups[0].n_chunks) * kRowsPerChunk > narrow_rows;
         bool row_blocks_ok = s16 && row_blocks_enabled();
         if (row_blocks_ok && narrow_needed) {
             double wasted = 0.0;   // extra warp time of tile-splitting where row blocks would have been chosen
-            for (uint32_t g = 0; g < n_groups; ++g) {
+            for (uint32_t g = 0; g < n_wave_groups; ++g) {
                 const uint64_t chunks = db->meta.groups[g].n_chunks, rows = chunks * kRowsPerChunk, work = rows * n_tiles;
                 if (work <= budget || n_tiles < 2 || rows > narrow_rows) continue;
                 const double eff_tiles = static_cast<double>(rows) / static_cast<double>(rows + 16 * (n_tiles - 1));
@@ -146,7 +185,8 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
             }
             row_blocks_ok = wasted > 0.12 * static_cast<double>(total_row_tiles);
         }
-        for (uint32_t g = 0; g < n_groups; ++g) {
+        for (uint32_t g = n_wave_groups; g < n_groups; ++g) us[g] = 0, vso[g] = 0, modes[g] = kGroupSingle;
+        for (uint32_t g = 0; g < n_wave_groups; ++g) {
             us[g] = n_units;
             vso[g] = 0;
             const uint64_t chunks = db->meta.groups[g].n_chunks;
@@ -178,7 +218,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
             any_narrow |= mode == kGroupNarrow;
             n_units += units;
         }
-        us[n_groups] = n_units;
+        us[n_wave_groups] = n_units;
         SWB_CUDA(cudaMemcpyAsync(db->d_unit_start, us, (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, s));
         SWB_CUDA(cudaMemcpyAsync(db->d_group_mode, modes, std::max<size_t>(n_groups, 1), cudaMemcpyHostToDevice, s));
@@ -189,13 +229,12 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
             if ((st = ensure_dev(&db->d_vstate, &db->vstate_cap, need, &db->device_bytes)) != SWB_OK) return st;
         }
         if ((st = ensure_dev(&db->d_progress, &db->progress_cap, n_units, &db->device_bytes)) != SWB_OK) return st;
-        SWB_CUDA(cudaMemsetAsync(db->d_progress, 0, static_cast<size_t>(n_units) * sizeof(uint32_t), s));
-        db->last_units = n_units;
+        if (n_units) SWB_CUDA(cudaMemsetAsync(db->d_progress, 0, static_cast<size_t>(n_units) * sizeof(uint32_t), s));
+        db->last_units = n_units + (n_groups - n_wave_groups);
     }
     SWB_CUDA(cudaMemcpyAsync(db->d_matrix, stage, off_query, cudaMemcpyHostToDevice, s));
     SWB_CUDA(cudaMemcpyAsync(db->d_query, stage + off_query, m, cudaMemcpyHostToDevice, s));
 
-    const size_t prof_elems = static_cast<size_t>(kProfRows) * pl.pstride;
     const size_t profi_elems = static_cast<size_t>(kProfRows) * pl.n_lane_tiles * 8;
     ProfileParams pp{};
     pp.query = db->d_query;
@@ -222,55 +261,50 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     SWB_CUDA(cudaEventRecord(db->ev[EV_UP], s));
 
     // ---- the scan ------------------------------------------------------------------------------------
-    if (packed && pipe_enabled() && pipe_ring_chunks(db, prof_elems) >= 2) {
-        PipeParams qp{};
+    // Pipeline groups run on a second stream next to the wavefront kernel's tall groups; the SMs the wavefront
+    // kernel used join the pipeline's item queue when it is done (a second, small pipeline launch behind it).
+    const uint32_t n_pipe_items = n_groups - pipe_first;
+    PipeParams qp{};
+    size_t pipe_smem = 0;
+    if (packed && n_pipe_items) {
         qp.codes = reinterpret_cast<const uint4*>(db->d_codes);
         qp.groups = db->d_groups;
-        qp.group_first = 0;
-        qp.n_items = n_groups;
+        qp.group_first = pipe_first;
+        qp.n_items = n_pipe_items;
         qp.prof8 = db->d_prof8;
         qp.pstride = pl.pstride;
         qp.prof_bytes = static_cast<uint32_t>((prof_elems + 255) & ~size_t(255));
         qp.n_tiles = n_tiles;
-        qp.ring_chunks = pipe_ring_chunks(db, prof_elems);
-        qp.border = db->d_border0;
+        qp.ring_chunks = pipe_rings;
         qp.lag_div = pipe_lag_div();
+        qp.border = db->d_border0;
         qp.slot_scores = db->d_slot_scores;
-        qp.ticket = db->d_counters;
+        qp.ticket = db->d_counters + 2;
         qp.neg_open2 = pack16(-open);
         qp.neg_ext2 = pack16(-ext);
-        const size_t smem = qp.prof_bytes + sizeof(PipeCtl) + static_cast<size_t>(kPipeWarps) * qp.ring_chunks * kPipeChunkBytes;
-        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(db->sm_count, n_groups));
-        SWB_CUDA(cudaFuncSetAttribute(pipeline_s16_kernel<kInterTile, kInterThreads>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(db->smem_optin)));
-#ifdef SWB_PIPE_STATS
-        static unsigned long long* d_stats = nullptr;   // debug builds only: where do the pipeline's warps wait?
-        if (!d_stats) cudaMalloc(&d_stats, sizeof(unsigned long long) * 4 * kPipeWarps * 1024);
-        cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4 * kPipeWarps * 1024, s);
-        qp.stats = d_stats;
-#endif
-        pipeline_s16_kernel<kInterTile, kInterThreads><<<grid, kInterThreads, smem, s>>>(qp);
-        ++db->launches;
-#ifdef SWB_PIPE_STATS
-        {
-            std::vector<unsigned long long> h(static_cast<size_t>(grid) * kPipeWarps * 4);
-            cudaStreamSynchronize(s);
-            cudaMemcpy(h.data(), d_stats, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-            double tot[kPipeWarps][4] = {};
-            for (uint32_t c = 0; c < grid; ++c)
-                for (uint32_t w = 0; w < kPipeWarps; ++w)
-                    for (int k = 0; k < 4; ++k) tot[w][k] += static_cast<double>(h[(static_cast<size_t>(c) * kPipeWarps + w) * 4 + k]);
-            std::fprintf(stderr, "pipe stats m=%u tiles=%u ring=%u: warp  wait_in%%  wait_out%%  item%%  (of the warp's lifetime)\n", m, n_tiles, qp.ring_chunks);
-            for (uint32_t w = 0; w < kPipeWarps; ++w)
-                std::fprintf(stderr, "   %2u  %6.2f  %6.2f  %6.2f   life %.2f ms\n", w, 100 * tot[w][0] / tot[w][3], 100 * tot[w][1] / tot[w][3],
-                             100 * tot[w][2] / tot[w][3], tot[w][3] / grid / 1.9e6);
+        pipe_smem = qp.prof_bytes + sizeof(PipeCtl) + static_cast<size_t>(kPipeWarps) * qp.ring_chunks * kPipeChunkBytes;
+        if (!db->pipe_attr_set) {
+            SWB_CUDA(cudaFuncSetAttribute(pipeline_s16_kernel<kInterTile, kInterThreads>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(db->smem_optin)));
+            db->pipe_attr_set = true;
         }
-#endif
-    } else if (packed) {
+        const uint32_t wave_grid = pipe_first ? wave_sms : 0;
+        const uint32_t side_grid = std::min<uint32_t>(static_cast<uint32_t>(db->sm_count) - wave_grid, n_pipe_items);
+        if (wave_grid) {
+            SWB_CUDA(cudaEventRecord(db->ev_fork, s));
+            SWB_CUDA(cudaStreamWaitEvent(db->side_stream, db->ev_fork, 0));
+            pipeline_s16_kernel<kInterTile, kInterThreads><<<side_grid, kInterThreads, pipe_smem, db->side_stream>>>(qp);
+            SWB_CUDA(cudaEventRecord(db->ev_join, db->side_stream));
+        } else {
+            pipeline_s16_kernel<kInterTile, kInterThreads><<<side_grid, kInterThreads, pipe_smem, s>>>(qp);
+        }
+        ++db->launches;
+    }
+    if (packed && pipe_first) {
         WaveParams wp{};
         wp.codes = reinterpret_cast<const uint4*>(db->d_codes);
         wp.groups = db->d_groups;
-        wp.n_groups = n_groups;
+        wp.n_groups = pipe_first;
         wp.unit_start = db->d_unit_start;
         wp.group_mode = db->d_group_mode;
         wp.vstate_off = db->d_vstate_off;
@@ -289,7 +323,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.neg_ext2 = pack16(-ext);
         const size_t smem = prof_elems;
         const uint32_t warps_per_cta = pl.threads / 32;
-        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(db->sm_count, (n_units + warps_per_cta - 1) / warps_per_cta));
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(wave_sms, (n_units + warps_per_cta - 1) / warps_per_cta));
         const bool in_smem = smem <= db->smem_optin;
         {
 #define SWB_LAUNCH_S16(NARROW, RB)                                                                                 \
@@ -312,6 +346,12 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
 #undef SWB_LAUNCH_S16
         }
         ++db->launches;
+        if (n_pipe_items) {
+            // the wavefront kernel's SMs are free now: let them help with whatever pipeline items are left
+            pipeline_s16_kernel<kInterTile, kInterThreads><<<grid, kInterThreads, pipe_smem, s>>>(qp);
+            ++db->launches;
+            SWB_CUDA(cudaStreamWaitEvent(s, db->ev_join, 0));
+        }
     }
     SWB_CUDA(cudaEventRecord(db->ev[EV_SCAN], s));
 
