@@ -130,6 +130,14 @@ swb_status swb_db_info_get(const swb_db* db, swb_db_info* info);
  * handle's own stream. */
 swb_status swb_db_set_stream(swb_db* db, void* cuda_stream);
 
+/* Which kernel scans the database (results are identical; tests and tuning use this to exercise each path):
+ *   SWB_SCAN_AUTO      per search: the on-chip tile pipeline for the bulk of the groups next to the wavefront
+ *                      kernel on the few tall ones; short queries and small databases use the wavefront kernel
+ *   SWB_SCAN_PIPELINE  every group through the on-chip pipeline whenever the query profile leaves room for its rings
+ *   SWB_SCAN_WAVEFRONT every group through the wavefront kernel */
+typedef enum swb_scan_policy { SWB_SCAN_AUTO = 0, SWB_SCAN_PIPELINE = 1, SWB_SCAN_WAVEFRONT = 2 } swb_scan_policy;
+swb_status swb_db_set_scan_policy(swb_db* db, int32_t policy);
+
 /* One query against the shard: scores every sequence, selects the top_k hits.
  *   hits      room for top_k entries;  *n_hits = min(top_k, n_local)
  *   stats     optional

@@ -80,6 +80,7 @@ SIGNATURES = {
     "swb_db_load": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),
     "swb_db_info_get": (C.c_int, [C.c_void_p, C.POINTER(SwbDbInfo)]),
     "swb_db_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "swb_db_set_scan_policy": (C.c_int, [C.c_void_p, C.c_int32]),
     "swb_search": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32,
                              C.POINTER(SwbHit), u32p, C.POINTER(SwbStats)]),
     "swb_search_many": (C.c_int, [C.c_void_p, C.POINTER(u8p), u32p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32,

@@ -92,6 +92,7 @@ struct swb_db {
     cudaStream_t side_stream = nullptr;   // the pipeline kernel, next to the wavefront kernel on `stream`
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool pipe_attr_set = false;
+    int scan_policy = SWB_SCAN_AUTO;
     int sm_count = 0;
     size_t smem_optin = 0;
     std::mutex mu;
@@ -296,6 +297,14 @@ swb_status swb_db_info_get(const swb_db* db, swb_db_info* info) {
     info->device_bytes = db->device_bytes;
     info->length_threshold = db->meta.length_threshold;
     info->device = db->device;
+    return SWB_OK;
+}
+
+swb_status swb_db_set_scan_policy(swb_db* db, int32_t policy) {
+    if (!db) return fail(SWB_ERR_INVALID, "db is null");
+    if (policy < SWB_SCAN_AUTO || policy > SWB_SCAN_WAVEFRONT) return fail(SWB_ERR_INVALID, "unknown scan policy");
+    std::lock_guard<std::mutex> lock(db->mu);
+    db->scan_policy = policy;
     return SWB_OK;
 }
 

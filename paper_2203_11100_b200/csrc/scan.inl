@@ -134,8 +134,12 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         // share of the whole search (in row-tiles) has grown to about the longest group's rows.
         const double fair_all = static_cast<double>(wave_row_tiles) / (static_cast<double>(db->sm_count) * (pl.threads / 32));
         const bool chain_bound = static_cast<double>(db->max_rows) > pipe_chain_factor() * fair_all;
-        if (pl.main == kMainS16 && pipe_enabled() && pipe_rings >= 2 && n_tiles >= pipe_min_tiles() && !chain_bound &&
-            n_groups >= 2 * static_cast<uint32_t>(db->sm_count)) {
+        if (pl.main == kMainS16 && pipe_rings >= 2 && db->scan_policy == SWB_SCAN_PIPELINE) {
+            pipe_first = 0;
+            wave_sms = 0;
+            wave_row_tiles = 0;
+        } else if (pl.main == kMainS16 && db->scan_policy == SWB_SCAN_AUTO && pipe_enabled() && pipe_rings >= 2 &&
+                   n_tiles >= pipe_min_tiles() && !chain_bound && n_groups >= 2 * static_cast<uint32_t>(db->sm_count)) {
             const uint64_t fair_cta = db->meta.padded_rows / static_cast<uint64_t>(db->sm_count);   // rows per CTA
             const uint64_t tall = std::max<uint64_t>(256, static_cast<uint64_t>(pipe_tall_fraction() * static_cast<double>(fair_cta)));
             uint32_t g = 0;

@@ -137,6 +137,12 @@ class Database:
         _raise(self._lib, self._lib.swb_db_info_get(self._h, C.byref(info)))
         return info.as_dict()
 
+    SCAN_AUTO, SCAN_PIPELINE, SCAN_WAVEFRONT = 0, 1, 2
+
+    def set_scan_policy(self, policy: int):
+        """Which kernel scans the database (swb_scan_policy); results are identical."""
+        _raise(self._lib, self._lib.swb_db_set_scan_policy(self._h, policy))
+
     def set_stream(self, cuda_stream: int):
         _raise(self._lib, self._lib.swb_db_set_stream(self._h, C.c_void_p(cuda_stream)))
 

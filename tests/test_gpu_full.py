@@ -60,6 +60,27 @@ def test_sampled_score_parity(full, port, b62):
     assert (got >= 0).all()
 
 
+def test_sampled_score_parity_through_the_pipeline(full, port, b62):
+    """m = 1000 takes the hybrid scan (on-chip pipeline + wavefront kernel on the tall groups): sampled scores equal
+    the oracle's, and the whole score vector equals the wavefront kernel's."""
+    queries, sdb, db = full
+    q = queries[9]
+    got, st = db.score_all(q, b62, GapModel(10, 2))
+    rng = np.random.default_rng(3)
+    lens = sdb.lengths()
+    sample = np.unique(np.concatenate([rng.choice(sdb.n, 1200, replace=False), np.argsort(lens)[-12:],
+                                       np.nonzero(lens == 0)[0][:5], np.array(sdb.planted[9])]))
+    sub = po.FlatDb.from_list([sdb.seq(int(i)) for i in sample])
+    exp = port.score_all(q, sub, b62, 10, 2)
+    assert (got[sample] == exp).all()
+    db.set_scan_policy(Database.SCAN_WAVEFRONT)
+    try:
+        alone, _ = db.score_all(q, b62, GapModel(10, 2))
+    finally:
+        db.set_scan_policy(Database.SCAN_AUTO)
+    assert (got == alone).all()
+
+
 def test_sharded_full_database(full, b62):
     queries, sdb, db = full
     q = queries[6]

@@ -414,3 +414,50 @@ def test_concurrent_callers_on_one_database(b62):
     for slot, (idx, sc) in enumerate(results):
         ei, es = expected[slot % len(queries)]
         assert (idx == ei).all() and (sc == es).all()
+
+
+@pytest.mark.parametrize("policy", [Database.SCAN_PIPELINE, Database.SCAN_WAVEFRONT])
+@pytest.mark.parametrize("seed,thr,gaps", [(11, 3000, (10, 2)), (12, 100, (11, 1)), (13, 0, (5, 5)), (14, 10 ** 9, (0, 0))])
+def test_random_databases_on_each_scan_kernel(port, b62, seed, thr, gaps, policy):
+    """Every group forced through the on-chip tile pipeline (and, for contrast, through the wavefront kernel):
+    all scores and the ranked list equal the oracle's.  Query lengths straddle the tile (32) and pass (16 tiles
+    = 512 columns) boundaries of the pipeline."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(200, 1500))
+    seqs = [synth.random_residues(rng, int(rng.integers(0, 400))) for _ in range(n)]
+    seqs[0] = synth.random_residues(rng, 2500)      # one tall group
+    seqs[1] = np.zeros(0, np.uint8)
+    fdb = po.FlatDb.from_list(seqs)
+    with Database(fdb.codes, fdb.offsets, length_threshold=thr) as db:
+        db.set_scan_policy(policy)
+        for m in (1, 31, 32, 33, 300, 511, 512, 513, 545, 1100):
+            q = synth.random_residues(rng, m)
+            got, st = db.score_all(q, b62, GapModel(*gaps))
+            exp = port.score_all(q, fdb, b62, *gaps)
+            assert (got == exp).all(), f"m={m}"
+        q = synth.mutate(rng, seqs[0], 0.1, 3)[:1500]   # a query with a strong hit in the tall group
+        idx, sc, _ = db.search(q, b62, GapModel(*gaps), 25)
+        ei, es, _ = port.run_search(q, fdb, b62, *gaps, length_threshold=thr, top_k=25)
+        assert (idx == ei).all() and (sc == es).all()
+
+
+def test_hybrid_scan_equals_each_kernel_alone(b62):
+    """A database large enough for the automatic policy to split the work (tall groups to the wavefront kernel,
+    the rest to the pipeline, side by side on two streams): identical score vectors under all three policies,
+    including back-to-back searches that reuse the border arrays and ticket counters."""
+    rng = np.random.default_rng(81)
+    queries = synth.make_queries([700, 1200], seed=81)
+    sdb = synth.make_database(40_000, target_residues=12_000_000, max_len=9000, queries=queries, seed=81)
+    g = GapModel(10, 2)
+    with Database(sdb.codes, sdb.offsets) as db:
+        ref = {}
+        for policy in (Database.SCAN_WAVEFRONT, Database.SCAN_PIPELINE, Database.SCAN_AUTO, Database.SCAN_AUTO):
+            db.set_scan_policy(policy)
+            for qi, q in enumerate(queries):
+                got, st = db.score_all(q, b62, g)
+                if qi in ref:
+                    assert (got == ref[qi]).all(), f"policy {policy} query {qi}"
+                else:
+                    ref[qi] = got
+                idx, sc, _ = db.search(q, b62, g, 10)
+                assert idx[0] == sdb.planted[qi][0]
