@@ -14,7 +14,7 @@ one full sweep: 20 searches, 8.5e12 cell updates.  GCUPS = sum(query_len x db_re
   e2e        the same sweep through the C-ABI call a user makes (swb_search: HOST query/matrix buffers in, HOST
              hits out, host<->device copies and host gaps inside the timed region), bracketed by CUDA events on
              the stream the kernels run on plus a barrier; max over ranks.
-  roofline   the dominant kernel (wavefront_s16_kernel) against the DPX cell-update roofline P_dpx x 2 / 6
+  roofline   the scan kernels (pipeline_s16_kernel, wavefront_s16_kernel) against the DPX cell-update roofline P_dpx x 2 / 6
              (SURVEY.md 8(d)); P_dpx is measured live by swb_measure_pipe_rates.  The HBM side (packed-database
              stream, 1 byte per residue per search) is reported against MEASURED_PEAKS.json.
   cpu_baseline  the unmodified reference (oracle/_ref/libswref.so, run_search without traceback) on the host
@@ -319,7 +319,8 @@ def main_native(args):
             "warmup": args.warmup, "ms_per_step": e2e_ms / steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "s16x2 (packed int16 DPX) + int32 re-run", "data": "synthetic",
             "config": {"workload": workload_name(args.scale), "parallelism": f"db-shard x{world}",
-                       "l2": "inputs larger than L2: 207 MB packed database + 1.7 GB border rows per sweep vs 126 MB L2",
+                       "l2": "inputs larger than L2: the 207 MB packed database is streamed once per search vs 126 MB L2; "
+                             "consecutive searches use different queries",
                        "db": {k: info[k] for k in ("n_total", "n_local", "n_groups", "residues", "padded_residues", "device_bytes")},
                        "pack_upload_s_outside_timing": pack_upload_s},
             "e2e": {"value": e2e, "unit": "GCUPS",
@@ -329,10 +330,12 @@ def main_native(args):
                     "pipelined_swb_search_many": (total_cells / (pipelined_ms * 1e-3) / 1e9) if pipelined_ms else None},
             "gpu_launches": launches,
             "clocks": clocks,
-            "roofline": {"bound": "dpx_alu", "kernel": "wavefront_s16_kernel", "achieved": scan_gcups, "peak": roof,
+            "roofline": {"bound": "dpx_alu", "kernel": "pipeline_s16_kernel (+ wavefront_s16_kernel: tall groups, short queries)",
+                         "achieved": scan_gcups, "peak": roof,
                          "unit": "GCUPS", "frac": scan_gcups / roof,
                          "peak_def": "P_dpx x 2 / 6, P_dpx = measured VIADDMNMX.S16x2 thread-instr/s (live, this run)",
-                         "p_dpx_ginst_per_s": p_dpx, "pipe_rates": rates, "traffic": traffic,
+                         "p_dpx_ginst_per_s": p_dpx, "pipe_rates": rates,
+                         "traffic": traffic.get("dram_bytes") if traffic else None, "traffic_detail": traffic,
                          "hbm": {"bound": "hbm", "achieved": db_stream_gbs, "peak": hbm_peak, "unit": "GB/s",
                                  "frac": db_stream_gbs / hbm_peak,
                                  "peak_src": "MEASURED_PEAKS.json" if peaks else "fallback",

@@ -227,6 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
             const uint2* bin = reinterpret_cast<const uint2*>(ring_in + (in_pos & ring_mask) * kPipeChunkBytes);
             uint8_t* bout = wrap_out ? gborder + static_cast<size_t>(chunk) * kPipeChunkBytes
                                      : ring_out + (out_pos & ring_mask) * kPipeChunkBytes;
+            uint2 bnext = make_uint2(NO, NO);
+            if (!first) bnext = bin[0];
 #pragma unroll
             for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
                 const uint32_t wa = r < 4 ? cur.x : cur.y;
@@ -242,8 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
                     wA[4 * i] = va.x, wA[4 * i + 1] = va.y, wA[4 * i + 2] = va.z, wA[4 * i + 3] = va.w;
                     wB[4 * i] = vb.x, wB[4 * i + 1] = vb.y, wB[4 * i + 2] = vb.z, wB[4 * i + 3] = vb.w;
                 }
-                uint2 bi = make_uint2(NO, NO);
-                if (!first) bi = bin[r * 32];
+                const uint2 bi = bnext;   // this row's inbound border, loaded while the previous row was computed
+                if (!first && r + 1 < static_cast<int>(kRowsPerChunk)) bnext = bin[(r + 1) * 32];
                 uint32_t hl = bi.x;   // Hm of the column left of the tile, this row
                 uint32_t E = bi.y;
                 uint32_t diag = diag_in;

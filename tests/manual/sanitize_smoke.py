@@ -25,6 +25,16 @@ for m in (40, 300, 1500):
             good = bool((got == exp).all())
             ok &= good
             print(f"m={m} thr={thr} parity={good} units={st['chunks_claimed']}")
+# the on-chip tile pipeline, forced for every group: ring hand-over, wrap-around through global memory (m > 512)
+for m in (33, 600, 1100):
+    q = synth.random_residues(rng, m)
+    exp = port.score_all(q, fdb, b62, 10, 2)
+    with Database(fdb.codes, fdb.offsets) as db:
+        db.set_scan_policy(Database.SCAN_PIPELINE)
+        got, st = db.score_all(q, b62, g)
+        good = bool((got == exp).all())
+        ok &= good
+        print(f"pipeline m={m} parity={good}")
 q = np.full(3400, 17, np.uint8)
 with Database.from_sequences([q, q[:3100], seqs[5]]) as db:
     got, st = db.score_all(q, b62, g)
