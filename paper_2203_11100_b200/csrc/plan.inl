@@ -50,7 +50,7 @@ uint32_t pipe_min_tiles() {
     return v;
 }
 
-// The pipeline is used when max_rows <= this factor x a warp's fair share of the search (row-tiles).
+// A search is chain-bound when max_rows > this factor x a warp's fair share of the search (row-tiles).
 double pipe_chain_factor() {
     static const double v = env_number("SWB200_PIPE_CHAIN", 1.2);
     return v;
@@ -62,7 +62,12 @@ double pipe_tall_fraction() {
     return v;
 }
 
-// SMs for the wavefront kernel = its share of the rows x this margin.
+double pipe_wave_margin_chain() {
+    static const double v = env_number("SWB200_PIPE_WAVE_MARGIN_CHAIN", 2.0);
+    return v;
+}
+
+// SMs for the wavefront kernel = its share of the rows x this margin (the one above when chain-bound).
 double pipe_wave_margin() {
     static const double v = env_number("SWB200_PIPE_WAVE_MARGIN", 1.25);
     return v;

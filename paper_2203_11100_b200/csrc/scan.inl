@@ -129,9 +129,10 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         pipe_first = n_groups;
         wave_sms = static_cast<uint32_t>(db->sm_count);
         uint64_t wave_row_tiles = db->meta.padded_rows * n_tiles;
-        // While the longest group's chain of rows (sequential in one thread per tile) is what bounds the search,
-        // the wavefront kernel needs every SM it can get for it: the pipeline only takes over once a warp's fair
-        // share of the whole search (in row-tiles) has grown to about the longest group's rows.
+        // While the longest group's chain of rows (sequential in one thread per tile) is what bounds the search
+        // -- its rows exceed a warp's fair share of the whole search in row-tiles -- the wavefront kernel's SMs
+        // are busy for the whole search whatever their number, and it gets more of them (measured: margin 2
+        // instead of 1.25 is worth 15 % at m = 375 and costs 2 % at m = 1000 on the Swiss-Prot shape).
         const double fair_all = static_cast<double>(wave_row_tiles) / (static_cast<double>(db->sm_count) * (pl.threads / 32));
         const bool chain_bound = static_cast<double>(db->max_rows) > pipe_chain_factor() * fair_all;
         if (pl.main == kMainS16 && pipe_rings >= 2 && db->scan_policy == SWB_SCAN_PIPELINE) {
@@ -139,7 +140,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
             wave_sms = 0;
             wave_row_tiles = 0;
         } else if (pl.main == kMainS16 && db->scan_policy == SWB_SCAN_AUTO && pipe_enabled() && pipe_rings >= 2 &&
-                   n_tiles >= pipe_min_tiles() && !chain_bound && n_groups >= 2 * static_cast<uint32_t>(db->sm_count)) {
+                   n_tiles >= pipe_min_tiles() && n_groups >= 2 * static_cast<uint32_t>(db->sm_count)) {
             const uint64_t fair_cta = db->meta.padded_rows / static_cast<uint64_t>(db->sm_count);   // rows per CTA
             const uint64_t tall = std::max<uint64_t>(256, static_cast<uint64_t>(pipe_tall_fraction() * static_cast<double>(fair_cta)));
             uint32_t g = 0;
@@ -153,7 +154,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
                 wave_sms = 0;
             } else {
                 const double share = static_cast<double>(rows_wave) / static_cast<double>(db->meta.padded_rows);
-                wave_sms = static_cast<uint32_t>(std::ceil(share * pipe_wave_margin() * db->sm_count));
+                wave_sms = static_cast<uint32_t>(std::ceil(share * (chain_bound ? pipe_wave_margin_chain() : pipe_wave_margin()) * db->sm_count));
                 wave_sms = std::max<uint32_t>(1, std::min<uint32_t>(wave_sms, static_cast<uint32_t>(db->sm_count) - 1));
             }
             wave_row_tiles = rows_wave * n_tiles;
@@ -294,6 +295,12 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         }
         const uint32_t wave_grid = pipe_first ? wave_sms : 0;
         const uint32_t side_grid = std::min<uint32_t>(static_cast<uint32_t>(db->sm_count) - wave_grid, n_pipe_items);
+#ifdef SWB_PIPE_STATS
+        static unsigned long long* d_stats = nullptr;   // debug builds only: where do the pipeline's warps wait?
+        if (!d_stats) cudaMalloc(&d_stats, sizeof(unsigned long long) * 4 * kPipeWarps * 1024);
+        cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4 * kPipeWarps * 1024, s);
+        qp.stats = d_stats;
+#endif
         if (wave_grid) {
             SWB_CUDA(cudaEventRecord(db->ev_fork, s));
             SWB_CUDA(cudaStreamWaitEvent(db->side_stream, db->ev_fork, 0));
@@ -357,6 +364,27 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
             SWB_CUDA(cudaStreamWaitEvent(s, db->ev_join, 0));
         }
     }
+#ifdef SWB_PIPE_STATS
+    if (packed && n_pipe_items) {
+        const uint32_t grid = std::min<uint32_t>(static_cast<uint32_t>(db->sm_count) - (pipe_first ? wave_sms : 0), n_pipe_items);
+        std::vector<unsigned long long> h(static_cast<size_t>(grid) * kPipeWarps * 4);
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h.data(), qp.stats, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        double tot[kPipeWarps][4] = {};
+        for (uint32_t c = 0; c < grid; ++c)
+            for (uint32_t w = 0; w < kPipeWarps; ++w)
+                for (int k = 0; k < 4; ++k) tot[w][k] += static_cast<double>(h[(static_cast<size_t>(c) * kPipeWarps + w) * 4 + k]);
+        std::fprintf(stderr, "pipe stats m=%u tiles=%u ring=%u grid=%u: warp  wait_in%%  wait_out%%  item%%  (of the warp's lifetime)\n", m, n_tiles,
+                     qp.ring_chunks, grid);
+        double sum_in = 0, sum_out = 0;
+        for (uint32_t w = 0; w < kPipeWarps; ++w) {
+            std::fprintf(stderr, "   %2u  %6.2f  %6.2f  %6.2f   life %.2f ms\n", w, 100 * tot[w][0] / tot[w][3], 100 * tot[w][1] / tot[w][3],
+                         100 * tot[w][2] / tot[w][3], tot[w][3] / grid / 1.9e6);
+            sum_in += 100 * tot[w][0] / tot[w][3] / kPipeWarps, sum_out += 100 * tot[w][1] / tot[w][3] / kPipeWarps;
+        }
+        std::fprintf(stderr, "   mean wait_in %.2f%% wait_out %.2f%%\n", sum_in, sum_out);
+    }
+#endif
     SWB_CUDA(cudaEventRecord(db->ev[EV_SCAN], s));
 
     // ---- int32: re-run of lanes above the trust limit, or everything when the packed path is out ----

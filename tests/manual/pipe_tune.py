@@ -10,11 +10,12 @@ def child(lens):
     qs = synth.make_queries(lens, 7)
     b62 = synth.blosum62()
     out = []
-    with Database(sdb.codes, sdb.offsets) as db:
+    shards = int(os.environ.get("TUNE_SHARDS", "1"))   # time shard 0 of N; numbers are N x shard throughput
+    with Database(sdb.codes, sdb.offsets, shard_rank=0, shard_count=shards) as db:
         for q in qs:
             db.search(q, b62, GapModel(10, 2), 10)
             best = min(db.search(q, b62, GapModel(10, 2), 10)[2]["ms_scan"] for _ in range(3))
-            out.append(f"{len(q)}:{len(q) * sdb.residues / best / 1e6:.0f}")
+            out.append(f"{len(q)}:{len(q) * sdb.residues / best / 1e6:.0f}({best:.1f}ms)")
     print("RESULT " + "  ".join(out), flush=True)
 
 
