@@ -248,25 +248,27 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
                 if (!first && r + 1 < static_cast<int>(kRowsPerChunk)) bnext = bin[(r + 1) * 32];
                 uint32_t hl = bi.x;   // Hm of the column left of the tile, this row
                 uint32_t E = bi.y;
-                uint32_t diag = diag_in;
+                // d of a column is formed from the OLD Hm of the column to its left, i.e. before that register is
+                // overwritten in place: every Hm[k] and F[k] then stays in one physical register for the whole
+                // chunk and the compiler needs no moves to rotate them
+                uint32_t d = __vadd2(diag_in, prmt(wA[0], wB[0], 0xC480u));
                 diag_in = hl;
 #pragma unroll
                 for (int k = 0; k < T; k += 2) {
-                    const uint32_t s0 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xC480u : 0xE6A2u);
                     const uint32_t s1 = prmt(wA[k / 4], wB[k / 4], (k & 3) == 0 ? 0xD591u : 0xF7B3u);
+                    // cell k
                     E = __viaddmax_s16x2(E, NE, hl);
                     F[k] = __viaddmax_s16x2(F[k], NE, Hm[k]);
-                    const uint32_t d0 = __vadd2(diag, s0);
-                    const uint32_t h0 = __vimax3_s16x2_relu(d0, E, F[k]);
-                    diag = Hm[k];
-                    hl = __vadd2(h0, NO);
+                    const uint32_t d0 = d;
+                    const uint32_t d1 = __vadd2(Hm[k], s1);
+                    hl = __vadd2(__vimax3_s16x2_relu(d0, E, F[k]), NO);
                     Hm[k] = hl;
+                    // cell k+1
                     E = __viaddmax_s16x2(E, NE, hl);
                     F[k + 1] = __viaddmax_s16x2(F[k + 1], NE, Hm[k + 1]);
-                    const uint32_t d1 = __vadd2(diag, s1);
-                    const uint32_t h1 = __vimax3_s16x2_relu(d1, E, F[k + 1]);
-                    diag = Hm[k + 1];
-                    hl = __vadd2(h1, NO);
+                    if (k + 2 < T)
+                        d = __vadd2(Hm[k + 1], prmt(wA[(k + 2) / 4], wB[(k + 2) / 4], ((k + 2) & 3) == 0 ? 0xC480u : 0xE6A2u));
+                    hl = __vadd2(__vimax3_s16x2_relu(d1, E, F[k + 1]), NO);
                     Hm[k + 1] = hl;
                     best = __vimax3_s16x2(best, d0, d1);   // see sweep_unit_s16: max over the diagonal terms is exact
                 }
