@@ -264,6 +264,27 @@ swb_status swb_measure_pipe_rates(int32_t device, double seconds, swb_pipe_rates
 swb_status swb_shard_assignment(const uint32_t* lens, uint32_t n, uint64_t length_threshold,
                                 uint32_t shard_count, uint32_t* shard_of);
 
+/* How a search of `query_len` columns over a database with these sequence lengths would be divided between the
+ * two scan kernels on a GPU of `sm_count` SMs (host arithmetic only, no device needed; for tests, tuning and
+ * capacity planning).  The reference's counterpart is the chunk lists of detail::make_chunks
+ * (scheduler.hpp:130-138) and the two worker pools (scheduler.hpp:200-213). */
+typedef struct swb_scan_plan_info {
+    uint32_t n_groups;          /* groups of 64 sequences in the shard                                     */
+    uint32_t n_tiles;           /* 32-column query tiles                                                   */
+    uint32_t pipeline_groups;   /* groups the on-chip pipeline scans (one item each)                       */
+    uint32_t wavefront_groups;  /* groups the wavefront kernel scans (the tallest ones, or all)            */
+    uint32_t wavefront_sms;     /* SMs the wavefront kernel runs on                                        */
+    uint32_t wavefront_units;   /* its work units                                                          */
+    uint32_t split_groups, narrow_groups, rowblock_groups;   /* wavefront groups cut by tile / 8-column tile / rows */
+    uint32_t ring_chunks;       /* pipeline: chunks per shared-memory ring next to this query's profile    */
+    int32_t chain_bound;        /* the longest group's chain of rows bounds the search                     */
+    int32_t reserved;
+    uint64_t pipeline_rows, wavefront_rows;   /* padded rows on either side                                */
+} swb_scan_plan_info;
+swb_status swb_scan_plan(const uint32_t* lens, uint32_t n, uint64_t length_threshold, uint32_t shard_rank,
+                         uint32_t shard_count, uint32_t query_len, uint32_t sm_count, int32_t policy,
+                         swb_scan_plan_info* out);
+
 #ifdef __cplusplus
 }
 #endif

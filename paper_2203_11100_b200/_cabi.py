@@ -54,6 +54,18 @@ class SwbAlignment(C.Structure):
                 ("subject_end", C.c_uint64), ("n_ops", C.c_uint64), ("score", C.c_int32), ("capped", C.c_int32)]
 
 
+class SwbScanPlanInfo(C.Structure):
+    _fields_ = [
+        ("n_groups", C.c_uint32), ("n_tiles", C.c_uint32), ("pipeline_groups", C.c_uint32), ("wavefront_groups", C.c_uint32),
+        ("wavefront_sms", C.c_uint32), ("wavefront_units", C.c_uint32), ("split_groups", C.c_uint32),
+        ("narrow_groups", C.c_uint32), ("rowblock_groups", C.c_uint32), ("ring_chunks", C.c_uint32),
+        ("chain_bound", C.c_int32), ("reserved", C.c_int32), ("pipeline_rows", C.c_uint64), ("wavefront_rows", C.c_uint64),
+    ]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_ if "reserved" not in name}
+
+
 class SwbPipeRates(C.Structure):
     _fields_ = [
         ("viaddmnmx_s16x2", C.c_double), ("vimnmx3_s16x2", C.c_double), ("viadd_16x2", C.c_double),
@@ -109,6 +121,8 @@ SIGNATURES = {
     "swb_mdb_shard": (C.c_void_p, [C.c_void_p, C.c_uint32]),
     "swb_measure_pipe_rates": (C.c_int, [C.c_int32, C.c_double, C.POINTER(SwbPipeRates)]),
     "swb_shard_assignment": (C.c_int, [u32p, C.c_uint32, C.c_uint64, C.c_uint32, u32p]),
+    "swb_scan_plan": (C.c_int, [u32p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int32,
+                                C.POINTER(SwbScanPlanInfo)]),
 }
 
 _lib = None

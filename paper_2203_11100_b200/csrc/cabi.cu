@@ -34,6 +34,10 @@
 #include "pipeline.cuh"
 #include "pack.hpp"
 #include "pipe_rates.cuh"
+#include "scan_plan.hpp"
+
+static_assert(swb::kScanAuto == SWB_SCAN_AUTO && swb::kScanPipeline == SWB_SCAN_PIPELINE && swb::kScanWavefront == SWB_SCAN_WAVEFRONT,
+              "scan_plan.hpp and swb200.h disagree on the scan policies");
 
 using namespace swb;
 
@@ -479,6 +483,54 @@ swb_status swb_shard_assignment(const uint32_t* lens, uint32_t n, uint64_t lengt
     std::vector<uint32_t> result;
     shard_assignment(src, length_threshold, shard_count, result);
     for (uint32_t i = 0; i < n; ++i) shard_of[i] = result[i];
+    return SWB_OK;
+}
+
+swb_status swb_scan_plan(const uint32_t* lens, uint32_t n, uint64_t length_threshold, uint32_t shard_rank,
+                         uint32_t shard_count, uint32_t query_len, uint32_t sm_count, int32_t policy,
+                         swb_scan_plan_info* out) {
+    if (!out || (n && !lens)) return fail(SWB_ERR_INVALID, "null argument");
+    if (shard_count < 1 || shard_rank >= shard_count) return fail(SWB_ERR_INVALID, "shard_rank must be < shard_count");
+    if (sm_count < 1) return fail(SWB_ERR_INVALID, "sm_count must be >= 1");
+    if (policy < SWB_SCAN_AUTO || policy > SWB_SCAN_WAVEFRONT) return fail(SWB_ERR_INVALID, "unknown scan policy");
+    std::memset(out, 0, sizeof(*out));
+    SeqSource src;
+    static const uint32_t kNoLens[1] = {0};
+    src.lens = n ? lens : kNoLens;
+    src.n = n;
+    std::vector<GroupDesc> groups;
+    uint64_t padded_rows = 0;
+    group_table(src, length_threshold, shard_rank, shard_count, groups, &padded_rows);
+    const uint32_t n_groups = static_cast<uint32_t>(groups.size());
+    out->n_groups = n_groups;
+    if (query_len == 0 || n_groups == 0) return SWB_OK;
+    constexpr size_t kSmemOptinB200 = 227 * 1024;
+    ScanShape shape;
+    shape.groups = groups.data();
+    shape.n_groups = n_groups;
+    shape.padded_rows = padded_rows;
+    shape.n_tiles = (query_len + kInterTile - 1) / kInterTile;
+    shape.n_tiles_narrow = (query_len + kNarrowTile - 1) / kNarrowTile;
+    shape.sm_count = sm_count;
+    shape.warps_per_cta = kInterThreads / 32;
+    shape.policy = policy;
+    shape.pipe_rings = ring_chunks_for(static_cast<size_t>(kProfRows) * profile_stride(query_len, kInterTile), kSmemOptinB200,
+                                       sizeof(PipeCtl), static_cast<size_t>(kPipeWarps) * kPipeChunkBytes, scan_knobs().pipe_ring_cap);
+    std::vector<uint32_t> us(static_cast<size_t>(n_groups) + 1), vso(n_groups);
+    std::vector<uint8_t> modes(n_groups);
+    const ScanPlan sp = plan_scan(shape, scan_knobs(), us.data(), vso.data(), modes.data());
+    out->n_tiles = shape.n_tiles;
+    out->pipeline_groups = n_groups - sp.pipe_first;
+    out->wavefront_groups = sp.pipe_first;
+    out->wavefront_sms = sp.wave_sms;
+    out->wavefront_units = sp.n_units;
+    out->split_groups = sp.n_split;
+    out->narrow_groups = sp.n_narrow;
+    out->rowblock_groups = sp.n_rowblock;
+    out->ring_chunks = shape.pipe_rings;
+    out->chain_bound = sp.chain_bound ? 1 : 0;
+    out->wavefront_rows = sp.wave_rows;
+    out->pipeline_rows = padded_rows - sp.wave_rows;
     return SWB_OK;
 }
 

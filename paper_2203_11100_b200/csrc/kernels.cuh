@@ -24,6 +24,7 @@
 #include <stdint.h>
 
 #include "pack.hpp"
+#include "scan_plan.hpp"
 
 namespace swb {
 
@@ -315,18 +316,7 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
     return best;
 }
 
-// Group modes, decided per search by the host (cabi.cu) and uploaded next to unit_start.
-enum GroupMode : uint8_t {
-    kGroupSingle = 0,   // one unit: all tiles of width T, one warp
-    kGroupSplit = 1,    // one unit per tile of width T: a wavefront of warps
-    kGroupNarrow = 2,   // one unit per tile of width 8: a wavefront with a 4x shorter per-row chain, for groups whose
-                        // rows x T sequential chain would otherwise outlast the whole search (short query, very
-                        // long sequences)
-    kGroupRowBlock = 3  // units are blocks of rows, each swept over all tiles one tile behind the block above; the
-                        // efficient split when the query has many tiles and the group few rows (long queries,
-                        // small per-GPU shards)
-};
-constexpr int kNarrowTile = 8;
+// Group modes (GroupMode, kNarrowTile): scan_plan.hpp, where the host decides them per search.
 
 // kNarrow: compile the 8-column path in.  Searches without narrow groups (all long queries) launch the variant
 // without it, whose register allocation is not disturbed by the second sweep.

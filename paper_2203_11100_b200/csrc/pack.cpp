@@ -63,7 +63,56 @@ void parallel_for(size_t n, Fn&& fn) {
     for (auto& t : pool) t.join();
 }
 
+// The shard's sequences, longest first: every long sequence is at least as long as every short one, so the long
+// pool followed by the short pool is sorted.
+void local_pool(const SeqSource& src, uint64_t threshold, uint32_t shard_rank, uint32_t shard_count,
+                std::vector<Key>& pool, uint32_t* n_short, uint32_t* n_long) {
+    std::vector<Key> shorts_all, longs_all, shorts, longs;
+    sorted_pools(src, threshold, shorts_all, longs_all);
+    if (shard_count == 1) {
+        shorts.swap(shorts_all);
+        longs.swap(longs_all);
+    } else {
+        for (size_t p = 0; p < shorts_all.size(); ++p)
+            if (snake(p, shard_count) == shard_rank) shorts.push_back(shorts_all[p]);
+        for (size_t p = 0; p < longs_all.size(); ++p)
+            if (shard_count - 1 - snake(p, shard_count) == shard_rank) longs.push_back(longs_all[p]);
+    }
+    *n_short = static_cast<uint32_t>(shorts.size());
+    *n_long = static_cast<uint32_t>(longs.size());
+    pool = std::move(longs);
+    pool.insert(pool.end(), shorts.begin(), shorts.end());
+}
+
+// Groups of 64 over the sorted pool; rows padded to the group's longest member (its first) rounded up to 8.
+// Returns the total number of chunks.
+uint64_t build_groups(const std::vector<Key>& pool, std::vector<GroupDesc>& groups, uint64_t* padded_rows,
+                      uint32_t* max_length) {
+    const size_t n_groups = (pool.size() + kGroupSeqs - 1) / kGroupSeqs;
+    groups.resize(n_groups);
+    uint64_t chunk_cursor = 0;
+    *padded_rows = 0;
+    *max_length = 0;
+    for (size_t g = 0; g < n_groups; ++g) {
+        const uint32_t longest = pool[g * kGroupSeqs].len;
+        const uint32_t n_chunks = (longest + kRowsPerChunk - 1) / kRowsPerChunk;
+        groups[g] = GroupDesc{chunk_cursor, n_chunks, static_cast<uint32_t>(g * kGroupSeqs)};
+        chunk_cursor += n_chunks;
+        *padded_rows += static_cast<uint64_t>(n_chunks) * kRowsPerChunk;
+        *max_length = std::max(*max_length, longest);
+    }
+    return chunk_cursor;
+}
+
 }  // namespace
+
+void group_table(const SeqSource& src, uint64_t threshold, uint32_t shard_rank, uint32_t shard_count,
+                 std::vector<GroupDesc>& groups, uint64_t* padded_rows) {
+    std::vector<Key> pool;
+    uint32_t n_short = 0, n_long = 0, max_length = 0;
+    local_pool(src, threshold, shard_rank, shard_count, pool, &n_short, &n_long);
+    build_groups(pool, groups, padded_rows, &max_length);
+}
 
 void shard_assignment(const SeqSource& src, uint64_t threshold, uint32_t shard_count,
                       std::vector<uint32_t>& shard_of) {
@@ -93,27 +142,11 @@ std::string pack_database(const SeqSource& src, uint64_t threshold, uint32_t sha
     out.shard_count = shard_count;
     out.length_threshold = threshold;
 
-    std::vector<Key> shorts_all, longs_all, shorts, longs;
-    sorted_pools(src, threshold, shorts_all, longs_all);
-    if (shard_count == 1) {
-        shorts.swap(shorts_all);
-        longs.swap(longs_all);
-    } else {
-        for (size_t p = 0; p < shorts_all.size(); ++p)
-            if (snake(p, shard_count) == shard_rank) shorts.push_back(shorts_all[p]);
-        for (size_t p = 0; p < longs_all.size(); ++p)
-            if (shard_count - 1 - snake(p, shard_count) == shard_rank) longs.push_back(longs_all[p]);
-    }
-    out.n_short = static_cast<uint32_t>(shorts.size());
-    out.n_long = static_cast<uint32_t>(longs.size());
+    std::vector<Key> pool;
+    local_pool(src, threshold, shard_rank, shard_count, pool, &out.n_short, &out.n_long);
     out.n_local = out.n_short + out.n_long;
 
-    // ---- groups of 64 over the whole shard, longest first ------------------------------------------
-    // every long sequence is at least as long as every short one, so longs + shorts is sorted
-    std::vector<Key> pool(std::move(longs));
-    pool.insert(pool.end(), shorts.begin(), shorts.end());
     const size_t n_groups = (pool.size() + kGroupSeqs - 1) / kGroupSeqs;
-    out.groups.resize(n_groups);
     out.slot_index.assign(n_groups * kGroupSeqs, kNoSequence);
     out.slot_len.assign(n_groups * kGroupSeqs, 0);
 
@@ -123,15 +156,7 @@ std::string pack_database(const SeqSource& src, uint64_t threshold, uint32_t sha
         return pos < pool.size() ? &pool[pos] : nullptr;
     };
 
-    uint64_t chunk_cursor = 0;
-    for (size_t g = 0; g < n_groups; ++g) {
-        const uint32_t longest = member(g, 0)->len;  // sorted: first member is the longest
-        const uint32_t n_chunks = (longest + kRowsPerChunk - 1) / kRowsPerChunk;
-        out.groups[g] = GroupDesc{chunk_cursor, n_chunks, static_cast<uint32_t>(g * kGroupSeqs)};
-        chunk_cursor += n_chunks;
-        out.padded_rows += static_cast<uint64_t>(n_chunks) * kRowsPerChunk;
-        out.max_length = std::max(out.max_length, longest);
-    }
+    const uint64_t chunk_cursor = build_groups(pool, out.groups, &out.padded_rows, &out.max_length);
     out.total_chunks = chunk_cursor;
     out.codes.assign(static_cast<size_t>(chunk_cursor) * 32 * 16, kPadCode);
 

@@ -59,13 +59,17 @@ struct SeqSource {
     const uint8_t* flat = nullptr;
     const uint64_t* offsets = nullptr;
     uint32_t n = 0;
-    uint64_t length(uint32_t i) const { return ptrs ? lens[i] : offsets[i + 1] - offsets[i]; }
+    uint64_t length(uint32_t i) const { return lens ? lens[i] : offsets[i + 1] - offsets[i]; }   // lens alone is enough for planning
     const uint8_t* data(uint32_t i) const { return ptrs ? ptrs[i] : flat + offsets[i]; }
 };
 
 // shard_of[i] for every sequence.  Deterministic; depends only on the lengths.
 void shard_assignment(const SeqSource& src, uint64_t threshold, uint32_t shard_count,
                       std::vector<uint32_t>& shard_of);
+
+// The shard's group table alone (what pack_database would build), from the lengths only: for planning and tests.
+void group_table(const SeqSource& src, uint64_t threshold, uint32_t shard_rank, uint32_t shard_count,
+                 std::vector<GroupDesc>& groups, uint64_t* padded_rows);
 
 // Returns empty string on success, else an error message; *bad_code set when a residue >= 24 was seen.
 std::string pack_database(const SeqSource& src, uint64_t threshold, uint32_t shard_rank,

@@ -1,100 +1,17 @@
-// plan.inl -- per-search decisions: which kernel scans the database, profile geometry, unit policy knobs.
+// plan.inl -- per-search decisions: arithmetic width, profile geometry, intra-task geometry (the division of the
+// scan into kernels and units is scan_plan.hpp).
 // Included by cabi.cu inside its anonymous namespace.
 
-// Fraction of a warp's fair share of the search above which a group is split into a wavefront.
-double unit_budget_fraction() {
-    static const double f = [] {
-        const char* e = std::getenv("SWB200_UNIT_BUDGET");
-        const double v = e ? std::atof(e) : 0.0;
-        return v > 0.0 ? v : 0.0;   // 0: automatic (see score_core)
-    }();
-    return f;
+// Policy knobs (defaults + environment overrides), read once.
+const ScanKnobs& scan_knobs() {
+    static const ScanKnobs k = ScanKnobs::from_env();
+    return k;
 }
 
-bool row_blocks_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("SWB200_ROWBLOCKS");
-        return !(e && std::string(e) == "0");
-    }();
-    return on;
-}
-
-// A group goes to 8-column tiles when its rows exceed this fraction of a warp's fair share (in row-tiles).
-double narrow_chain_fraction() {
-    static const double f = [] {
-        const char* e = std::getenv("SWB200_NARROW");
-        const double v = e ? std::atof(e) : 0.0;
-        return v > 0.0 ? v : 0.9;
-    }();
-    return f;
-}
-
-// The on-chip tile pipeline (pipeline.cuh) scans the database unless SWB200_PIPE=0.
-bool pipe_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("SWB200_PIPE");
-        return !(e && std::string(e) == "0");
-    }();
-    return on;
-}
-
-double env_number(const char* name, double fallback) {
-    const char* e = std::getenv(name);
-    const double v = e ? std::atof(e) : 0.0;
-    return v > 0.0 ? v : fallback;
-}
-
-// Queries with fewer tiles than this stay with the wavefront kernel.
-uint32_t pipe_min_tiles() {
-    static const uint32_t v = static_cast<uint32_t>(env_number("SWB200_PIPE_MINTILES", 9));
-    return v;
-}
-
-// A search is chain-bound when max_rows > this factor x a warp's fair share of the search (row-tiles).
-double pipe_chain_factor() {
-    static const double v = env_number("SWB200_PIPE_CHAIN", 1.2);
-    return v;
-}
-
-// A group taller than this fraction of a CTA's fair share of rows stays with the wavefront kernel.
-double pipe_tall_fraction() {
-    static const double v = env_number("SWB200_PIPE_TALL", 0.35);
-    return v;
-}
-
-double pipe_wave_margin_chain() {
-    static const double v = env_number("SWB200_PIPE_WAVE_MARGIN_CHAIN", 2.0);
-    return v;
-}
-
-// SMs for the wavefront kernel = its share of the rows x this margin (the one above when chain-bound).
-double pipe_wave_margin() {
-    static const double v = env_number("SWB200_PIPE_WAVE_MARGIN", 1.25);
-    return v;
-}
-
-uint32_t pipe_lag_div() {
-    static const uint32_t d = [] {
-        const char* e = std::getenv("SWB200_PIPE_LAGDIV");
-        const int v = e ? std::atoi(e) : 0;
-        return v >= 1 ? static_cast<uint32_t>(v) : 24u;
-    }();
-    return d;
-}
-
-// Capacity of each border ring (chunks, a power of two) that fits next to the profile; < 2: the pipeline cannot run.
+// Capacity of each border ring of the pipeline kernel next to a profile of `prof_elems` bytes; < 2: it cannot run.
 uint32_t pipe_ring_chunks(const swb_db* db, size_t prof_elems) {
-    static const uint32_t cap = [] {
-        const char* e = std::getenv("SWB200_PIPE_RING");
-        const int v = e ? std::atoi(e) : 0;
-        return v >= 2 ? static_cast<uint32_t>(v) : 4u;
-    }();
-    const size_t fixed = ((prof_elems + 255) & ~size_t(255)) + sizeof(PipeCtl);
-    if (fixed >= db->smem_optin) return 0;
-    const size_t room = (db->smem_optin - fixed) / (static_cast<size_t>(kPipeWarps) * kPipeChunkBytes);
-    uint32_t c = 1;
-    while (c * 2 <= room && c * 2 <= cap) c *= 2;
-    return room >= 1 ? c : 0;
+    return ring_chunks_for(prof_elems, db->smem_optin, sizeof(PipeCtl), static_cast<size_t>(kPipeWarps) * kPipeChunkBytes,
+                           scan_knobs().pipe_ring_cap);
 }
 
 QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext) {
@@ -119,9 +36,7 @@ QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t
 
     pl.tile = kInterTile;
     pl.threads = kInterThreads;
-    // wavefront profile stride: columns padded to whole tiles, then to 16 (mod 128) bytes
-    const uint32_t mpad = std::max<uint32_t>(pl.tile, (m + pl.tile - 1) / pl.tile * pl.tile);
-    pl.pstride = mpad + ((16 + 128 - (mpad % 128)) % 128);
+    pl.pstride = profile_stride(m, pl.tile);
 
     // intra-task geometry: T columns per lane (4..8), W warps per CTA, passes
     uint64_t best_cols = ~0ull;

@@ -100,142 +100,40 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     const size_t prof_elems = static_cast<size_t>(kProfRows) * pl.pstride;
     const uint32_t pipe_rings = pipe_ring_chunks(db, prof_elems);
     bool any_narrow = false, any_rowblock = false;
-    uint64_t vstate_slots = 0;
     if (packed) {
-        // Unit policy (see kernels.cuh, GroupMode).  Work is counted in row-tiles (one row of one T-column tile);
-        // `fair` is one warp's share of the whole search.
-        //   single    the default: one warp scores the group's 64 sequences end to end;
-        //   split     a group whose sweep exceeds `budget` is cut so that no unit dominates the makespan and there
-        //             are enough units for every warp, either
-        //               by tile   (wavefront of warps, each 2 chunks behind its left neighbour:
-        //                          efficiency rows / (rows + 16 (tiles - 1))), or
-        //               by rows   (blocks of rows, each one tile behind the block above:
-        //                          efficiency tiles / (tiles + blocks - 1)),
-        //             whichever wastes less;
-        //   narrow    even a tile-split group's per-tile chain (rows x T columns, strictly sequential in one thread,
-        //             ~900 clk per row when the SM empties out, against ~1600 clk per row-tile of saturated
-        //             throughput) would take more than about half the whole search: 8-column tiles cut that chain
-        //             four-fold.
-        // Row blocks and narrow tiles exist in the s16 kernel only.
+        // which kernel scans which groups, and the wavefront kernel's units: scan_plan.hpp
         uint32_t* us = reinterpret_cast<uint32_t*>(stage + off_units);
         uint32_t* vso = reinterpret_cast<uint32_t*>(stage + off_vsoff);
         uint8_t* modes = stage + off_modes;
-        // Division of labour between the two scan kernels (pipeline.cuh).  The on-chip pipeline gives a group one
-        // CTA, so a group whose rows x tiles exceed about a third of a CTA's fair share of the search (or whose
-        // chain of rows would outlast it) would unbalance it: those few tall groups at the head of the sorted list
-        // stay with the wavefront kernel, which spreads a group over warps of many SMs, and run next to the
-        // pipeline on `wave_sms` SMs of their own.  Short queries (few tiles: little border traffic to save,
-        // chains too short to keep 16 warps in step) and small databases stay with the wavefront kernel entirely.
-        pipe_first = n_groups;
-        wave_sms = static_cast<uint32_t>(db->sm_count);
-        uint64_t wave_row_tiles = db->meta.padded_rows * n_tiles;
-        // While the longest group's chain of rows (sequential in one thread per tile) is what bounds the search
-        // -- its rows exceed a warp's fair share of the whole search in row-tiles -- the wavefront kernel's SMs
-        // are busy for the whole search whatever their number, and it gets more of them (measured: margin 2
-        // instead of 1.25 is worth 15 % at m = 375 and costs 2 % at m = 1000 on the Swiss-Prot shape).
-        const double fair_all = static_cast<double>(wave_row_tiles) / (static_cast<double>(db->sm_count) * (pl.threads / 32));
-        const bool chain_bound = static_cast<double>(db->max_rows) > pipe_chain_factor() * fair_all;
-        if (pl.main == kMainS16 && pipe_rings >= 2 && db->scan_policy == SWB_SCAN_PIPELINE) {
-            pipe_first = 0;
-            wave_sms = 0;
-            wave_row_tiles = 0;
-        } else if (pl.main == kMainS16 && db->scan_policy == SWB_SCAN_AUTO && pipe_enabled() && pipe_rings >= 2 &&
-                   n_tiles >= pipe_min_tiles() && n_groups >= 2 * static_cast<uint32_t>(db->sm_count)) {
-            const uint64_t fair_cta = db->meta.padded_rows / static_cast<uint64_t>(db->sm_count);   // rows per CTA
-            const uint64_t tall = std::max<uint64_t>(256, static_cast<uint64_t>(pipe_tall_fraction() * static_cast<double>(fair_cta)));
-            uint32_t g = 0;
-            uint64_t rows_wave = 0;
-            while (g < n_groups && static_cast<uint64_t>(db->meta.groups[g].n_chunks) * kRowsPerChunk > tall) {
-                rows_wave += static_cast<uint64_t>(db->meta.groups[g].n_chunks) * kRowsPerChunk;
-                ++g;
-            }
-            pipe_first = g;
-            if (g == 0) {
-                wave_sms = 0;
-            } else {
-                const double share = static_cast<double>(rows_wave) / static_cast<double>(db->meta.padded_rows);
-                wave_sms = static_cast<uint32_t>(std::ceil(share * (chain_bound ? pipe_wave_margin_chain() : pipe_wave_margin()) * db->sm_count));
-                wave_sms = std::max<uint32_t>(1, std::min<uint32_t>(wave_sms, static_cast<uint32_t>(db->sm_count) - 1));
-            }
-            wave_row_tiles = rows_wave * n_tiles;
-        }
-        const uint32_t n_wave_groups = pipe_first;   // the wavefront kernel's groups: [0, pipe_first)
-        const uint64_t total_row_tiles = wave_row_tiles;
-        const uint64_t warps = static_cast<uint64_t>(std::max<uint32_t>(wave_sms, 1)) * (pl.threads / 32);
-        const uint64_t fair = total_row_tiles / warps;
-        // With plenty of groups per warp (a whole Swiss-Prot on one GPU: 3.7) only units larger than about
-        // three quarters of a warp's fair share need cutting -- LPT order fills the rest; a small shard with fewer
-        // groups than warps has to be cut finer to give every warp several units.
-        const double auto_fraction = std::min(0.75, std::max(0.08, static_cast<double>(n_wave_groups) / (4.0 * static_cast<double>(warps))));
-        const double fraction = unit_budget_fraction() > 0.0 ? unit_budget_fraction() : auto_fraction;
-        const uint64_t budget = std::max<uint64_t>(2048, static_cast<uint64_t>(fraction * static_cast<double>(fair)));
-        const uint64_t narrow_rows = std::max<uint64_t>(2048, static_cast<uint64_t>(narrow_chain_fraction() * fair));
-        const bool s16 = pl.main == kMainS16;
-        // groups are sorted longest first: narrow tiles are needed iff the first group needs them.  The kernel
-        // variant that carries both extra paths spills registers in the common 32-column sweep (about 12 % slower),
-        // so a search that needs narrow tiles cuts its other large groups by rows only if cutting them by tile
-        // instead would waste more than that (small shards, long queries).
-        const bool narrow_needed = s16 && n_wave_groups && n_tiles_narrow > 1 &&
-                                   static_cast<uint64_t>(db->meta.groups[0].n_chunks) * kRowsPerChunk > narrow_rows;
-        bool row_blocks_ok = s16 && row_blocks_enabled();
-        if (row_blocks_ok && narrow_needed) {
-            double wasted = 0.0;   // extra warp time of tile-splitting where row blocks would have been chosen
-            for (uint32_t g = 0; g < n_wave_groups; ++g) {
-                const uint64_t chunks = db->meta.groups[g].n_chunks, rows = chunks * kRowsPerChunk, work = rows * n_tiles;
-                if (work <= budget || n_tiles < 2 || rows > narrow_rows) continue;
-                const double eff_tiles = static_cast<double>(rows) / static_cast<double>(rows + 16 * (n_tiles - 1));
-                const uint64_t blocks = std::min<uint64_t>((work + budget - 1) / budget, std::max<uint64_t>(chunks / 2, 1));
-                const double eff_rows = static_cast<double>(n_tiles) / static_cast<double>(n_tiles + blocks - 1);
-                if (blocks >= 2 && eff_rows > eff_tiles) wasted += static_cast<double>(work) * (1.0 / eff_tiles - 1.0 / eff_rows);
-            }
-            row_blocks_ok = wasted > 0.12 * static_cast<double>(total_row_tiles);
-        }
-        for (uint32_t g = n_wave_groups; g < n_groups; ++g) us[g] = 0, vso[g] = 0, modes[g] = kGroupSingle;
-        for (uint32_t g = 0; g < n_wave_groups; ++g) {
-            us[g] = n_units;
-            vso[g] = 0;
-            const uint64_t chunks = db->meta.groups[g].n_chunks;
-            const uint64_t rows = chunks * kRowsPerChunk;
-            const uint64_t work = rows * n_tiles;
-            uint8_t mode = kGroupSingle;
-            uint32_t units = 1;
-            if (work > budget && n_tiles > 1) {
-                mode = kGroupSplit;
-                units = n_tiles;
-                const double eff_tiles = static_cast<double>(rows) / static_cast<double>(rows + 16 * (n_tiles - 1));
-                // row blocks of at least 2 chunks, about `budget` row-tiles each
-                const uint64_t blocks = std::min<uint64_t>((work + budget - 1) / budget, std::max<uint64_t>(chunks / 2, 1));
-                const double eff_rows = static_cast<double>(n_tiles) / static_cast<double>(n_tiles + blocks - 1);
-                if (row_blocks_ok && blocks >= 2 && eff_rows > eff_tiles) {
-                    mode = kGroupRowBlock;
-                    units = static_cast<uint32_t>(blocks);
-                    vso[g] = static_cast<uint32_t>(vstate_slots);
-                    vstate_slots += n_tiles;
-                    any_rowblock = true;
-                }
-            }
-            if (s16 && rows > narrow_rows && n_tiles_narrow > 1) {
-                if (mode == kGroupRowBlock) vstate_slots -= n_tiles;
-                mode = kGroupNarrow;
-                units = n_tiles_narrow;
-            }
-            modes[g] = mode;
-            any_narrow |= mode == kGroupNarrow;
-            n_units += units;
-        }
-        us[n_wave_groups] = n_units;
+        ScanShape shape;
+        shape.groups = db->meta.groups.data();
+        shape.n_groups = n_groups;
+        shape.padded_rows = db->meta.padded_rows;
+        shape.n_tiles = n_tiles;
+        shape.n_tiles_narrow = n_tiles_narrow;
+        shape.sm_count = static_cast<uint32_t>(db->sm_count);
+        shape.warps_per_cta = pl.threads / 32;
+        shape.s16 = pl.main == kMainS16;
+        shape.policy = db->scan_policy;
+        shape.pipe_rings = pipe_rings;
+        const ScanPlan sp = plan_scan(shape, scan_knobs(), us, vso, modes);
+        pipe_first = sp.pipe_first;
+        wave_sms = sp.wave_sms;
+        n_units = sp.n_units;
+        any_narrow = sp.any_narrow;
+        any_rowblock = sp.any_rowblock;
         SWB_CUDA(cudaMemcpyAsync(db->d_unit_start, us, (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, s));
         SWB_CUDA(cudaMemcpyAsync(db->d_group_mode, modes, std::max<size_t>(n_groups, 1), cudaMemcpyHostToDevice, s));
         SWB_CUDA(cudaMemcpyAsync(db->d_vstate_off, vso, std::max<size_t>(n_groups, 1) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, s));
         if (any_rowblock) {
-            const size_t need = static_cast<size_t>(vstate_slots) * (kVStateWords / 4) * 32;
+            const size_t need = static_cast<size_t>(sp.vstate_slots) * (kVStateWords / 4) * 32;
             if ((st = ensure_dev(&db->d_vstate, &db->vstate_cap, need, &db->device_bytes)) != SWB_OK) return st;
         }
         if ((st = ensure_dev(&db->d_progress, &db->progress_cap, n_units, &db->device_bytes)) != SWB_OK) return st;
         if (n_units) SWB_CUDA(cudaMemsetAsync(db->d_progress, 0, static_cast<size_t>(n_units) * sizeof(uint32_t), s));
-        db->last_units = n_units + (n_groups - n_wave_groups);
+        db->last_units = n_units + (n_groups - pipe_first);
     }
     SWB_CUDA(cudaMemcpyAsync(db->d_matrix, stage, off_query, cudaMemcpyHostToDevice, s));
     SWB_CUDA(cudaMemcpyAsync(db->d_query, stage + off_query, m, cudaMemcpyHostToDevice, s));
@@ -281,7 +179,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         qp.prof_bytes = static_cast<uint32_t>((prof_elems + 255) & ~size_t(255));
         qp.n_tiles = n_tiles;
         qp.ring_chunks = pipe_rings;
-        qp.lag_div = pipe_lag_div();
+        qp.lag_div = scan_knobs().pipe_lag_div;
         qp.border = db->d_border0;
         qp.slot_scores = db->d_slot_scores;
         qp.ticket = db->d_counters + 2;

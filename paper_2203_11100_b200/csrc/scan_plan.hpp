@@ -1,0 +1,250 @@
+// scan_plan.hpp -- host-only: how one search is divided between the two scan kernels and into work units.
+//
+// Replaces the reference's chunk lists (detail::make_chunks, scheduler.hpp:130-138: short chunks of
+// lane_width*16 sequences, long chunks of one) and its two worker pools (scheduler.hpp:200-213).  Pure
+// arithmetic on the packed database's group table; no CUDA, so the CPU test-suite exercises it through
+// swb_scan_plan (tests/test_host.py).
+//
+// Work is counted in row-tiles (one row of one 32-column tile for a group of 64 sequences).
+//
+// 1. Division of labour (pipeline.cuh).  The on-chip pipeline gives a group one CTA, so a group whose rows
+//    exceed about a third of a CTA's fair share of the database would unbalance it: those few tall groups at
+//    the head of the sorted list stay with the wavefront kernel, which spreads a group over warps of many SMs,
+//    and run next to the pipeline on `wave_sms` SMs of their own.  Queries of fewer than 9 tiles (little border
+//    traffic to save, chains too short to keep 16 warps in step) and databases with fewer than two groups per SM
+//    stay with the wavefront kernel entirely.
+// 2. Unit policy of the wavefront kernel (kernels.cuh, GroupMode).  `fair` is one warp's share of its groups.
+//      single    the default: one warp scores the group's 64 sequences end to end;
+//      split     a group whose sweep exceeds `budget` is cut so that no unit dominates the makespan and there
+//                are enough units for every warp, either
+//                  by tile   (wavefront of warps, each 2 chunks behind its left neighbour:
+//                             efficiency rows / (rows + 16 (tiles - 1))), or
+//                  by rows   (blocks of rows, each one tile behind the block above:
+//                             efficiency tiles / (tiles + blocks - 1)),
+//                whichever wastes less;
+//      narrow    even a tile-split group's per-tile chain (rows x 32 columns, strictly sequential in one
+//                thread, ~900 clk per row when the SM empties out, against ~1600 clk per row-tile of saturated
+//                throughput) would take more than about half the whole search: 8-column tiles cut that chain
+//                four-fold.
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <string>
+
+#include "pack.hpp"
+
+namespace swb {
+
+// Group modes of the wavefront kernel, decided per search and uploaded next to unit_start.
+enum GroupMode : uint8_t {
+    kGroupSingle = 0,   // one unit: all tiles of width T, one warp
+    kGroupSplit = 1,    // one unit per tile of width T: a wavefront of warps
+    kGroupNarrow = 2,   // one unit per tile of width 8: a wavefront with a 4x shorter per-row chain, for groups whose
+                        // rows x T sequential chain would otherwise outlast the whole search (short query, very
+                        // long sequences)
+    kGroupRowBlock = 3  // units are blocks of rows, each swept over all tiles one tile behind the block above; the
+                        // efficient split when the query has many tiles and the group few rows (long queries,
+                        // small per-GPU shards)
+};
+constexpr int kNarrowTile = 8;
+
+enum ScanPolicy : int { kScanAuto = 0, kScanPipeline = 1, kScanWavefront = 2 };   // = swb_scan_policy
+
+// Tuning knobs; the defaults were measured on B200 (profiles/r01_summary.md), the environment overrides them.
+struct ScanKnobs {
+    double unit_budget = 0.0;        // SWB200_UNIT_BUDGET: fraction of a warp's fair share above which a group is split (0: automatic)
+    bool row_blocks = true;          // SWB200_ROWBLOCKS=0 disables the row-block split
+    double narrow_chain = 0.9;       // SWB200_NARROW: a group goes to 8-column tiles when its rows exceed this x fair
+    bool pipe = true;                // SWB200_PIPE=0: never use the pipeline under the automatic policy
+    uint32_t pipe_min_tiles = 9;     // SWB200_PIPE_MINTILES
+    double pipe_chain = 1.2;         // SWB200_PIPE_CHAIN: chain-bound when max_rows > this x a warp's fair share of the search
+    double pipe_tall = 0.35;         // SWB200_PIPE_TALL: groups taller than this x a CTA's fair share of rows go to the wavefront kernel
+    double wave_margin = 1.25;       // SWB200_PIPE_WAVE_MARGIN: wavefront SMs = its share of the rows x this ...
+    double wave_margin_chain = 2.0;  // SWB200_PIPE_WAVE_MARGIN_CHAIN: ... or x this when chain-bound (its SMs are then
+                                     // busy for the whole search whatever their number: +15 % at m = 375, -2 % at m = 1000)
+    uint32_t pipe_ring_cap = 4;      // SWB200_PIPE_RING: chunks per shared-memory ring at most (power of two)
+    uint32_t pipe_lag_div = 24;      // SWB200_PIPE_LAGDIV: a tile starts group_chunks / this chunks behind its neighbour
+
+    static ScanKnobs from_env() {
+        ScanKnobs k;
+        auto num = [](const char* name, double fallback) {
+            const char* e = std::getenv(name);
+            const double v = e ? std::atof(e) : 0.0;
+            return v > 0.0 ? v : fallback;
+        };
+        auto off = [](const char* name) {
+            const char* e = std::getenv(name);
+            return e && std::string(e) == "0";
+        };
+        k.unit_budget = num("SWB200_UNIT_BUDGET", 0.0);
+        k.row_blocks = !off("SWB200_ROWBLOCKS");
+        k.narrow_chain = num("SWB200_NARROW", k.narrow_chain);
+        k.pipe = !off("SWB200_PIPE");
+        k.pipe_min_tiles = static_cast<uint32_t>(num("SWB200_PIPE_MINTILES", k.pipe_min_tiles));
+        k.pipe_chain = num("SWB200_PIPE_CHAIN", k.pipe_chain);
+        k.pipe_tall = num("SWB200_PIPE_TALL", k.pipe_tall);
+        k.wave_margin = num("SWB200_PIPE_WAVE_MARGIN", k.wave_margin);
+        k.wave_margin_chain = num("SWB200_PIPE_WAVE_MARGIN_CHAIN", k.wave_margin_chain);
+        k.pipe_ring_cap = std::max<uint32_t>(2, static_cast<uint32_t>(num("SWB200_PIPE_RING", k.pipe_ring_cap)));
+        k.pipe_lag_div = std::max<uint32_t>(1, static_cast<uint32_t>(num("SWB200_PIPE_LAGDIV", k.pipe_lag_div)));
+        return k;
+    }
+};
+
+struct ScanShape {
+    const GroupDesc* groups = nullptr;   // sorted by rows, longest first
+    uint32_t n_groups = 0;
+    uint64_t padded_rows = 0;            // sum of the groups' padded rows
+    uint32_t n_tiles = 0;                // ceil(m / 32)
+    uint32_t n_tiles_narrow = 0;         // ceil(m / 8)
+    uint32_t sm_count = 0;
+    uint32_t warps_per_cta = 16;
+    bool s16 = true;                     // the packed int16 kernels scan (row blocks, narrow tiles, pipeline exist there only)
+    int policy = kScanAuto;
+    uint32_t pipe_rings = 0;             // chunks per ring that fit next to this query's profile (< 2: no pipeline)
+};
+
+struct ScanPlan {
+    uint32_t pipe_first = 0;   // groups [pipe_first, n_groups) go through the on-chip pipeline, [0, pipe_first) through the wavefront kernel
+    uint32_t wave_sms = 0;     // SMs the wavefront kernel gets
+    uint32_t n_units = 0;      // wavefront units
+    uint64_t vstate_slots = 0; // tiles of register state handed between row blocks
+    bool any_narrow = false, any_rowblock = false, chain_bound = false;
+    uint32_t n_split = 0, n_narrow = 0, n_rowblock = 0;   // groups per mode (the rest of [0, pipe_first) is single)
+    uint64_t wave_rows = 0;    // padded rows of the wavefront kernel's groups
+};
+
+// unit_start [n_groups + 1], vstate_off [n_groups], modes [n_groups] are filled for every group (pipeline groups: 0).
+inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* unit_start, uint32_t* vstate_off, uint8_t* modes) {
+    ScanPlan pl;
+    const uint32_t n_groups = in.n_groups, n_tiles = in.n_tiles;
+    auto rows_of = [&](uint32_t g) { return static_cast<uint64_t>(in.groups[g].n_chunks) * kRowsPerChunk; };
+    const uint32_t max_rows = n_groups ? static_cast<uint32_t>(rows_of(0)) : 0;
+
+    // ---- 1. which kernel ------------------------------------------------------------------------------------
+    pl.pipe_first = n_groups;
+    pl.wave_sms = in.sm_count;
+    pl.wave_rows = in.padded_rows;
+    const double fair_all = static_cast<double>(in.padded_rows) * n_tiles / (static_cast<double>(in.sm_count) * in.warps_per_cta);
+    pl.chain_bound = static_cast<double>(max_rows) > k.pipe_chain * fair_all;
+    const bool can_pipe = in.s16 && in.pipe_rings >= 2 && n_groups > 0;
+    if (can_pipe && in.policy == kScanPipeline) {
+        pl.pipe_first = 0;
+        pl.wave_sms = 0;
+        pl.wave_rows = 0;
+    } else if (can_pipe && in.policy == kScanAuto && k.pipe && n_tiles >= k.pipe_min_tiles && n_groups >= 2 * in.sm_count) {
+        const uint64_t fair_cta = in.padded_rows / in.sm_count;   // rows per CTA
+        const uint64_t tall = std::max<uint64_t>(256, static_cast<uint64_t>(k.pipe_tall * static_cast<double>(fair_cta)));
+        uint32_t g = 0;
+        uint64_t rows_wave = 0;
+        while (g < n_groups && rows_of(g) > tall) rows_wave += rows_of(g++);
+        pl.pipe_first = g;
+        pl.wave_rows = rows_wave;
+        if (g == 0) {
+            pl.wave_sms = 0;
+        } else {
+            const double share = static_cast<double>(rows_wave) / static_cast<double>(in.padded_rows);
+            const double margin = pl.chain_bound ? k.wave_margin_chain : k.wave_margin;
+            pl.wave_sms = static_cast<uint32_t>(std::ceil(share * margin * in.sm_count));
+            pl.wave_sms = std::max<uint32_t>(1, std::min<uint32_t>(pl.wave_sms, in.sm_count - 1));
+        }
+    }
+
+    // ---- 2. units of the wavefront kernel's groups [0, pipe_first) ---------------------------------------------
+    const uint32_t n_wave = pl.pipe_first;
+    const uint64_t total_row_tiles = pl.wave_rows * n_tiles;
+    const uint64_t warps = static_cast<uint64_t>(std::max<uint32_t>(pl.wave_sms, 1)) * in.warps_per_cta;
+    const uint64_t fair = total_row_tiles / warps;
+    // With plenty of groups per warp (a whole Swiss-Prot on one GPU: 3.7) only units larger than about three
+    // quarters of a warp's fair share need cutting -- LPT order fills the rest; a small shard with fewer groups
+    // than warps has to be cut finer to give every warp several units.
+    const double auto_fraction = std::min(0.75, std::max(0.08, static_cast<double>(n_wave) / (4.0 * static_cast<double>(warps))));
+    const double fraction = k.unit_budget > 0.0 ? k.unit_budget : auto_fraction;
+    const uint64_t budget = std::max<uint64_t>(2048, static_cast<uint64_t>(fraction * static_cast<double>(fair)));
+    const uint64_t narrow_rows = std::max<uint64_t>(2048, static_cast<uint64_t>(k.narrow_chain * static_cast<double>(fair)));
+    // Groups are sorted longest first: narrow tiles are needed iff the first group needs them.  The kernel variant
+    // that carries both extra paths spills registers in the common 32-column sweep (about 12 % slower), so a search
+    // that needs narrow tiles cuts its other large groups by rows only if cutting them by tile instead would waste
+    // more than that (small shards, long queries).
+    const bool narrow_needed = in.s16 && n_wave && in.n_tiles_narrow > 1 && rows_of(0) > narrow_rows;
+    bool row_blocks_ok = in.s16 && k.row_blocks;
+    auto split_shape = [&](uint32_t g, double* eff_tiles, double* eff_rows) {   // -> row blocks of >= 2 chunks, ~budget row-tiles each
+        const uint64_t chunks = in.groups[g].n_chunks, rows = rows_of(g), work = rows * n_tiles;
+        *eff_tiles = static_cast<double>(rows) / static_cast<double>(rows + 16 * (n_tiles - 1));
+        const uint64_t blocks = std::min<uint64_t>((work + budget - 1) / budget, std::max<uint64_t>(chunks / 2, 1));
+        *eff_rows = static_cast<double>(n_tiles) / static_cast<double>(n_tiles + blocks - 1);
+        return blocks;
+    };
+    if (row_blocks_ok && narrow_needed) {
+        double wasted = 0.0;   // extra warp time of tile-splitting where row blocks would have been chosen
+        for (uint32_t g = 0; g < n_wave; ++g) {
+            const uint64_t rows = rows_of(g), work = rows * n_tiles;
+            if (work <= budget || n_tiles < 2 || rows > narrow_rows) continue;
+            double eff_tiles, eff_rows;
+            const uint64_t blocks = split_shape(g, &eff_tiles, &eff_rows);
+            if (blocks >= 2 && eff_rows > eff_tiles) wasted += static_cast<double>(work) * (1.0 / eff_tiles - 1.0 / eff_rows);
+        }
+        row_blocks_ok = wasted > 0.12 * static_cast<double>(total_row_tiles);
+    }
+    for (uint32_t g = n_wave; g < n_groups; ++g) unit_start[g] = 0, vstate_off[g] = 0, modes[g] = kGroupSingle;
+    for (uint32_t g = 0; g < n_wave; ++g) {
+        unit_start[g] = pl.n_units;
+        vstate_off[g] = 0;
+        const uint64_t rows = rows_of(g), work = rows * n_tiles;
+        uint8_t mode = kGroupSingle;
+        uint32_t units = 1;
+        bool took_vstate = false;
+        if (work > budget && n_tiles > 1) {
+            mode = kGroupSplit;
+            units = n_tiles;
+            double eff_tiles, eff_rows;
+            const uint64_t blocks = split_shape(g, &eff_tiles, &eff_rows);
+            if (row_blocks_ok && blocks >= 2 && eff_rows > eff_tiles) {
+                mode = kGroupRowBlock;
+                units = static_cast<uint32_t>(blocks);
+                vstate_off[g] = static_cast<uint32_t>(pl.vstate_slots);
+                pl.vstate_slots += n_tiles;
+                took_vstate = true;
+            }
+        }
+        if (in.s16 && rows > narrow_rows && in.n_tiles_narrow > 1) {
+            if (took_vstate) pl.vstate_slots -= n_tiles;
+            mode = kGroupNarrow;
+            units = in.n_tiles_narrow;
+        }
+        modes[g] = mode;
+        pl.n_split += mode == kGroupSplit;
+        pl.n_narrow += mode == kGroupNarrow;
+        pl.n_rowblock += mode == kGroupRowBlock;
+        pl.n_units += units;
+    }
+    pl.any_narrow = pl.n_narrow > 0;
+    pl.any_rowblock = pl.n_rowblock > 0;
+    unit_start[n_wave] = pl.n_units;
+    for (uint32_t g = n_wave + 1; g <= n_groups; ++g) unit_start[g] = pl.n_units;
+    return pl;
+}
+
+// Capacity of each border ring (chunks, a power of two) that fits next to a profile of `prof_bytes` in
+// `smem_optin` bytes of shared memory; < 2: the pipeline cannot run.  fixed_bytes: the pipeline's control block.
+inline uint32_t ring_chunks_for(size_t prof_bytes, size_t smem_optin, size_t fixed_bytes, size_t ring_chunk_bytes_all_warps,
+                                uint32_t cap) {
+    const size_t fixed = ((prof_bytes + 255) & ~size_t(255)) + fixed_bytes;
+    if (fixed >= smem_optin) return 0;
+    const size_t room = (smem_optin - fixed) / ring_chunk_bytes_all_warps;
+    if (room < 1) return 0;
+    uint32_t c = 1;
+    while (c * 2 <= room && c * 2 <= cap) c *= 2;
+    return c;
+}
+
+// Row stride of the int8 profile: columns padded to whole 32-column tiles, then to 16 (mod 128) bytes so that the
+// 25 rows spread over the shared-memory banks.
+inline uint32_t profile_stride(uint32_t m, uint32_t tile) {
+    const uint32_t mpad = std::max<uint32_t>(tile, (m + tile - 1) / tile * tile);
+    return mpad + ((16 + 128 - (mpad % 128)) % 128);
+}
+
+}  // namespace swb

@@ -337,6 +337,18 @@ def shard_assignment(lengths, length_threshold: int, shard_count: int) -> np.nda
     return out[:len(lens)]
 
 
+def scan_plan(lengths, query_len: int, sm_count: int = 148, length_threshold: int = 3000, shard_rank: int = 0,
+              shard_count: int = 1, policy: int = 0) -> dict:
+    """How a search would be divided between the two scan kernels (swb_scan_plan; host only, no GPU needed)."""
+    lib = _cabi.load()
+    lens = np.ascontiguousarray(np.asarray(lengths, dtype=np.uint32))
+    info = _cabi.SwbScanPlanInfo()
+    rc = lib.swb_scan_plan(_ptr(lens, _u32p), len(lens), int(length_threshold) & (2 ** 64 - 1), shard_rank, shard_count,
+                           query_len, sm_count, policy, C.byref(info))
+    _raise(lib, rc)
+    return info.as_dict()
+
+
 def measure_pipe_rates(device: int = 0, seconds: float = 1.0) -> dict:
     lib = _cabi.load()
     r = _cabi.SwbPipeRates()

@@ -143,3 +143,52 @@ def test_cli_usage_and_exit_codes(lib, tmp_path):
     bad = tmp_path / "bad.fa"
     bad.write_text("ACGT\n")
     assert run("stats", "-d", str(bad)).returncode == 4                    # format error
+
+
+def _swissprot_lengths():
+    rng = np.random.Generator(np.random.PCG64(0x5357_4442_02))
+    return synth.random_lengths(rng, synth.SWISSPROT_SEQS, synth.SWISSPROT_RESIDUES, synth.SWISSPROT_MAXLEN)
+
+
+def test_scan_plan_divides_every_group_exactly_once(lib):
+    """The host-side division of a search between the two scan kernels (scan_plan.hpp, the GPU counterpart of
+    make_chunks + the two worker pools, scheduler.hpp:130-138,200-213): every group is on exactly one side, the
+    tall ones on the wavefront side, and its SM share follows its share of the rows."""
+    lens = _swissprot_lengths()
+    for m in (144, 257, 375, 1000, 2005, 5478):
+        p = search.scan_plan(lens, m)
+        assert p["pipeline_groups"] + p["wavefront_groups"] == p["n_groups"] == (len(lens) + 63) // 64
+        assert p["pipeline_rows"] + p["wavefront_rows"] >= int(lens.sum()) // 64     # padded rows cover the residues
+        assert p["n_tiles"] == (m + 31) // 32
+        if m < 257:                                   # fewer than 9 tiles: wavefront kernel only
+            assert p["pipeline_groups"] == 0 and p["wavefront_sms"] == 148
+        else:
+            assert p["pipeline_groups"] > 0.99 * p["n_groups"]
+            assert 0 < p["wavefront_groups"] < 64 and 1 <= p["wavefront_sms"] < 148
+            share = p["wavefront_rows"] / (p["wavefront_rows"] + p["pipeline_rows"])
+            margin = 2.0 if p["chain_bound"] else 1.25
+            assert p["wavefront_sms"] == int(np.ceil(share * margin * 148))
+            assert p["wavefront_units"] >= p["wavefront_groups"]
+    assert search.scan_plan(lens, 375)["chain_bound"] == 1 and search.scan_plan(lens, 2005)["chain_bound"] == 0
+    assert search.scan_plan(lens, 1000)["ring_chunks"] == 4 and search.scan_plan(lens, 5478)["ring_chunks"] == 2
+
+
+def test_scan_plan_policies_and_small_databases(lib):
+    lens = _swissprot_lengths()
+    forced = search.scan_plan(lens, 2005, policy=search.Database.SCAN_PIPELINE)
+    assert forced["pipeline_groups"] == forced["n_groups"] and forced["wavefront_units"] == 0
+    wave = search.scan_plan(lens, 2005, policy=search.Database.SCAN_WAVEFRONT)
+    assert wave["pipeline_groups"] == 0 and wave["wavefront_sms"] == 148 and wave["wavefront_units"] >= wave["n_groups"]
+    small = search.scan_plan(lens[:10_000], 2005)                      # 157 groups < 2 per SM
+    assert small["pipeline_groups"] == 0
+    huge = search.scan_plan(lens, 9000)                                # the profile leaves no room for the rings
+    assert huge["ring_chunks"] < 2 and huge["pipeline_groups"] == 0
+    assert search.scan_plan(lens, 9000, policy=search.Database.SCAN_PIPELINE)["pipeline_groups"] == 0
+    shard = search.scan_plan(lens, 2005, shard_rank=3, shard_count=8)  # 1/8 of the database: still hybrid
+    assert shard["n_groups"] in (1105, 1106) and shard["pipeline_groups"] > 0.9 * shard["n_groups"]
+    empty = search.scan_plan(np.zeros(0, np.uint32), 100)
+    assert empty["n_groups"] == 0
+    with pytest.raises(ValueError, match="shard_rank"):
+        search.scan_plan(lens, 100, shard_rank=2, shard_count=2)
+    with pytest.raises(ValueError, match="scan policy"):
+        search.scan_plan(lens, 100, policy=7)
