@@ -97,6 +97,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     uint32_t n_units = 0;
     uint32_t pipe_first = n_groups;   // groups [pipe_first, n_groups) go through the on-chip pipeline
     uint32_t wave_sms = static_cast<uint32_t>(db->sm_count);   // SMs the wavefront kernel gets
+    uint32_t wave_threads = kInterThreads;                      // and its CTA size
     const size_t prof_elems = static_cast<size_t>(kProfRows) * pl.pstride;
     const uint32_t pipe_rings = pipe_ring_chunks(db, prof_elems);
     bool any_narrow = false, any_rowblock = false;
@@ -119,6 +120,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         const ScanPlan sp = plan_scan(shape, scan_knobs(), us, vso, modes);
         pipe_first = sp.pipe_first;
         wave_sms = sp.wave_sms;
+        wave_threads = sp.wave_threads;
         n_units = sp.n_units;
         any_narrow = sp.any_narrow;
         any_rowblock = sp.any_rowblock;
@@ -231,7 +233,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.neg_open2 = pack16(-open);
         wp.neg_ext2 = pack16(-ext);
         const size_t smem = prof_elems;
-        const uint32_t warps_per_cta = pl.threads / 32;
+        const uint32_t warps_per_cta = wave_threads / 32;
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(wave_sms, (n_units + warps_per_cta - 1) / warps_per_cta));
         const bool in_smem = smem <= db->smem_optin;
         {
@@ -241,9 +243,9 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
             SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB>,       \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,                             \
                                           static_cast<int>(db->smem_optin)));                                      \
-            wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB><<<grid, kInterThreads, smem, s>>>(wp); \
+            wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB><<<grid, wave_threads, smem, s>>>(wp); \
         } else {                                                                                                   \
-            wavefront_s16_kernel<false, kInterTile, kInterThreads, NARROW, RB><<<grid, kInterThreads, 0, s>>>(wp); \
+            wavefront_s16_kernel<false, kInterTile, kInterThreads, NARROW, RB><<<grid, wave_threads, 0, s>>>(wp); \
         }                                                                                                          \
     }
             // the narrow-tile and row-block paths are only compiled into the variants that need them, so that the

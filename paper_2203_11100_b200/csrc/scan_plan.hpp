@@ -66,6 +66,10 @@ struct ScanKnobs {
                                      // busy for the whole search whatever their number: +15 % at m = 375, -2 % at m = 1000)
     uint32_t pipe_ring_cap = 4;      // SWB200_PIPE_RING: chunks per shared-memory ring at most (power of two)
     uint32_t pipe_lag_div = 24;      // SWB200_PIPE_LAGDIV: a tile starts group_chunks / this chunks behind its neighbour
+    double wave_thin = 4.0;          // SWB200_WAVE_THIN: next to the pipeline, the wavefront kernel runs 8 warps per SM instead of
+                                     // 16 when max_rows exceeds this x a warp's fair share of the search, and 4 warps beyond 1.5 x
+                                     // this: its SMs then hold little besides the longest group's chain, which runs faster with
+                                     // fewer warps per scheduler (1/8 Swiss-Prot, m = 1000: 8.3 -> 6.4 ms)
 
     static ScanKnobs from_env() {
         ScanKnobs k;
@@ -89,6 +93,7 @@ struct ScanKnobs {
         k.wave_margin_chain = num("SWB200_PIPE_WAVE_MARGIN_CHAIN", k.wave_margin_chain);
         k.pipe_ring_cap = std::max<uint32_t>(2, static_cast<uint32_t>(num("SWB200_PIPE_RING", k.pipe_ring_cap)));
         k.pipe_lag_div = std::max<uint32_t>(1, static_cast<uint32_t>(num("SWB200_PIPE_LAGDIV", k.pipe_lag_div)));
+        k.wave_thin = num("SWB200_WAVE_THIN", k.wave_thin);
         return k;
     }
 };
@@ -109,6 +114,7 @@ struct ScanShape {
 struct ScanPlan {
     uint32_t pipe_first = 0;   // groups [pipe_first, n_groups) go through the on-chip pipeline, [0, pipe_first) through the wavefront kernel
     uint32_t wave_sms = 0;     // SMs the wavefront kernel gets
+    uint32_t wave_threads = 512; // its CTA size
     uint32_t n_units = 0;      // wavefront units
     uint64_t vstate_slots = 0; // tiles of register state handed between row blocks
     bool any_narrow = false, any_rowblock = false, chain_bound = false;
@@ -155,7 +161,13 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
     // ---- 2. units of the wavefront kernel's groups [0, pipe_first) ---------------------------------------------
     const uint32_t n_wave = pl.pipe_first;
     const uint64_t total_row_tiles = pl.wave_rows * n_tiles;
-    const uint64_t warps = static_cast<uint64_t>(std::max<uint32_t>(pl.wave_sms, 1)) * in.warps_per_cta;
+    pl.wave_threads = in.warps_per_cta * 32;
+    if (pl.pipe_first < n_groups && pl.pipe_first > 0) {
+        const double chain = static_cast<double>(max_rows) / std::max(fair_all, 1.0);
+        if (chain >= 1.5 * k.wave_thin) pl.wave_threads = std::min<uint32_t>(pl.wave_threads, 128);
+        else if (chain >= k.wave_thin) pl.wave_threads = std::min<uint32_t>(pl.wave_threads, 256);
+    }
+    const uint64_t warps = static_cast<uint64_t>(std::max<uint32_t>(pl.wave_sms, 1)) * (pl.wave_threads / 32);
     const uint64_t fair = total_row_tiles / warps;
     // With plenty of groups per warp (a whole Swiss-Prot on one GPU: 3.7) only units larger than about three
     // quarters of a warp's fair share need cutting -- LPT order fills the rest; a small shard with fewer groups
