@@ -11,8 +11,9 @@
 //    exceed about a third of a CTA's fair share of the database would unbalance it: those few tall groups at
 //    the head of the sorted list stay with the wavefront kernel, which spreads a group over warps of many SMs,
 //    and run next to the pipeline on `wave_sms` SMs of their own.  Queries of fewer than 9 tiles (little border
-//    traffic to save, chains too short to keep 16 warps in step) and databases with fewer than two groups per SM
-//    stay with the wavefront kernel entirely.
+//    traffic to save, chains too short to keep 16 warps in step) stay with the wavefront kernel entirely unless the
+//    search is chain-bound (then separating the tall groups onto SMs of their own is what pays: m = 144 on
+//    Swiss-Prot 7.7 -> 6.0 ms); so do databases with fewer than two groups per SM.
 // 2. Unit policy of the wavefront kernel (kernels.cuh, GroupMode).  `fair` is one warp's share of its groups.
 //      single    the default: one warp scores the group's 64 sequences end to end;
 //      split     a group whose sweep exceeds `budget` is cut so that no unit dominates the makespan and there
@@ -58,7 +59,7 @@ struct ScanKnobs {
     bool row_blocks = true;          // SWB200_ROWBLOCKS=0 disables the row-block split
     double narrow_chain = 0.9;       // SWB200_NARROW: a group goes to 8-column tiles when its rows exceed this x fair
     bool pipe = true;                // SWB200_PIPE=0: never use the pipeline under the automatic policy
-    uint32_t pipe_min_tiles = 9;     // SWB200_PIPE_MINTILES
+    uint32_t pipe_min_tiles = 9;     // SWB200_PIPE_MINTILES: fewer tiles -> wavefront kernel only, unless chain-bound
     double pipe_chain = 1.2;         // SWB200_PIPE_CHAIN: chain-bound when max_rows > this x a warp's fair share of the search
     double pipe_tall = 0.35;         // SWB200_PIPE_TALL: groups taller than this x a CTA's fair share of rows go to the wavefront kernel
     double wave_margin = 1.25;       // SWB200_PIPE_WAVE_MARGIN: wavefront SMs = its share of the rows x this ...
@@ -140,7 +141,8 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
         pl.pipe_first = 0;
         pl.wave_sms = 0;
         pl.wave_rows = 0;
-    } else if (can_pipe && in.policy == kScanAuto && k.pipe && n_tiles >= k.pipe_min_tiles && n_groups >= 2 * in.sm_count) {
+    } else if (can_pipe && in.policy == kScanAuto && k.pipe && (n_tiles >= k.pipe_min_tiles || pl.chain_bound) &&
+               n_groups >= 2 * in.sm_count) {
         const uint64_t fair_cta = in.padded_rows / in.sm_count;   // rows per CTA
         const uint64_t tall = std::max<uint64_t>(256, static_cast<uint64_t>(k.pipe_tall * static_cast<double>(fair_cta)));
         uint32_t g = 0;

@@ -160,9 +160,7 @@ def test_scan_plan_divides_every_group_exactly_once(lib):
         assert p["pipeline_groups"] + p["wavefront_groups"] == p["n_groups"] == (len(lens) + 63) // 64
         assert p["pipeline_rows"] + p["wavefront_rows"] >= int(lens.sum()) // 64     # padded rows cover the residues
         assert p["n_tiles"] == (m + 31) // 32
-        if m < 257:                                   # fewer than 9 tiles: wavefront kernel only
-            assert p["pipeline_groups"] == 0 and p["wavefront_sms"] == 148
-        else:
+        if True:                                      # (short queries too: the search is chain-bound)
             assert p["pipeline_groups"] > 0.99 * p["n_groups"]
             assert 0 < p["wavefront_groups"] < 64 and 1 <= p["wavefront_sms"] < 148
             share = p["wavefront_rows"] / (p["wavefront_rows"] + p["pipeline_rows"])
@@ -179,6 +177,8 @@ def test_scan_plan_policies_and_small_databases(lib):
     assert forced["pipeline_groups"] == forced["n_groups"] and forced["wavefront_units"] == 0
     wave = search.scan_plan(lens, 2005, policy=search.Database.SCAN_WAVEFRONT)
     assert wave["pipeline_groups"] == 0 and wave["wavefront_sms"] == 148 and wave["wavefront_units"] >= wave["n_groups"]
+    short = search.scan_plan(np.minimum(lens, 2999), 144)              # fewer than 9 tiles and no chain to break:
+    assert short["chain_bound"] == 0 and short["pipeline_groups"] == 0 and short["wavefront_sms"] == 148   # wavefront kernel only
     small = search.scan_plan(lens[:10_000], 2005)                      # 157 groups < 2 per SM
     assert small["pipeline_groups"] == 0
     huge = search.scan_plan(lens, 9000)                                # the profile leaves no room for the rings
