@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libswb200.so"
 SOURCES = ["cabi.cu", "pack.cpp"]
-HEADERS = ["kernels.cuh", "pipeline.cuh", "scan_plan.hpp", "pipe_rates.cuh", "pack.hpp", "plan.inl", "handle.inl", "scan.inl", "persist.inl", "pairs.inl", "pipe.inl",
+HEADERS = ["kernels.cuh", "pipeline.cuh", "duo.cuh", "duo.inl", "scan_plan.hpp", "pipe_rates.cuh", "pack.hpp", "plan.inl", "handle.inl", "scan.inl", "persist.inl", "pairs.inl", "pipe.inl",
            "multi.inl"]
 
 NVCC_FLAGS = [

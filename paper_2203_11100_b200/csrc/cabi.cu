@@ -32,6 +32,7 @@
 #include "../../include/swb200.h"
 #include "kernels.cuh"
 #include "pipeline.cuh"
+#include "duo.cuh"
 #include "pack.hpp"
 #include "pipe_rates.cuh"
 #include "scan_plan.hpp"
@@ -132,6 +133,12 @@ struct swb_db {
     uint64_t* d_sort = nullptr;
     size_t sort_cap = 0;
     int32_t* d_all_scores = nullptr;
+    int32_t* d_slot_scores2 = nullptr;   // second query of a pair (duo.cuh)
+    uint32_t* d_prof2 = nullptr;
+    size_t prof2_cap = 0;
+    uint8_t* d_query2 = nullptr;
+    uint32_t query2_cap = 0;
+    bool duo_attr_set = false;
 
     // query side
     uint32_t query_cap = 0;
@@ -266,7 +273,7 @@ void swb_db_destroy(swb_db* db) {
         if (db->own_stream) cudaStreamSynchronize(db->own_stream);
         if (db->side_stream) cudaStreamSynchronize(db->side_stream);
         void* ptrs[] = {db->d_codes,      db->d_groups,   db->d_slot_index, db->d_slot_len,    db->d_border0,
-                        db->d_border1,    db->d_iborder0, db->d_iborder1,   db->d_slot_scores, db->d_flag_list,
+                        db->d_border1,    db->d_iborder0, db->d_iborder1, db->d_slot_scores2, db->d_prof2, db->d_query2,   db->d_slot_scores, db->d_flag_list,
                         db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_vstate_off, db->d_vstate, db->d_progress, db->d_keys,        db->d_sel[0],
                         db->d_sel[1],     db->d_sort,     db->d_all_scores, db->d_query,       db->d_matrix,
                         db->d_prof8,      db->d_prof8i,   db->d_prof32i};
@@ -354,6 +361,8 @@ swb_status swb_search_keys(swb_db* db, const uint8_t* query, uint32_t query_len,
     return SWB_OK;
 }
 
+#include "duo.inl"
+
 swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint32_t* query_lens, uint32_t n_queries,
                            const int32_t* matrix, int32_t gap_open, int32_t gap_extend, uint32_t top_k, swb_hit* hits,
                            uint32_t* n_hits, float* ms_per_query) {
@@ -371,34 +380,66 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
     const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint64_t>(n_keys, 1)));
     const size_t n_groups = db->meta.groups.size();
 
-    // one staging area per query (inputs up, keys + counters down), sized up front: the pinned buffer must not
+    // Queries of similar length share one scan (duo.cuh): walk the queries longest first and pair neighbours.
+    std::vector<uint32_t> order(n_queries);
+    for (uint32_t q = 0; q < n_queries; ++q) order[q] = q;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return query_lens[a] > query_lens[b]; });
+    struct Job {
+        uint32_t a, b;   // query numbers; b == a: a single-query scan
+    };
+    std::vector<Job> jobs;
+    for (uint32_t i = 0; i < n_queries; ++i) {
+        const uint32_t a = order[i];
+        if (i + 1 < n_queries && duo_applies(db, query_lens[a], query_lens[order[i + 1]], matrix, gap_open, gap_extend)) {
+            jobs.push_back(Job{a, order[i + 1]});
+            ++i;
+        } else {
+            jobs.push_back(Job{a, a});
+        }
+    }
+    std::sort(jobs.begin(), jobs.end(), [](const Job& x, const Job& y) { return std::min(x.a, x.b) < std::min(y.a, y.b); });
+
+    // one staging area per job (inputs up) and per query (keys down), sized up front: the pinned buffer must not
     // move while copies are in flight
-    std::vector<size_t> in_off(n_queries), out_off(n_queries);
+    std::vector<size_t> in_off(jobs.size()), out_off(n_queries);
     size_t total = 0;
+    for (size_t j = 0; j < jobs.size(); ++j) {
+        in_off[j] = total;
+        total += (576 * sizeof(int32_t) + query_lens[jobs[j].a] + query_lens[jobs[j].b] + 128 + (n_groups + 1) * 9 + 255) & ~size_t(255);
+    }
     for (uint32_t q = 0; q < n_queries; ++q) {
-        in_off[q] = total;
-        total += (576 * sizeof(int32_t) + query_lens[q] + 64 + (n_groups + 1) * 9 + 255) & ~size_t(255);
         out_off[q] = total;
         total += (static_cast<size_t>(k_eff) * sizeof(uint64_t) + 16 + 255) & ~size_t(255);
     }
     if ((st = ensure_stage(db, total)) != SWB_OK) return st;
-    while (db->many_events.size() < 2 * static_cast<size_t>(n_queries)) {
+    while (db->many_events.size() < 2 * jobs.size()) {
         cudaEvent_t ev;
         SWB_CUDA(cudaEventCreate(&ev));
         db->many_events.push_back(ev);
     }
-    // queries are issued back to back on the stream: the host prepares query q+1 (unit table, launches) while the
-    // GPU still scans query q, and nothing synchronises until the last one is in flight
-    for (uint32_t q = 0; q < n_queries && st == SWB_OK; ++q) {
-        db->stage_base = in_off[q];
-        cudaEventRecord(db->many_events[2 * q], s);
-        const uint64_t* d_top = nullptr;
-        st = search_keys_locked(db, queries[q], query_lens[q], matrix, gap_open, gap_extend, k_eff, &d_top);
-        if (st != SWB_OK) break;
-        if (cudaMemcpyAsync(db->h_stage + out_off[q], d_top, static_cast<size_t>(k_eff) * sizeof(uint64_t),
-                            cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    auto keys_down = [&](uint32_t q, const uint64_t* d_top) {
+        if (cudaMemcpyAsync(db->h_stage + out_off[q], d_top, static_cast<size_t>(k_eff) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess)
             st = fail(SWB_ERR_CUDA, "cudaMemcpyAsync failed");
-        cudaEventRecord(db->many_events[2 * q + 1], s);
+    };
+    // jobs are issued back to back on the stream: the host prepares the next one (unit table, launches) while the
+    // GPU still scans, and nothing synchronises until the last one is in flight
+    for (size_t j = 0; j < jobs.size() && st == SWB_OK; ++j) {
+        const uint32_t a = jobs[j].a, b = jobs[j].b;
+        db->stage_base = in_off[j];
+        cudaEventRecord(db->many_events[2 * j], s);
+        const uint64_t* d_top = nullptr;
+        if (a == b) {
+            st = search_keys_locked(db, queries[a], query_lens[a], matrix, gap_open, gap_extend, k_eff, &d_top);
+            if (st == SWB_OK) keys_down(a, d_top);
+        } else {
+            st = score_duo_core(db, queries[a], query_lens[a], queries[b], query_lens[b], matrix, gap_open, gap_extend);
+            if (st == SWB_OK) st = finish_duo_query(db, db->d_query, query_lens[a], matrix, gap_open, gap_extend, db->d_slot_scores, k_eff, &d_top);
+            if (st == SWB_OK) keys_down(a, d_top);
+            if (st == SWB_OK) st = finish_duo_query(db, db->d_query2, query_lens[b], matrix, gap_open, gap_extend, db->d_slot_scores2, k_eff, &d_top);
+            if (st == SWB_OK) keys_down(b, d_top);
+        }
+        cudaEventRecord(db->many_events[2 * j + 1], s);
     }
     db->stage_base = 0;
     const cudaError_t sync = cudaStreamSynchronize(s);
@@ -412,8 +453,21 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
             hits[static_cast<size_t>(q) * top_k + cnt].score = static_cast<int32_t>(keys[i] >> 32);
         }
         n_hits[q] = cnt;
-        if (ms_per_query) cudaEventElapsedTime(&ms_per_query[q], db->many_events[2 * q], db->many_events[2 * q + 1]);
     }
+    if (ms_per_query)
+        for (size_t j = 0; j < jobs.size(); ++j) {
+            // a shared scan's time is split between its two queries in proportion to their lengths
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, db->many_events[2 * j], db->many_events[2 * j + 1]);
+            const uint32_t a = jobs[j].a, b = jobs[j].b;
+            if (a == b) {
+                ms_per_query[a] = ms;
+            } else {
+                const float la = static_cast<float>(query_lens[a]), lb = static_cast<float>(query_lens[b]);
+                ms_per_query[a] = ms * la / (la + lb);
+                ms_per_query[b] = ms * lb / (la + lb);
+            }
+        }
     return SWB_OK;
 }
 

@@ -1,0 +1,234 @@
+// duo.cuh -- the on-chip tile pipeline for TWO queries at once.
+//
+// pipeline_s16_kernel packs two database sequences into the int16 halves of every DPX word; the two halves then
+// need two different profile rows (one per residue), and one PRMT per pair of cells stitches the two int8
+// entries into a substitution word: 4.5 ALU-pipe instructions per two cells, the pipe that bounds the kernel.
+// Here the halves are two QUERIES against the same sequence: same residue, same column, so the profile can hold
+// the finished s16x2 word (query A's entry in the low half, query B's in the high half) and the PRMT disappears:
+// 3.5 ALU-pipe instructions per two cells.  A thread now carries one sequence; an item is one half (32 sequences)
+// of an interleaved group of 64.
+//
+// Everything else is pipeline.cuh's design: slot stream over a CTA's 16 warps, border rings in shared memory, the
+// link into warp 0 through global memory for queries of more than 16 tiles, items by ticket.  One difference: the
+// 4-byte profile of a long query does not fit shared memory, so each warp keeps only the slice of its current tile
+// (25 rows x 32 columns, 3.6 KB) and reloads it at every slot start; shared-memory use no longer depends on m.
+//
+// Used by swb_search_many for pairs of queries of similar length (the shorter one is padded with zero-score
+// columns, which cannot raise a score).
+#pragma once
+#include "pipeline.cuh"
+
+namespace swb {
+
+constexpr uint32_t kDuoRowWords = kInterTile + 4;                 // 36 words = 144 B: rows 16 B apart modulo 128
+constexpr uint32_t kDuoSliceWords = kProfRows * kDuoRowWords;     // one tile's profile slice: 900 words
+constexpr uint32_t kDuoSliceBytes = (kDuoSliceWords * 4 + 255) & ~255u;
+
+// prof2[tile][symbol][36]: word c = (M[s][qa[j]] + open) | (M[s][qb[j]] + open) << 16, j = tile * 32 + c; pad rows,
+// pad columns (past either query's end) and the 4 filler words carry `open` (substitution score 0).
+struct DuoProfileParams {
+    const uint8_t* qa;
+    const uint8_t* qb;
+    uint32_t ma, mb;
+    const int32_t* matrix;
+    int32_t shift;
+    uint32_t n_tiles;
+    uint32_t* prof2;
+};
+
+__global__ void build_duo_profile_kernel(DuoProfileParams p) {
+    const uint32_t total = p.n_tiles * kDuoSliceWords;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t tile = i / kDuoSliceWords, rem = i % kDuoSliceWords;
+        const uint32_t s = rem / kDuoRowWords, c = rem % kDuoRowWords;
+        const uint32_t j = tile * kInterTile + c;
+        int32_t va = p.shift, vb = p.shift;
+        if (s < kAlphabet && c < kInterTile) {
+            if (j < p.ma) va += p.matrix[s * kAlphabet + p.qa[j]];
+            if (j < p.mb) vb += p.matrix[s * kAlphabet + p.qb[j]];
+        }
+        p.prof2[i] = (static_cast<uint32_t>(va) & 0xffffu) | (static_cast<uint32_t>(vb) << 16);
+    }
+}
+
+struct DuoParams {
+    const uint4* codes;
+    const GroupDesc* groups;
+    uint32_t n_items;         // 2 x groups: item i = half (i & 1) of group (i >> 1), longest first
+    const uint32_t* prof2;
+    uint32_t n_tiles;         // ceil(max(ma, mb) / 32)
+    uint32_t ring_chunks;
+    uint32_t lag_div;
+    uint2* border0;           // database-shaped border rows for the link into warp 0: half 0 / half 1 of a group
+    uint2* border1;
+    int32_t* scores_a;        // per slot, zeroed per search, updated with atomicMax
+    int32_t* scores_b;
+    uint32_t* ticket;
+    uint32_t neg_open2, neg_ext2;
+};
+
+template <int T, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) {
+    static_assert(T == 32, "the slice layout assumes 32-column tiles");
+    extern __shared__ __align__(256) uint8_t smem[];
+    PipeCtl* ctl = reinterpret_cast<PipeCtl*>(smem);
+    uint8_t* slices = smem + sizeof(PipeCtl);
+    uint8_t* rings = slices + kPipeWarps * kDuoSliceBytes;
+    {
+        uint32_t* c = reinterpret_cast<uint32_t*>(ctl);
+        for (uint32_t i = threadIdx.x; i < sizeof(PipeCtl) / 4; i += kThreads) c[i] = 0;
+        __syncthreads();
+    }
+
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t next = (warp + 1) % kPipeWarps;
+    const bool wrap = p.n_tiles > kPipeWarps;
+    const bool wrap_in = wrap && warp == 0, wrap_out = wrap && next == 0;
+    const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
+    const uint32_t ring_mask = p.ring_chunks - 1;
+    const uint32_t ring_bytes = p.ring_chunks * kPipeChunkBytes;
+    const uint8_t* ring_in = rings + warp * ring_bytes + lane * 8;
+    const uint32_t ring_stage = static_cast<uint32_t>(__cvta_generic_to_shared(rings)) + lane * 16;
+    uint8_t* ring_out = rings + next * ring_bytes + lane * 8;
+    uint32_t* const slice = reinterpret_cast<uint32_t*>(slices + warp * kDuoSliceBytes);
+    uint32_t in_pos = 0, out_pos = 0;
+
+    // pipe_item() hands out tickets against n_items / group_first of a PipeParams
+    PipeParams tickets{};
+    tickets.n_items = p.n_items;
+    tickets.group_first = 0;
+    tickets.ticket = p.ticket;
+
+    for (uint32_t slot = warp;; slot += kPipeWarps) {
+        const uint32_t item = slot / p.n_tiles, tile = slot - item * p.n_tiles;
+        const uint32_t it = pipe_item(tickets, ctl, item, lane);
+        if (it == kPipeEnd) break;
+        if (lane == 0) ctl->warp_item[warp] = item;
+        const uint32_t half = it & 1;
+        const GroupDesc gd = p.groups[it >> 1];
+        const bool first = tile == 0, last = tile + 1 == p.n_tiles;
+        const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
+        uint2* const gb = (half ? p.border1 : p.border0) + gd.chunk_base * kRowsPerChunk * 32;
+        uint8_t* gborder = reinterpret_cast<uint8_t*>(gb + lane);
+        const uint8_t* gstage = reinterpret_cast<const uint8_t*>(gb) + lane * 16;
+        const uint32_t in_end = in_pos + gd.n_chunks;
+        const uint32_t lag = max(1u, min(p.ring_chunks - 1, gd.n_chunks / p.lag_div));
+
+        // this tile's profile slice -> the warp's private shared-memory copy
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(p.prof2 + static_cast<size_t>(tile) * kDuoSliceWords);
+            uint4* dst = reinterpret_cast<uint4*>(slice);
+            __syncwarp();
+            for (uint32_t i = lane; i < kDuoSliceWords / 4; i += 32) dst[i] = __ldg(src + i);
+            __syncwarp();
+        }
+
+        uint32_t Hm[T], F[T];
+#pragma unroll
+        for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
+        uint32_t diag_in = NO, best = 0;
+        uint4 cw = __ldg(gcodes);
+        const uint32_t in_base = in_pos;
+        uint32_t staged = in_pos;
+
+        for (uint32_t chunk = 0; chunk < gd.n_chunks; ++chunk) {
+            const uint4 cur = cw;
+            if (chunk + 1 < gd.n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
+            if (!first) {
+                if (wrap_in) {
+                    if (staged == in_pos) {
+                        const uint32_t need = min(in_pos + 2, in_end);
+                        while (lds_acquire(&ctl->head[0]) < need) __nanosleep(20);
+                        stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
+                                    gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
+                        ++staged;
+                    }
+                    asm volatile("cp.async.wait_all;" ::: "memory");
+                    __syncwarp();
+                    if (staged < in_end && lds_acquire(&ctl->head[0]) > staged) {
+                        stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
+                                    gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
+                        ++staged;
+                    }
+                } else {
+                    const uint32_t need = min(chunk == 0 ? in_pos + lag : in_pos + 1, in_end);
+                    while (lds_acquire(&ctl->head[warp]) < need) __nanosleep(20);
+                }
+            }
+            if (!last && !wrap_out)
+                while (out_pos - lds_acquire(&ctl->tail[next]) >= p.ring_chunks) __nanosleep(20);
+            const uint2* bin = reinterpret_cast<const uint2*>(ring_in + (in_pos & ring_mask) * kPipeChunkBytes);
+            uint8_t* bout = wrap_out ? gborder + static_cast<size_t>(chunk) * kPipeChunkBytes
+                                     : ring_out + (out_pos & ring_mask) * kPipeChunkBytes;
+            uint2 bnext = make_uint2(NO, NO);
+            if (!first) bnext = bin[0];
+            const uint32_t r_lo = half ? cur.z : cur.x, r_hi = half ? cur.w : cur.y;   // this half's 8 residues
+#pragma unroll
+            for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
+                const uint32_t a = ((r < 4 ? r_lo : r_hi) >> (8 * (r & 3))) & 0xffu;
+                const uint4* prow = reinterpret_cast<const uint4*>(slice + a * kDuoRowWords);
+                const uint2 bi = bnext;
+                if (!first && r + 1 < static_cast<int>(kRowsPerChunk)) bnext = bin[(r + 1) * 32];
+                uint32_t hl = bi.x, E = bi.y;
+                uint4 sw = prow[0];
+                uint32_t d = __vadd2(diag_in, sw.x);
+                diag_in = hl;
+#pragma unroll
+                for (int k = 0; k < T; k += 4) {
+                    const uint4 sn = k + 4 < T ? prow[k / 4 + 1] : sw;   // the next four columns' substitution words
+                    // column k
+                    E = __viaddmax_s16x2(E, NE, hl);
+                    F[k] = __viaddmax_s16x2(F[k], NE, Hm[k]);
+                    const uint32_t d0 = d;
+                    const uint32_t d1 = __vadd2(Hm[k], sw.y);
+                    hl = __vadd2(__vimax3_s16x2_relu(d0, E, F[k]), NO);
+                    Hm[k] = hl;
+                    // column k + 1
+                    E = __viaddmax_s16x2(E, NE, hl);
+                    F[k + 1] = __viaddmax_s16x2(F[k + 1], NE, Hm[k + 1]);
+                    const uint32_t d2 = __vadd2(Hm[k + 1], sw.z);
+                    hl = __vadd2(__vimax3_s16x2_relu(d1, E, F[k + 1]), NO);
+                    Hm[k + 1] = hl;
+                    best = __vimax3_s16x2(best, d0, d1);
+                    // column k + 2
+                    E = __viaddmax_s16x2(E, NE, hl);
+                    F[k + 2] = __viaddmax_s16x2(F[k + 2], NE, Hm[k + 2]);
+                    const uint32_t d3 = __vadd2(Hm[k + 2], sw.w);
+                    hl = __vadd2(__vimax3_s16x2_relu(d2, E, F[k + 2]), NO);
+                    Hm[k + 2] = hl;
+                    // column k + 3
+                    E = __viaddmax_s16x2(E, NE, hl);
+                    F[k + 3] = __viaddmax_s16x2(F[k + 3], NE, Hm[k + 3]);
+                    if (k + 4 < T) d = __vadd2(Hm[k + 3], sn.x);
+                    hl = __vadd2(__vimax3_s16x2_relu(d3, E, F[k + 3]), NO);
+                    Hm[k + 3] = hl;
+                    best = __vimax3_s16x2(best, d2, d3);
+                    sw = sn;
+                }
+                if (!last) *reinterpret_cast<uint2*>(bout + r * 256) = make_uint2(hl, E);
+            }
+            __syncwarp();
+            if (!first) {
+                ++in_pos;
+                if (lane == 0 && !wrap_in) sts_release(&ctl->tail[warp], in_pos);
+            }
+            if (!last) {
+                ++out_pos;
+                if (lane == 0) {
+                    if (wrap_out) __threadfence();
+                    sts_release(&ctl->head[next], out_pos);
+                }
+            }
+        }
+
+        // halves -> the two queries' scores of this lane's sequence
+        const int32_t sa = static_cast<int32_t>(best & 0xffffu);
+        const int32_t sb = static_cast<int32_t>(best >> 16);
+        const uint32_t sl = gd.first_slot + half * 32 + lane;
+        if (sa) atomicMax(p.scores_a + sl, sa);
+        if (sb) atomicMax(p.scores_b + sl, sb);
+    }
+    if (lane == 0) ctl->warp_item[warp] = kPipeEnd;
+}
+
+}  // namespace swb

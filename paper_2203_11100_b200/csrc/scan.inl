@@ -18,7 +18,7 @@ void launch_intra_t(uint32_t t, const IntraParams& ip, uint32_t ctas, uint32_t w
 }
 
 // Launch the int32 intra-task kernel over `list` (nullptr = every slot).
-swb_status run_intra(swb_db* db, const QueryPlan& pl, const uint32_t* list, cudaStream_t s) {
+swb_status run_intra(swb_db* db, const QueryPlan& pl, const uint32_t* list, cudaStream_t s, int32_t* slot_scores = nullptr) {
     swb_status st;
     if (!db->intra_ctas) {
         // per-CTA border rows are only touched when the query needs more than one pass, but the
@@ -44,7 +44,7 @@ swb_status run_intra(swb_db* db, const QueryPlan& pl, const uint32_t* list, cuda
     ip.border0 = db->d_iborder0;
     ip.border1 = db->d_iborder1;
     ip.border_rows = std::max<uint32_t>(db->max_rows, 1);
-    ip.slot_scores = db->d_slot_scores;
+    ip.slot_scores = slot_scores ? slot_scores : db->d_slot_scores;
     ip.open = pl.open;
     ip.ext = pl.ext;
     if (pl.wide) launch_intra_t<int32_t>(pl.intra_t, ip, db->intra_ctas, pl.intra_w, s);

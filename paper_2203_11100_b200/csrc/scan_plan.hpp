@@ -67,6 +67,9 @@ struct ScanKnobs {
                                      // busy for the whole search whatever their number: +15 % at m = 375, -2 % at m = 1000)
     uint32_t pipe_ring_cap = 4;      // SWB200_PIPE_RING: chunks per shared-memory ring at most (power of two)
     uint32_t pipe_lag_div = 24;      // SWB200_PIPE_LAGDIV: a tile starts group_chunks / this chunks behind its neighbour
+    double duo_ratio = 0.75;         // SWB200_DUO: swb_search_many scans two queries at once (duo.cuh) when the shorter one has
+                                     // at least this fraction of the longer one's length (the two-query kernel is ~15 % faster
+                                     // per padded cell: below 0.74 the padding eats the gain); > 1: never
     double wave_thin = 4.0;          // SWB200_WAVE_THIN: next to the pipeline, the wavefront kernel runs 8 warps per SM instead of
                                      // 16 when max_rows exceeds this x a warp's fair share of the search, and 4 warps beyond 1.5 x
                                      // this: its SMs then hold little besides the longest group's chain, which runs faster with
@@ -95,6 +98,7 @@ struct ScanKnobs {
         k.pipe_ring_cap = std::max<uint32_t>(2, static_cast<uint32_t>(num("SWB200_PIPE_RING", k.pipe_ring_cap)));
         k.pipe_lag_div = std::max<uint32_t>(1, static_cast<uint32_t>(num("SWB200_PIPE_LAGDIV", k.pipe_lag_div)));
         k.wave_thin = num("SWB200_WAVE_THIN", k.wave_thin);
+        k.duo_ratio = num("SWB200_DUO", k.duo_ratio);
         return k;
     }
 };

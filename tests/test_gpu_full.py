@@ -81,6 +81,37 @@ def test_sampled_score_parity_through_the_pipeline(full, port, b62):
     assert (got == alone).all()
 
 
+def test_batched_sweep_equals_single_searches(full, b62):
+    """swb_search_many over the whole 20-query sweep (queries of similar length share one scan through the
+    two-query kernel, the rest go one by one): every ranked list equals the one swb_search returns."""
+    queries, sdb, db = full
+    many, ms = db.search_many(queries, b62, GapModel(10, 2), 10)
+    assert len(many) == len(queries) and (ms > 0).all()
+    for qi, q in enumerate(queries):
+        idx, sc, _ = db.search(q, b62, GapModel(10, 2), 10)
+        assert (many[qi][0] == idx).all() and (many[qi][1] == sc).all(), f"query {qi} (m={len(q)})"
+        assert idx[0] == sdb.planted[qi][0]
+    again, _ = db.search_many(queries[::-1], b62, GapModel(10, 2), 10)      # other order, other pairing
+    for (i1, s1), (i2, s2) in zip(many, again[::-1]):
+        assert (i1 == i2).all() and (s1 == s2).all()
+
+
+def test_two_query_scan_with_overflow(port):
+    """BLOSUM50 12/2 with two long queries whose planted copies leave the int16 range: the shared scan flags them
+    and each query's flagged lanes come back exact from the int32 re-run."""
+    b50 = synth.blosum50()
+    queries = synth.make_queries([7600, 8000], seed=56)
+    sdb = synth.make_database(30_000, target_residues=9_000_000, max_len=9000, queries=queries, seed=56)
+    g = GapModel(12, 2)
+    with Database(sdb.codes, sdb.offsets) as db:
+        many, _ = db.search_many(queries, b50, g, 8)
+        for qi, q in enumerate(queries):
+            idx, sc, st = db.search(q, b50, g, 8)
+            assert (many[qi][0] == idx).all() and (many[qi][1] == sc).all()
+            assert idx[0] == sdb.planted[qi][0] and sc[0] > 32767 and st["rescored_i32"] >= 1
+            assert sc[0] == port.score_scalar(q, q, b50, 12, 2)
+
+
 def test_sharded_full_database(full, b62):
     queries, sdb, db = full
     q = queries[6]
