@@ -92,7 +92,7 @@ typedef struct swb_db_info {
     uint64_t device_bytes;     /* HBM held by this handle (database + work buffers)               */
     uint64_t length_threshold;
     int32_t device;
-    int32_t reserved;
+    uint32_t kernel_launches_total;  /* kernels this handle has launched so far (searches and re-runs; wraps) */
 } swb_db_info;
 
 const char* swb_last_error(void);

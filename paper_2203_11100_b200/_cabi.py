@@ -42,7 +42,7 @@ class SwbDbInfo(C.Structure):
         ("n_groups", C.c_uint32), ("max_length", C.c_uint32), ("shard_rank", C.c_uint32),
         ("shard_count", C.c_uint32), ("residues", C.c_uint64), ("padded_residues", C.c_uint64),
         ("device_bytes", C.c_uint64), ("length_threshold", C.c_uint64), ("device", C.c_int32),
-        ("reserved", C.c_int32),
+        ("kernel_launches_total", C.c_uint32),
     ]
 
     def as_dict(self):

@@ -154,7 +154,8 @@ struct swb_db {
     std::vector<cudaEvent_t> many_events;   // per-query start/end events of swb_search_many
     uint32_t* h_counters = nullptr;   // pinned copy of d_counters
     cudaEvent_t ev[EV_COUNT] = {};
-    uint32_t launches = 0;
+    uint32_t launches = 0;        // of the current search
+    uint32_t launches_total = 0;  // of all earlier ones
     uint32_t last_units = 0;
     uint32_t last_tile = kInterTile;
     std::vector<uint32_t> slot_of;   // db_index -> slot (built on the first traceback request)
@@ -308,6 +309,7 @@ swb_status swb_db_info_get(const swb_db* db, swb_db_info* info) {
     info->device_bytes = db->device_bytes;
     info->length_threshold = db->meta.length_threshold;
     info->device = db->device;
+    info->kernel_launches_total = db->launches_total + db->launches;
     return SWB_OK;
 }
 

@@ -11,6 +11,7 @@ swb_status score_duo_core(swb_db* db, const uint8_t* qa, uint32_t ma, const uint
     const uint32_t m = std::max(ma, mb);
     const uint32_t n_tiles = (m + kInterTile - 1) / kInterTile;
     const uint32_t n_groups = static_cast<uint32_t>(db->meta.groups.size());
+    db->launches_total += db->launches;
     db->launches = 0;
     db->last_tile = kInterTile;
     if (!db->d_slot_scores2)

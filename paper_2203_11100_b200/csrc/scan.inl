@@ -58,6 +58,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
                       int32_t ext) {
     cudaStream_t s = db->stream;
     const QueryPlan pl = make_plan(db, m, matrix, open, ext);
+    db->launches_total += db->launches;
     db->launches = 0;
     db->last_units = 0;
     db->last_tile = pl.tile;
