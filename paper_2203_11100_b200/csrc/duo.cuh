@@ -163,14 +163,21 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
             uint2 bnext = make_uint2(NO, NO);
             if (!first) bnext = bin[0];
             const uint32_t r_lo = half ? cur.z : cur.x, r_hi = half ? cur.w : cur.y;   // this half's 8 residues
+            // a row's first four substitution words are loaded while the previous row is computed
+            const uint4* prow_next = reinterpret_cast<const uint4*>(slice + (r_lo & 0xffu) * kDuoRowWords);
+            uint4 sw_next = prow_next[0];
 #pragma unroll
             for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
-                const uint32_t a = ((r < 4 ? r_lo : r_hi) >> (8 * (r & 3))) & 0xffu;
-                const uint4* prow = reinterpret_cast<const uint4*>(slice + a * kDuoRowWords);
+                const uint4* prow = prow_next;
+                uint4 sw = sw_next;
+                if (r + 1 < static_cast<int>(kRowsPerChunk)) {
+                    const uint32_t an = (((r + 1) < 4 ? r_lo : r_hi) >> (8 * ((r + 1) & 3))) & 0xffu;
+                    prow_next = reinterpret_cast<const uint4*>(slice + an * kDuoRowWords);
+                    sw_next = prow_next[0];
+                }
                 const uint2 bi = bnext;
                 if (!first && r + 1 < static_cast<int>(kRowsPerChunk)) bnext = bin[(r + 1) * 32];
                 uint32_t hl = bi.x, E = bi.y;
-                uint4 sw = prow[0];
                 uint32_t d = __vadd2(diag_in, sw.x);
                 diag_in = hl;
 #pragma unroll

@@ -229,20 +229,30 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
                                      : ring_out + (out_pos & ring_mask) * kPipeChunkBytes;
             uint2 bnext = make_uint2(NO, NO);
             if (!first) bnext = bin[0];
+            // the first 16 columns' profile bytes of a row are loaded while the previous row is computed
+            const int8_t* pa_next = ptile + (cur.x & 0xffu) * p.pstride;
+            const int8_t* pb_next = ptile + (cur.z & 0xffu) * p.pstride;
+            uint4 va_next = *reinterpret_cast<const uint4*>(pa_next), vb_next = *reinterpret_cast<const uint4*>(pb_next);
 #pragma unroll
             for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
-                const uint32_t wa = r < 4 ? cur.x : cur.y;
-                const uint32_t wb = r < 4 ? cur.z : cur.w;
-                const uint32_t a1 = (wa >> (8 * (r & 3))) & 0xffu;
-                const uint32_t a2 = (wb >> (8 * (r & 3))) & 0xffu;
-                const int8_t* pa = ptile + a1 * p.pstride;
-                const int8_t* pb = ptile + a2 * p.pstride;
+                const int8_t* pa = pa_next;
+                const int8_t* pb = pb_next;
                 uint32_t wA[T / 4], wB[T / 4];
+                wA[0] = va_next.x, wA[1] = va_next.y, wA[2] = va_next.z, wA[3] = va_next.w;
+                wB[0] = vb_next.x, wB[1] = vb_next.y, wB[2] = vb_next.z, wB[3] = vb_next.w;
 #pragma unroll
-                for (int i = 0; i < T / 16; ++i) {
+                for (int i = 1; i < T / 16; ++i) {
                     const uint4 va = reinterpret_cast<const uint4*>(pa)[i], vb = reinterpret_cast<const uint4*>(pb)[i];
                     wA[4 * i] = va.x, wA[4 * i + 1] = va.y, wA[4 * i + 2] = va.z, wA[4 * i + 3] = va.w;
                     wB[4 * i] = vb.x, wB[4 * i + 1] = vb.y, wB[4 * i + 2] = vb.z, wB[4 * i + 3] = vb.w;
+                }
+                if (r + 1 < static_cast<int>(kRowsPerChunk)) {
+                    const uint32_t wa = r + 1 < 4 ? cur.x : cur.y;
+                    const uint32_t wb = r + 1 < 4 ? cur.z : cur.w;
+                    pa_next = ptile + ((wa >> (8 * ((r + 1) & 3))) & 0xffu) * p.pstride;
+                    pb_next = ptile + ((wb >> (8 * ((r + 1) & 3))) & 0xffu) * p.pstride;
+                    va_next = *reinterpret_cast<const uint4*>(pa_next);
+                    vb_next = *reinterpret_cast<const uint4*>(pb_next);
                 }
                 const uint2 bi = bnext;   // this row's inbound border, loaded while the previous row was computed
                 if (!first && r + 1 < static_cast<int>(kRowsPerChunk)) bnext = bin[(r + 1) * 32];
