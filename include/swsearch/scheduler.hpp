@@ -140,6 +140,41 @@ inline std::vector<WorkChunk> make_chunks(std::size_t pool_size, std::size_t chu
 
 }  // namespace detail
 
+namespace detail {
+
+/// Tracebacks of all surviving hits, on the GPU, straight from the resident database (scheduler.hpp:246-249).
+inline void attach_alignments(const EncodedSequence& query, const SequenceDatabase& db, const ScoringMatrix& matrix,
+                              const GapModel& gaps, const SearchConfig& config, swb_mdb* resident, RankedResults& results) {
+    if (config.compute_alignments && !results.hits.empty()) {
+        // all surviving hits are traced back on the GPU in one go, straight from the resident database
+        const std::size_t count = results.hits.size();
+        std::vector<swb_hit> raw_hits(count);
+        std::vector<std::uint64_t> offsets(count + 1, 0);
+        for (std::size_t i = 0; i < count; ++i) {
+            raw_hits[i] = swb_hit{results.hits[i].db_index, results.hits[i].score.value};
+            offsets[i + 1] = offsets[i] + query.length() + db.sequences[results.hits[i].db_index].length();
+        }
+        std::vector<swb_alignment> raw(count);
+        std::vector<std::uint8_t> scripts(std::max<std::uint64_t>(offsets[count], 1));
+        gpu::check(swb_mdb_align_hits(resident, query.codes.data(), static_cast<std::uint32_t>(query.length()),
+                                      gpu::matrix_table(matrix), gaps.open(), gaps.extend(), raw_hits.data(),
+                                      static_cast<std::uint32_t>(count), config.traceback_memory_cap, raw.data(),
+                                      scripts.data(), offsets.data()));
+        for (std::size_t i = 0; i < count; ++i) {
+            Alignment a;
+            a.score = {raw[i].score};
+            a.capped = raw[i].capped != 0;
+            a.query_begin = raw[i].query_begin, a.query_end = raw[i].query_end;
+            a.subject_begin = raw[i].subject_begin, a.subject_end = raw[i].subject_end;
+            a.ops.resize(raw[i].n_ops);
+            for (std::size_t k = 0; k < a.ops.size(); ++k) a.ops[k] = static_cast<EditOp>(scripts[offsets[i] + k]);
+            results.hits[i].alignment = std::move(a);
+        }
+    }
+}
+
+}  // namespace detail
+
 /// Search one query against the whole database on the GPUs.
 inline RankedResults run_search(const EncodedSequence& query, const SequenceDatabase& db, const ScoringMatrix& matrix,
                                 const GapModel& gaps, const SearchConfig& config, SearchStats* stats = nullptr) {
@@ -169,33 +204,57 @@ inline RankedResults run_search(const EncodedSequence& query, const SequenceData
         }
     }
 
-    if (config.compute_alignments && !results.hits.empty()) {
-        // all surviving hits are traced back on the GPU in one go, straight from the resident database
-        const std::size_t count = results.hits.size();
-        std::vector<swb_hit> raw_hits(count);
-        std::vector<std::uint64_t> offsets(count + 1, 0);
-        for (std::size_t i = 0; i < count; ++i) {
-            raw_hits[i] = swb_hit{results.hits[i].db_index, results.hits[i].score.value};
-            offsets[i + 1] = offsets[i] + query.length() + db.sequences[results.hits[i].db_index].length();
-        }
-        std::vector<swb_alignment> raw(count);
-        std::vector<std::uint8_t> scripts(std::max<std::uint64_t>(offsets[count], 1));
-        gpu::check(swb_mdb_align_hits(resident, query.codes.data(), static_cast<std::uint32_t>(query.length()),
-                                      gpu::matrix_table(matrix), gaps.open(), gaps.extend(), raw_hits.data(),
-                                      static_cast<std::uint32_t>(count), config.traceback_memory_cap, raw.data(),
-                                      scripts.data(), offsets.data()));
-        for (std::size_t i = 0; i < count; ++i) {
-            Alignment a;
-            a.score = {raw[i].score};
-            a.capped = raw[i].capped != 0;
-            a.query_begin = raw[i].query_begin, a.query_end = raw[i].query_end;
-            a.subject_begin = raw[i].subject_begin, a.subject_end = raw[i].subject_end;
-            a.ops.resize(raw[i].n_ops);
-            for (std::size_t k = 0; k < a.ops.size(); ++k) a.ops[k] = static_cast<EditOp>(scripts[offsets[i] + k]);
-            results.hits[i].alignment = std::move(a);
-        }
-    }
+    detail::attach_alignments(query, db, matrix, gaps, config, resident, results);
     return results;
+}
+
+/// Several queries against the same database: the same results as a loop over run_search (which is what the
+/// reference's callers write), but issued to the GPU as one batch -- searches overlap each other's
+/// host preparation, and queries of similar length share one database scan (swb_search_many).  With the database
+/// sharded over several GPUs this falls back to the loop.
+inline std::vector<RankedResults> run_search_batch(const std::vector<EncodedSequence>& queries, const SequenceDatabase& db,
+                                                   const ScoringMatrix& matrix, const GapModel& gaps,
+                                                   const SearchConfig& config, SearchStats* stats = nullptr) {
+    config.validate();
+    for (const EncodedSequence& query : queries)
+        for (std::uint8_t code : query.codes)
+            if (code >= ScoringMatrix::size) throw std::out_of_range("query code outside matrix alphabet");
+    std::vector<RankedResults> all(queries.size());
+    swb_mdb* resident = gpu::resident(db, config.length_threshold);
+    const std::size_t want = std::min<std::size_t>(config.top_k, db.num_sequences());
+    if (queries.empty()) return all;
+    if (swb_mdb_shard_count(resident) != 1 || want == 0) {
+        for (std::size_t q = 0; q < queries.size(); ++q) all[q] = run_search(queries[q], db, matrix, gaps, config, stats);
+        return all;
+    }
+    swb_db* shard = swb_mdb_shard(resident, 0);
+    std::vector<const std::uint8_t*> rows(queries.size());
+    std::vector<std::uint32_t> lengths(queries.size());
+    for (std::size_t q = 0; q < queries.size(); ++q) {
+        rows[q] = queries[q].codes.data();
+        lengths[q] = static_cast<std::uint32_t>(queries[q].length());
+    }
+    std::vector<swb_hit> hits(queries.size() * want);
+    std::vector<std::uint32_t> found(queries.size(), 0);
+    gpu::check(swb_search_many(shard, rows.data(), lengths.data(), static_cast<std::uint32_t>(queries.size()),
+                               gpu::matrix_table(matrix), gaps.open(), gaps.extend(), static_cast<std::uint32_t>(want),
+                               hits.data(), found.data(), nullptr));
+    swb_db_info info{};
+    gpu::check(swb_db_info_get(shard, &info));
+    for (std::size_t q = 0; q < queries.size(); ++q) {
+        all[q].hits.resize(found[q]);
+        for (std::uint32_t i = 0; i < found[q]; ++i) {
+            all[q].hits[i].db_index = hits[q * want + i].db_index;
+            all[q].hits[i].score = {hits[q * want + i].score};
+        }
+        if (stats != nullptr) {
+            stats->lane_scored += info.n_short;
+            stats->wavefront_scored += info.n_long;
+            stats->chunks_claimed += info.n_groups;
+        }
+        detail::attach_alignments(queries[q], db, matrix, gaps, config, resident, all[q]);
+    }
+    return all;
 }
 
 }  // namespace swsearch
