@@ -131,7 +131,7 @@ bool duo_applies(const swb_db* db, uint32_t ma, uint32_t mb, const int32_t* matr
     if (k.duo_ratio > 1.0 || lo == 0 || static_cast<double>(lo) < k.duo_ratio * static_cast<double>(hi)) return false;
     if ((hi + kInterTile - 1) / kInterTile < k.pipe_min_tiles) return false;   // short queries: chains, not throughput
     if (db->scan_policy != SWB_SCAN_AUTO || db->force_intra) return false;
-    if (db->meta.groups.size() < 2 * static_cast<size_t>(db->sm_count)) return false;
+    if (static_cast<double>(db->meta.groups.size()) < k.duo_min_groups_per_sm * static_cast<double>(db->sm_count)) return false;
     return make_plan(db, hi, matrix, open, ext).main == kMainS16;
 }
 

@@ -70,6 +70,7 @@ struct ScanKnobs {
     double duo_ratio = 0.75;         // SWB200_DUO: swb_search_many scans two queries at once (duo.cuh) when the shorter one has
                                      // at least this fraction of the longer one's length (the two-query kernel is ~15 % faster
                                      // per padded cell: below 0.74 the padding eats the gain); > 1: never
+    double duo_min_groups_per_sm = 2.0; // SWB200_DUO_MINGROUPS: ... and the database has at least this many groups per SM
     double wave_thin = 4.0;          // SWB200_WAVE_THIN: next to the pipeline, the wavefront kernel runs 8 warps per SM instead of
                                      // 16 when max_rows exceeds this x a warp's fair share of the search, and 4 warps beyond 1.5 x
                                      // this: its SMs then hold little besides the longest group's chain, which runs faster with
@@ -99,6 +100,7 @@ struct ScanKnobs {
         k.pipe_lag_div = std::max<uint32_t>(1, static_cast<uint32_t>(num("SWB200_PIPE_LAGDIV", k.pipe_lag_div)));
         k.wave_thin = num("SWB200_WAVE_THIN", k.wave_thin);
         k.duo_ratio = num("SWB200_DUO", k.duo_ratio);
+        k.duo_min_groups_per_sm = num("SWB200_DUO_MINGROUPS", k.duo_min_groups_per_sm);
         return k;
     }
 };

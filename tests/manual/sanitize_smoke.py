@@ -1,6 +1,7 @@
 """Small all-paths exercise for compute-sanitizer: single units, tile-split, row-block, narrow tiles, int32 re-run,
 wide mode, pair / batch entry points, multi-shard merge, large-k sort."""
-import sys
+import os, sys
+os.environ.setdefault("SWB200_DUO_MINGROUPS", "0.001")   # let the two-query scan run on this small database
 sys.path.insert(0, ".")
 import numpy as np
 from oracle import pyoracle as po
@@ -35,6 +36,15 @@ for m in (33, 600, 1100):
         good = bool((got == exp).all())
         ok &= good
         print(f"pipeline m={m} parity={good}")
+# the two-query scan of swb_search_many (queries of similar length share it), against single searches
+qs = [synth.random_residues(rng, m) for m in (300, 320, 600, 640, 90)]
+with Database(fdb.codes, fdb.offsets) as db:
+    many, _ = db.search_many(qs, b62, g, 20)
+    for q, (mi, ms_) in zip(qs, many):
+        ei, es, _ = port.run_search(q, fdb, b62, 10, 2, top_k=20)
+        good = bool((mi == ei).all() and (ms_ == es).all())
+        ok &= good
+        print(f"search_many m={len(q)} parity={good}")
 q = np.full(3400, 17, np.uint8)
 with Database.from_sequences([q, q[:3100], seqs[5]]) as db:
     got, st = db.score_all(q, b62, g)

@@ -461,3 +461,16 @@ def test_hybrid_scan_equals_each_kernel_alone(b62):
                     ref[qi] = got
                 idx, sc, _ = db.search(q, b62, g, 10)
                 assert idx[0] == sdb.planted[qi][0]
+
+
+def test_two_query_scan_against_the_oracle():
+    """swb_search_many with the two-query scan forced onto small random databases (tests/_duo_small.py, in a
+    subprocess because the policy knobs are read once per process): every ranked list equals the oracle's, for
+    query lengths around the tile and pass boundaries, four gap models, all routing thresholds."""
+    import os, subprocess, sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, SWB200_DUO_MINGROUPS="0.001")
+    out = subprocess.run([sys.executable, str(root / "tests" / "_duo_small.py")], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0 and "DUO-SMALL-OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
