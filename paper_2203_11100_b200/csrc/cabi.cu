@@ -133,11 +133,15 @@ struct swb_db {
     uint64_t* d_sort = nullptr;
     size_t sort_cap = 0;
     int32_t* d_all_scores = nullptr;
-    int32_t* d_slot_scores2 = nullptr;   // second query of a pair (duo.cuh)
+    // shared scans of swb_search_many (duo.cuh)
+    int32_t* d_multi_scores = nullptr;   // [queries of the scan][n_slots]
+    size_t multi_scores_cap = 0;
+    uint8_t* d_multi_codes = nullptr;    // the scan's queries, concatenated
+    size_t multi_codes_cap = 0;
+    uint8_t* d_duo_tiles = nullptr;      // DuoTile[n_tiles]
+    size_t duo_tiles_cap = 0;
     uint32_t* d_prof2 = nullptr;
     size_t prof2_cap = 0;
-    uint8_t* d_query2 = nullptr;
-    uint32_t query2_cap = 0;
     bool duo_attr_set = false;
 
     // query side
@@ -274,7 +278,7 @@ void swb_db_destroy(swb_db* db) {
         if (db->own_stream) cudaStreamSynchronize(db->own_stream);
         if (db->side_stream) cudaStreamSynchronize(db->side_stream);
         void* ptrs[] = {db->d_codes,      db->d_groups,   db->d_slot_index, db->d_slot_len,    db->d_border0,
-                        db->d_border1,    db->d_iborder0, db->d_iborder1, db->d_slot_scores2, db->d_prof2, db->d_query2,   db->d_slot_scores, db->d_flag_list,
+                        db->d_border1,    db->d_iborder0, db->d_iborder1, db->d_multi_scores, db->d_multi_codes, db->d_duo_tiles, db->d_prof2,   db->d_slot_scores, db->d_flag_list,
                         db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_vstate_off, db->d_vstate, db->d_progress, db->d_keys,        db->d_sel[0],
                         db->d_sel[1],     db->d_sort,     db->d_all_scores, db->d_query,       db->d_matrix,
                         db->d_prof8,      db->d_prof8i,   db->d_prof32i};
@@ -382,24 +386,17 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
     const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint64_t>(n_keys, 1)));
     const size_t n_groups = db->meta.groups.size();
 
-    // Queries of similar length share one scan (duo.cuh): walk the queries longest first and pair neighbours.
-    std::vector<uint32_t> order(n_queries);
-    for (uint32_t q = 0; q < n_queries; ++q) order[q] = q;
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return query_lens[a] > query_lens[b]; });
+    // Queries share database scans where that pays (duo.inl): the rest go one by one.
     struct Job {
-        uint32_t a, b;   // query numbers; b == a: a single-query scan
+        int scan;        // >= 0: shared scan number; -1: a single-query scan of `query`
+        uint32_t query;
     };
+    std::vector<DuoScan> scans;
+    std::vector<uint32_t> single;
+    plan_duo_scans(db, query_lens, n_queries, matrix, gap_open, gap_extend, scans, single);
     std::vector<Job> jobs;
-    for (uint32_t i = 0; i < n_queries; ++i) {
-        const uint32_t a = order[i];
-        if (i + 1 < n_queries && duo_applies(db, query_lens[a], query_lens[order[i + 1]], matrix, gap_open, gap_extend)) {
-            jobs.push_back(Job{a, order[i + 1]});
-            ++i;
-        } else {
-            jobs.push_back(Job{a, a});
-        }
-    }
-    std::sort(jobs.begin(), jobs.end(), [](const Job& x, const Job& y) { return std::min(x.a, x.b) < std::min(y.a, y.b); });
+    for (size_t i = 0; i < scans.size(); ++i) jobs.push_back(Job{static_cast<int>(i), 0});
+    for (uint32_t q : single) jobs.push_back(Job{-1, q});
 
     // one staging area per job (inputs up) and per query (keys down), sized up front: the pinned buffer must not
     // move while copies are in flight
@@ -407,7 +404,16 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
     size_t total = 0;
     for (size_t j = 0; j < jobs.size(); ++j) {
         in_off[j] = total;
-        total += (576 * sizeof(int32_t) + query_lens[jobs[j].a] + query_lens[jobs[j].b] + 128 + (n_groups + 1) * 9 + 255) & ~size_t(255);
+        size_t need = 576 * sizeof(int32_t) + 256 + (n_groups + 1) * 9;
+        if (jobs[j].scan >= 0) {
+            const DuoScan& sc = scans[jobs[j].scan];
+            for (uint32_t q : sc.a) need += (query_lens[q] + 15) & ~15u;
+            for (uint32_t q : sc.b) need += (query_lens[q] + 15) & ~15u;
+            need += static_cast<size_t>(std::max(sc.tiles_a, sc.tiles_b)) * sizeof(DuoTile);
+        } else {
+            need += query_lens[jobs[j].query];
+        }
+        total += (need + 255) & ~size_t(255);
     }
     for (uint32_t q = 0; q < n_queries; ++q) {
         out_off[q] = total;
@@ -426,20 +432,23 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
     };
     // jobs are issued back to back on the stream: the host prepares the next one (unit table, launches) while the
     // GPU still scans, and nothing synchronises until the last one is in flight
+    std::vector<uint32_t> scan_queries, code_off;
     for (size_t j = 0; j < jobs.size() && st == SWB_OK; ++j) {
-        const uint32_t a = jobs[j].a, b = jobs[j].b;
         db->stage_base = in_off[j];
         cudaEventRecord(db->many_events[2 * j], s);
         const uint64_t* d_top = nullptr;
-        if (a == b) {
-            st = search_keys_locked(db, queries[a], query_lens[a], matrix, gap_open, gap_extend, k_eff, &d_top);
-            if (st == SWB_OK) keys_down(a, d_top);
+        if (jobs[j].scan < 0) {
+            const uint32_t q = jobs[j].query;
+            st = search_keys_locked(db, queries[q], query_lens[q], matrix, gap_open, gap_extend, k_eff, &d_top);
+            if (st == SWB_OK) keys_down(q, d_top);
         } else {
-            st = score_duo_core(db, queries[a], query_lens[a], queries[b], query_lens[b], matrix, gap_open, gap_extend);
-            if (st == SWB_OK) st = finish_duo_query(db, db->d_query, query_lens[a], matrix, gap_open, gap_extend, db->d_slot_scores, k_eff, &d_top);
-            if (st == SWB_OK) keys_down(a, d_top);
-            if (st == SWB_OK) st = finish_duo_query(db, db->d_query2, query_lens[b], matrix, gap_open, gap_extend, db->d_slot_scores2, k_eff, &d_top);
-            if (st == SWB_OK) keys_down(b, d_top);
+            st = score_streams_core(db, queries, query_lens, scans[jobs[j].scan], matrix, gap_open, gap_extend, scan_queries, code_off);
+            for (size_t i = 0; i < scan_queries.size() && st == SWB_OK; ++i) {
+                const uint32_t q = scan_queries[i];
+                st = finish_duo_query(db, db->d_multi_codes + code_off[i], query_lens[q], matrix, gap_open, gap_extend,
+                                      db->d_multi_scores + i * static_cast<size_t>(db->n_slots), k_eff, &d_top);
+                if (st == SWB_OK) keys_down(q, d_top);
+            }
         }
         cudaEventRecord(db->many_events[2 * j + 1], s);
     }
@@ -458,17 +467,19 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
     }
     if (ms_per_query)
         for (size_t j = 0; j < jobs.size(); ++j) {
-            // a shared scan's time is split between its two queries in proportion to their lengths
+            // a shared scan's time is split between its queries in proportion to their lengths
             float ms = 0.f;
             cudaEventElapsedTime(&ms, db->many_events[2 * j], db->many_events[2 * j + 1]);
-            const uint32_t a = jobs[j].a, b = jobs[j].b;
-            if (a == b) {
-                ms_per_query[a] = ms;
-            } else {
-                const float la = static_cast<float>(query_lens[a]), lb = static_cast<float>(query_lens[b]);
-                ms_per_query[a] = ms * la / (la + lb);
-                ms_per_query[b] = ms * lb / (la + lb);
+            if (jobs[j].scan < 0) {
+                ms_per_query[jobs[j].query] = ms;
+                continue;
             }
+            const DuoScan& sc = scans[jobs[j].scan];
+            double columns = 0.0;
+            for (uint32_t q : sc.a) columns += query_lens[q];
+            for (uint32_t q : sc.b) columns += query_lens[q];
+            for (const std::vector<uint32_t>* stream : {&sc.a, &sc.b})
+                for (uint32_t q : *stream) ms_per_query[q] = static_cast<float>(ms * query_lens[q] / std::max(columns, 1.0));
         }
     return SWB_OK;
 }

@@ -1,4 +1,4 @@
-// duo.cuh -- the on-chip tile pipeline for TWO queries at once.
+// duo.cuh -- the on-chip tile pipeline for two STREAMS of queries at once.
 //
 // pipeline_s16_kernel packs two database sequences into the int16 halves of every DPX word; the two halves then
 // need two different profile rows (one per residue), and one PRMT per pair of cells stitches the two int8
@@ -13,8 +13,12 @@
 // 4-byte profile of a long query does not fit shared memory, so each warp keeps only the slice of its current tile
 // (25 rows x 32 columns, 3.6 KB) and reloads it at every slot start; shared-memory use no longer depends on m.
 //
-// Used by swb_search_many for pairs of queries of similar length (the shorter one is padded with zero-score
-// columns, which cannot raise a score).
+// Streams.  Each half is not one query but a STREAM of queries laid end to end, every query starting on a tile
+// boundary (DuoTile): at a query's first tile the inbound border of that half is reset to the matrix edge, and at
+// the end of every tile the half's running maximum goes to the score array of the query the tile belongs to.  A
+// batch of queries of any lengths is dealt over the two streams so that they end up equally long, and the only
+// padding left is each query's last tile (swb_search_many; the pad columns carry substitution score 0, which cannot
+// raise a score).
 #pragma once
 #include "pipeline.cuh"
 
@@ -24,12 +28,22 @@ constexpr uint32_t kDuoRowWords = kInterTile + 4;                 // 36 words = 
 constexpr uint32_t kDuoSliceWords = kProfRows * kDuoRowWords;     // one tile's profile slice: 900 words
 constexpr uint32_t kDuoSliceBytes = (kDuoSliceWords * 4 + 255) & ~255u;
 
-// prof2[tile][symbol][36]: word c = (M[s][qa[j]] + open) | (M[s][qb[j]] + open) << 16, j = tile * 32 + c; pad rows,
-// pad columns (past either query's end) and the 4 filler words carry `open` (substitution score 0).
+constexpr uint32_t kDuoNone = 0xFFFFFFFFu;
+
+// One 32-column tile of the two streams.
+struct DuoTile {
+    uint32_t qa, qb;          // query (number within the scan) the low / high half belongs to, kDuoNone: padding
+    uint32_t reset;           // bit 0 / bit 1: the low / high half starts a query here
+    uint32_t a_off, a_left;   // low half: offset of the tile's first column in the scan's concatenated query codes,
+    uint32_t b_off, b_left;   // and how many real columns are left from there (0: padding); same for the high half
+    uint32_t reserved;
+};
+
+// prof2[tile][symbol][36]: word c = (M[s][a_c] + open) | (M[s][b_c] + open) << 16 for the tile's columns c < 32;
+// pad rows, pad columns (past a query's end) and the 4 filler words carry `open` (substitution score 0).
 struct DuoProfileParams {
-    const uint8_t* qa;
-    const uint8_t* qb;
-    uint32_t ma, mb;
+    const uint8_t* codes;     // the scan's queries, concatenated
+    const DuoTile* tiles;
     const int32_t* matrix;
     int32_t shift;
     uint32_t n_tiles;
@@ -41,11 +55,11 @@ __global__ void build_duo_profile_kernel(DuoProfileParams p) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const uint32_t tile = i / kDuoSliceWords, rem = i % kDuoSliceWords;
         const uint32_t s = rem / kDuoRowWords, c = rem % kDuoRowWords;
-        const uint32_t j = tile * kInterTile + c;
+        const DuoTile td = p.tiles[tile];
         int32_t va = p.shift, vb = p.shift;
         if (s < kAlphabet && c < kInterTile) {
-            if (j < p.ma) va += p.matrix[s * kAlphabet + p.qa[j]];
-            if (j < p.mb) vb += p.matrix[s * kAlphabet + p.qb[j]];
+            if (c < td.a_left) va += p.matrix[s * kAlphabet + p.codes[td.a_off + c]];
+            if (c < td.b_left) vb += p.matrix[s * kAlphabet + p.codes[td.b_off + c]];
         }
         p.prof2[i] = (static_cast<uint32_t>(va) & 0xffffu) | (static_cast<uint32_t>(vb) << 16);
     }
@@ -56,13 +70,14 @@ struct DuoParams {
     const GroupDesc* groups;
     uint32_t n_items;         // 2 x groups: item i = half (i & 1) of group (i >> 1), longest first
     const uint32_t* prof2;
-    uint32_t n_tiles;         // ceil(max(ma, mb) / 32)
+    const DuoTile* tiles;     // [n_tiles]
+    uint32_t n_tiles;         // tiles of the longer stream
     uint32_t ring_chunks;
     uint32_t lag_div;
     uint2* border0;           // database-shaped border rows for the link into warp 0: half 0 / half 1 of a group
     uint2* border1;
-    int32_t* scores_a;        // per slot, zeroed per search, updated with atomicMax
-    int32_t* scores_b;
+    int32_t* scores;          // [queries of the scan][n_slots], zeroed per scan, updated with atomicMax
+    uint32_t n_slots;
     uint32_t* ticket;
     uint32_t neg_open2, neg_ext2;
 };
@@ -107,6 +122,10 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
         const uint32_t half = it & 1;
         const GroupDesc gd = p.groups[it >> 1];
         const bool first = tile == 0, last = tile + 1 == p.n_tiles;
+        const DuoTile td = p.tiles[tile];
+        // a half that starts a query here takes the matrix edge instead of its left neighbour's border
+        const uint32_t keep = ((td.reset & 1u) ? 0u : 0x0000FFFFu) | ((td.reset & 2u) ? 0u : 0xFFFF0000u);
+        const uint32_t edge = NO & ~keep;
         const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
         uint2* const gb = (half ? p.border1 : p.border0) + gd.chunk_base * kRowsPerChunk * 32;
         uint8_t* gborder = reinterpret_cast<uint8_t*>(gb + lane);
@@ -161,7 +180,10 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
             uint8_t* bout = wrap_out ? gborder + static_cast<size_t>(chunk) * kPipeChunkBytes
                                      : ring_out + (out_pos & ring_mask) * kPipeChunkBytes;
             uint2 bnext = make_uint2(NO, NO);
-            if (!first) bnext = bin[0];
+            if (!first) {
+                bnext = bin[0];
+                bnext.x = (bnext.x & keep) | edge, bnext.y = (bnext.y & keep) | edge;
+            }
             const uint32_t r_lo = half ? cur.z : cur.x, r_hi = half ? cur.w : cur.y;   // this half's 8 residues
             // a row's first four substitution words are loaded while the previous row is computed
             const uint4* prow_next = reinterpret_cast<const uint4*>(slice + (r_lo & 0xffu) * kDuoRowWords);
@@ -176,7 +198,10 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
                     sw_next = prow_next[0];
                 }
                 const uint2 bi = bnext;
-                if (!first && r + 1 < static_cast<int>(kRowsPerChunk)) bnext = bin[(r + 1) * 32];
+                if (!first && r + 1 < static_cast<int>(kRowsPerChunk)) {
+                    bnext = bin[(r + 1) * 32];
+                    bnext.x = (bnext.x & keep) | edge, bnext.y = (bnext.y & keep) | edge;
+                }
                 uint32_t hl = bi.x, E = bi.y;
                 uint32_t d = __vadd2(diag_in, sw.x);
                 diag_in = hl;
@@ -228,12 +253,12 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
             }
         }
 
-        // halves -> the two queries' scores of this lane's sequence
+        // halves -> this lane's sequence against the two queries this tile belongs to
         const int32_t sa = static_cast<int32_t>(best & 0xffffu);
         const int32_t sb = static_cast<int32_t>(best >> 16);
         const uint32_t sl = gd.first_slot + half * 32 + lane;
-        if (sa) atomicMax(p.scores_a + sl, sa);
-        if (sb) atomicMax(p.scores_b + sl, sb);
+        if (sa && td.qa != kDuoNone) atomicMax(p.scores + static_cast<size_t>(td.qa) * p.n_slots + sl, sa);
+        if (sb && td.qb != kDuoNone) atomicMax(p.scores + static_cast<size_t>(td.qb) * p.n_slots + sl, sb);
     }
     if (lane == 0) ctl->warp_item[warp] = kPipeEnd;
 }

@@ -1,61 +1,89 @@
-// duo.inl -- two queries per scan (duo.cuh): host side.  Included by cabi.cu inside extern "C".
+// duo.inl -- two streams of queries per scan (duo.cuh): host side.  Included by cabi.cu inside extern "C".
 
 namespace {
 
-// Scores every local sequence against both queries; results land in d_slot_scores (a) and d_slot_scores2 (b).
+// One shared scan: the two streams of queries (numbers into the caller's arrays), each in the order they are laid out.
+struct DuoScan {
+    std::vector<uint32_t> a, b;
+    uint32_t tiles_a = 0, tiles_b = 0;
+};
+
+inline uint32_t tiles_of(uint32_t m) { return (m + kInterTile - 1) / kInterTile; }
+
+// Scores every local sequence against every query of the scan; query number `scan_queries[i]` (a's members first, then
+// b's) gets the score array d_multi_scores + i * n_slots and the device copy d_multi_codes + code_off[i].
 // Asynchronous on db->stream.  Requires the packed int16 path (matrix + open within int8).
-swb_status score_duo_core(swb_db* db, const uint8_t* qa, uint32_t ma, const uint8_t* qb, uint32_t mb, const int32_t* matrix,
-                          int32_t open, int32_t ext) {
+swb_status score_streams_core(swb_db* db, const uint8_t* const* queries, const uint32_t* lens, const DuoScan& scan,
+                              const int32_t* matrix, int32_t open, int32_t ext, std::vector<uint32_t>& scan_queries,
+                              std::vector<uint32_t>& code_off) {
     cudaStream_t s = db->stream;
     swb_status st;
-    const uint32_t m = std::max(ma, mb);
-    const uint32_t n_tiles = (m + kInterTile - 1) / kInterTile;
+    const uint32_t n_tiles = std::max(scan.tiles_a, scan.tiles_b);
     const uint32_t n_groups = static_cast<uint32_t>(db->meta.groups.size());
+    scan_queries.clear();
+    scan_queries.insert(scan_queries.end(), scan.a.begin(), scan.a.end());
+    scan_queries.insert(scan_queries.end(), scan.b.begin(), scan.b.end());
+    const uint32_t nq = static_cast<uint32_t>(scan_queries.size());
     db->launches_total += db->launches;
     db->launches = 0;
     db->last_tile = kInterTile;
-    if (!db->d_slot_scores2)
-        if ((st = dev_alloc(&db->d_slot_scores2, db->n_slots, &db->device_bytes)) != SWB_OK) return st;
-    SWB_CUDA(cudaEventRecord(db->ev[EV_START], s));
-    SWB_CUDA(cudaMemsetAsync(db->d_slot_scores, 0, std::max<size_t>(db->n_slots, 1) * sizeof(int32_t), s));
-    SWB_CUDA(cudaMemsetAsync(db->d_slot_scores2, 0, std::max<size_t>(db->n_slots, 1) * sizeof(int32_t), s));
-    SWB_CUDA(cudaMemsetAsync(db->d_counters, 0, 4 * sizeof(uint32_t), s));
+    db->last_units = n_groups * 2;
 
-    // stage matrix + both queries
-    const size_t off_qa = 576 * sizeof(int32_t), off_qb = off_qa + ((ma + 15) & ~15u);
-    if ((st = ensure_stage(db, db->stage_base + off_qb + mb + 16)) != SWB_OK) return st;
+    // ---- staging: matrix | concatenated codes | tile table ---------------------------------------------------------
+    code_off.assign(nq, 0);
+    size_t codes_bytes = 0;
+    for (uint32_t i = 0; i < nq; ++i) {
+        code_off[i] = static_cast<uint32_t>(codes_bytes);
+        codes_bytes += (lens[scan_queries[i]] + 15) & ~15u;
+    }
+    const size_t off_codes = 576 * sizeof(int32_t);
+    const size_t off_tiles = (off_codes + codes_bytes + 31) & ~size_t(31);
+    const size_t stage_bytes = off_tiles + static_cast<size_t>(n_tiles) * sizeof(DuoTile);
+    if ((st = ensure_stage(db, db->stage_base + stage_bytes)) != SWB_OK) return st;
     uint8_t* const stage = db->h_stage + db->stage_base;
-    std::memcpy(stage, matrix, off_qa);
-    std::memcpy(stage + off_qa, qa, ma);
-    std::memcpy(stage + off_qb, qb, mb);
-    if (ma > db->query_cap) {
-        if (db->d_query) cudaFree(db->d_query);
-        db->d_query = nullptr;
-        if ((st = dev_alloc(&db->d_query, static_cast<size_t>(ma) * 2, &db->device_bytes)) != SWB_OK) return st;
-        db->query_cap = ma * 2;
-    }
-    if (mb > db->query2_cap) {
-        if (db->d_query2) cudaFree(db->d_query2);
-        db->d_query2 = nullptr;
-        if ((st = dev_alloc(&db->d_query2, static_cast<size_t>(mb) * 2, &db->device_bytes)) != SWB_OK) return st;
-        db->query2_cap = mb * 2;
-    }
-    SWB_CUDA(cudaMemcpyAsync(db->d_matrix, stage, off_qa, cudaMemcpyHostToDevice, s));
-    SWB_CUDA(cudaMemcpyAsync(db->d_query, stage + off_qa, ma, cudaMemcpyHostToDevice, s));
-    SWB_CUDA(cudaMemcpyAsync(db->d_query2, stage + off_qb, mb, cudaMemcpyHostToDevice, s));
+    std::memcpy(stage, matrix, off_codes);
+    for (uint32_t i = 0; i < nq; ++i) std::memcpy(stage + off_codes + code_off[i], queries[scan_queries[i]], lens[scan_queries[i]]);
+    DuoTile* tiles = reinterpret_cast<DuoTile*>(stage + off_tiles);
+    for (uint32_t t = 0; t < n_tiles; ++t) tiles[t] = DuoTile{kDuoNone, kDuoNone, 3u, 0, 0, 0, 0, 0};
+    auto lay_out = [&](const std::vector<uint32_t>& stream, uint32_t first_local, bool high) {
+        uint32_t t = 0;
+        for (size_t k = 0; k < stream.size(); ++k) {
+            const uint32_t local = first_local + static_cast<uint32_t>(k), m = lens[stream[k]];
+            for (uint32_t c = 0; c < m; c += kInterTile, ++t) {
+                DuoTile& td = tiles[t];
+                (high ? td.qb : td.qa) = local;
+                (high ? td.b_off : td.a_off) = code_off[local] + c;
+                (high ? td.b_left : td.a_left) = m - c;
+                if (c) td.reset &= high ? ~2u : ~1u;   // only a query's first tile starts from the matrix edge
+            }
+        }
+    };
+    lay_out(scan.a, 0, false);
+    lay_out(scan.b, static_cast<uint32_t>(scan.a.size()), true);
 
+    if ((st = ensure_dev(&db->d_multi_codes, &db->multi_codes_cap, codes_bytes + 64, &db->device_bytes)) != SWB_OK) return st;
+    if ((st = ensure_dev(&db->d_duo_tiles, &db->duo_tiles_cap, static_cast<size_t>(n_tiles) * sizeof(DuoTile), &db->device_bytes)) != SWB_OK)
+        return st;
+    if ((st = ensure_dev(&db->d_multi_scores, &db->multi_scores_cap, static_cast<size_t>(nq) * std::max<uint32_t>(db->n_slots, 1),
+                         &db->device_bytes)) != SWB_OK)
+        return st;
     if ((st = ensure_dev(&db->d_prof2, &db->prof2_cap, static_cast<size_t>(n_tiles) * kDuoSliceWords, &db->device_bytes)) != SWB_OK)
         return st;
+    SWB_CUDA(cudaEventRecord(db->ev[EV_START], s));
+    SWB_CUDA(cudaMemsetAsync(db->d_multi_scores, 0, static_cast<size_t>(nq) * std::max<uint32_t>(db->n_slots, 1) * sizeof(int32_t), s));
+    SWB_CUDA(cudaMemsetAsync(db->d_counters, 0, 4 * sizeof(uint32_t), s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_matrix, stage, off_codes, cudaMemcpyHostToDevice, s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_multi_codes, stage + off_codes, codes_bytes, cudaMemcpyHostToDevice, s));
+    SWB_CUDA(cudaMemcpyAsync(db->d_duo_tiles, tiles, static_cast<size_t>(n_tiles) * sizeof(DuoTile), cudaMemcpyHostToDevice, s));
+
     DuoProfileParams pp{};
-    pp.qa = db->d_query;
-    pp.qb = db->d_query2;
-    pp.ma = ma;
-    pp.mb = mb;
+    pp.codes = db->d_multi_codes;
+    pp.tiles = reinterpret_cast<const DuoTile*>(db->d_duo_tiles);
     pp.matrix = db->d_matrix;
     pp.shift = open;
     pp.n_tiles = n_tiles;
     pp.prof2 = db->d_prof2;
-    build_duo_profile_kernel<<<64, 256, 0, s>>>(pp);
+    build_duo_profile_kernel<<<128, 256, 0, s>>>(pp);
     ++db->launches;
     SWB_CUDA(cudaEventRecord(db->ev[EV_UP], s));
 
@@ -64,13 +92,14 @@ swb_status score_duo_core(swb_db* db, const uint8_t* qa, uint32_t ma, const uint
     dp.groups = db->d_groups;
     dp.n_items = n_groups * 2;
     dp.prof2 = db->d_prof2;
+    dp.tiles = reinterpret_cast<const DuoTile*>(db->d_duo_tiles);
     dp.n_tiles = n_tiles;
     dp.ring_chunks = scan_knobs().pipe_ring_cap >= 4 ? 4 : 2;
     dp.lag_div = scan_knobs().pipe_lag_div;
     dp.border0 = db->d_border0;
     dp.border1 = db->d_border1;
-    dp.scores_a = db->d_slot_scores;
-    dp.scores_b = db->d_slot_scores2;
+    dp.scores = db->d_multi_scores;
+    dp.n_slots = db->n_slots;
     dp.ticket = db->d_counters + 2;
     dp.neg_open2 = pack16(-open);
     dp.neg_ext2 = pack16(-ext);
@@ -90,7 +119,7 @@ swb_status score_duo_core(swb_db* db, const uint8_t* qa, uint32_t ma, const uint
     return SWB_OK;
 }
 
-// After score_duo_core: exact re-run of one query's flagged lanes, its keys and its top k.  `q_dev` is the query's
+// After score_streams_core: exact re-run of one query's flagged lanes, its keys and its top k.  `q_dev` is the query's
 // device copy, `scores` its slot scores.
 swb_status finish_duo_query(swb_db* db, const uint8_t* q_dev, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext,
                             int32_t* scores, uint32_t top_k, const uint64_t** d_out) {
@@ -124,15 +153,58 @@ swb_status finish_duo_query(swb_db* db, const uint8_t* q_dev, uint32_t m, const 
     return select_topk(db, db->d_keys, db->n_slots, top_k, d_out);
 }
 
-// Can this pair of queries share one scan?
-bool duo_applies(const swb_db* db, uint32_t ma, uint32_t mb, const int32_t* matrix, int32_t open, int32_t ext) {
+// Can queries of this batch share scans at all on this handle?
+bool duo_enabled(const swb_db* db) {
     const ScanKnobs& k = scan_knobs();
-    const uint32_t lo = std::min(ma, mb), hi = std::max(ma, mb);
-    if (k.duo_ratio > 1.0 || lo == 0 || static_cast<double>(lo) < k.duo_ratio * static_cast<double>(hi)) return false;
-    if ((hi + kInterTile - 1) / kInterTile < k.pipe_min_tiles) return false;   // short queries: chains, not throughput
-    if (db->scan_policy != SWB_SCAN_AUTO || db->force_intra) return false;
-    if (static_cast<double>(db->meta.groups.size()) < k.duo_min_groups_per_sm * static_cast<double>(db->sm_count)) return false;
-    return make_plan(db, hi, matrix, open, ext).main == kMainS16;
+    if (k.duo_ratio > 1.0 || db->scan_policy != SWB_SCAN_AUTO || db->force_intra) return false;
+    return static_cast<double>(db->meta.groups.size()) >= k.duo_min_groups_per_sm * static_cast<double>(db->sm_count);
+}
+
+// Deals the eligible queries of a batch over shared scans: longest first, each to the shortest stream so far, so that
+// the two streams of a scan end up equally long.  A scan whose streams differ too much (the padding would eat the
+// two-query kernel's ~15 % advantage) or that is too short to keep the pipeline busy is dissolved again: its queries
+// go one by one.  `single` receives every query that is not part of a scan.
+void plan_duo_scans(const swb_db* db, const uint32_t* lens, uint32_t n_queries, const int32_t* matrix, int32_t open, int32_t ext,
+                    std::vector<DuoScan>& scans, std::vector<uint32_t>& single) {
+    scans.clear();
+    single.clear();
+    const ScanKnobs& k = scan_knobs();
+    std::vector<uint32_t> eligible;
+    const bool enabled = duo_enabled(db) && make_plan(db, 64, matrix, open, ext).main == kMainS16;
+    for (uint32_t q = 0; q < n_queries; ++q) (enabled && lens[q] > 0 ? eligible : single).push_back(q);
+    if (eligible.size() < 2) {
+        single.insert(single.end(), eligible.begin(), eligible.end());
+        std::sort(single.begin(), single.end());
+        return;
+    }
+    std::stable_sort(eligible.begin(), eligible.end(), [&](uint32_t x, uint32_t y) { return lens[x] > lens[y]; });
+    uint64_t total_tiles = 0;
+    for (uint32_t q : eligible) total_tiles += tiles_of(lens[q]);
+    const uint32_t n_scans = static_cast<uint32_t>((total_tiles + 2ull * k.duo_stream_tiles - 1) / (2ull * k.duo_stream_tiles));
+    scans.resize(n_scans);
+    for (uint32_t q : eligible) {
+        DuoScan* best = nullptr;
+        bool high = false;
+        uint32_t least = ~0u;
+        for (DuoScan& sc : scans) {
+            if (sc.tiles_a < least) least = sc.tiles_a, best = &sc, high = false;
+            if (sc.tiles_b < least) least = sc.tiles_b, best = &sc, high = true;
+        }
+        (high ? best->b : best->a).push_back(q);
+        (high ? best->tiles_b : best->tiles_a) += tiles_of(lens[q]);
+    }
+    std::vector<DuoScan> kept;
+    for (DuoScan& sc : scans) {
+        const uint32_t lo = std::min(sc.tiles_a, sc.tiles_b), hi = std::max(sc.tiles_a, sc.tiles_b);
+        if (lo == 0 || static_cast<double>(lo) < k.duo_ratio * static_cast<double>(hi) || hi < k.pipe_min_tiles) {
+            single.insert(single.end(), sc.a.begin(), sc.a.end());
+            single.insert(single.end(), sc.b.begin(), sc.b.end());
+        } else {
+            kept.push_back(std::move(sc));
+        }
+    }
+    scans.swap(kept);
+    std::sort(single.begin(), single.end());
 }
 
 }  // namespace
@@ -149,7 +221,15 @@ swb_status swb_score_all_duo(swb_db* db, const uint8_t* qa, uint32_t ma, const u
     DeviceGuard guard(db->device);
     const QueryPlan pl = make_plan(db, std::max(ma, mb), matrix, gap_open, gap_extend);
     if (pl.main != kMainS16) return fail(SWB_ERR_UNSUPPORTED, "the two-query scan needs the packed int16 path");
-    st = score_duo_core(db, qa, ma, qb, mb, matrix, gap_open, gap_extend);
+    const uint8_t* two[2] = {qa, qb};
+    const uint32_t two_len[2] = {ma, mb};
+    DuoScan scan;
+    scan.a = {0};
+    scan.b = {1};
+    scan.tiles_a = tiles_of(ma);
+    scan.tiles_b = tiles_of(mb);
+    std::vector<uint32_t> order, code_off;
+    st = score_streams_core(db, two, two_len, scan, matrix, gap_open, gap_extend, order, code_off);
     if (st != SWB_OK) return st;
     cudaStream_t s = db->stream;
     const uint32_t n_total = db->meta.n_total;
@@ -157,10 +237,11 @@ swb_status swb_score_all_duo(swb_db* db, const uint8_t* qa, uint32_t ma, const u
         if ((st = dev_alloc(&db->d_all_scores, n_total, &db->device_bytes)) != SWB_OK) return st;
     const unsigned blocks = std::max(1u, std::min(1024u, (db->n_slots + 255) / 256));
     int32_t* outs[2] = {scores_a, scores_b};
-    int32_t* srcs[2] = {db->d_slot_scores, db->d_slot_scores2};
     for (int q = 0; q < 2; ++q) {
         SWB_CUDA(cudaMemcpyAsync(db->d_all_scores, outs[q], static_cast<size_t>(n_total) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-        if (db->n_slots) scatter_scores_kernel<<<blocks, 256, 0, s>>>(srcs[q], db->d_slot_index, db->n_slots, db->d_all_scores);
+        if (db->n_slots)
+            scatter_scores_kernel<<<blocks, 256, 0, s>>>(db->d_multi_scores + static_cast<size_t>(q) * db->n_slots, db->d_slot_index,
+                                                          db->n_slots, db->d_all_scores);
         SWB_CUDA(cudaMemcpyAsync(outs[q], db->d_all_scores, static_cast<size_t>(n_total) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     }
     SWB_CUDA(cudaEventRecord(db->ev[EV_TOPK], s));

@@ -67,9 +67,11 @@ struct ScanKnobs {
                                      // busy for the whole search whatever their number: +15 % at m = 375, -2 % at m = 1000)
     uint32_t pipe_ring_cap = 4;      // SWB200_PIPE_RING: chunks per shared-memory ring at most (power of two)
     uint32_t pipe_lag_div = 24;      // SWB200_PIPE_LAGDIV: a tile starts group_chunks / this chunks behind its neighbour
-    double duo_ratio = 0.75;         // SWB200_DUO: swb_search_many scans two queries at once (duo.cuh) when the shorter one has
-                                     // at least this fraction of the longer one's length (the two-query kernel is ~15 % faster
-                                     // per padded cell: below 0.74 the padding eats the gain); > 1: never
+    double duo_ratio = 0.75;         // SWB200_DUO: swb_search_many lays its queries out as two streams per scan (duo.cuh); a scan
+                                     // is kept when its shorter stream has at least this fraction of the longer one's tiles (the
+                                     // two-stream kernel is ~15 % faster per padded cell: below 0.74 the padding eats the gain);
+                                     // > 1: never
+    uint32_t duo_stream_tiles = 704; // SWB200_DUO_TILES: tiles per stream of a shared scan at most (a tall group's item must not outlast the scan)
     double duo_min_groups_per_sm = 2.0; // SWB200_DUO_MINGROUPS: ... and the database has at least this many groups per SM
     double wave_thin = 4.0;          // SWB200_WAVE_THIN: next to the pipeline, the wavefront kernel runs 8 warps per SM instead of
                                      // 16 when max_rows exceeds this x a warp's fair share of the search, and 4 warps beyond 1.5 x
@@ -100,6 +102,7 @@ struct ScanKnobs {
         k.pipe_lag_div = std::max<uint32_t>(1, static_cast<uint32_t>(num("SWB200_PIPE_LAGDIV", k.pipe_lag_div)));
         k.wave_thin = num("SWB200_WAVE_THIN", k.wave_thin);
         k.duo_ratio = num("SWB200_DUO", k.duo_ratio);
+        k.duo_stream_tiles = std::max<uint32_t>(16, static_cast<uint32_t>(num("SWB200_DUO_TILES", k.duo_stream_tiles)));
         k.duo_min_groups_per_sm = num("SWB200_DUO_MINGROUPS", k.duo_min_groups_per_sm);
         return k;
     }
