@@ -148,11 +148,11 @@ swb_status swb_search(swb_db* db, const uint8_t* query, uint32_t query_len, cons
 
 /* Several queries against the shard, pipelined: every query's upload, scan and select are
  * issued back to back on the handle's stream and the call synchronises once, so host preparation and launch
- * latency of query q+1 overlap the scan of query q.  Queries of similar length (the shorter at least 3/4 of the
- * longer, 257 residues or more, on a database of at least two groups per SM) additionally SHARE one scan: the
- * two-query kernel keeps one sequence per thread and the two queries in the int16 halves of every DPX word, which
- * saves the per-cell PRMT of the two-sequence kernels (about 15 % per cell).  Results are identical to n_queries
- * calls of swb_search.
+ * latency of query q+1 overlap the scan of query q.  On a database of at least two groups per SM the queries
+ * additionally SHARE database scans: they are laid end to end in two streams, one per int16 half of the DPX words
+ * (one sequence per thread), which saves the per-cell PRMT of the two-sequence kernels (about 15 % per cell) and
+ * reads the database once per scan instead of once per query.  Results are identical to n_queries calls of
+ * swb_search.
  *   hits          n_queries x top_k entries; query q's hits start at hits[q * top_k]
  *   n_hits        n_queries counts
  *   ms_per_query  optional: device time of each query (CUDA events; a shared scan's time is split by length) */
@@ -160,8 +160,8 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
                            uint32_t n_queries, const int32_t* matrix, int32_t gap_open, int32_t gap_extend,
                            uint32_t top_k, swb_hit* hits, uint32_t* n_hits, float* ms_per_query);
 
-/* All scores of TWO queries from one scan (the two-query kernel swb_search_many uses for queries of similar
- * length), in database order, before any int32 re-run: scores above 32767 - max(matrix) are not exact here.
+/* All scores of TWO queries from one shared scan (the two-stream kernel of swb_search_many with one query per
+ * stream), in database order, before any int32 re-run: scores above 32767 - max(matrix) are not exact here.
  * For tests and measurement of that kernel. */
 swb_status swb_score_all_duo(swb_db* db, const uint8_t* query_a, uint32_t len_a, const uint8_t* query_b, uint32_t len_b,
                              const int32_t* matrix, int32_t gap_open, int32_t gap_extend, int32_t* scores_a,
