@@ -9,7 +9,7 @@ one full sweep: 20 searches, 8.5e12 cell updates.  GCUPS = sum(query_len x db_re
 (SPEC.md:353), real residues only (padding is never counted).
 
   value      the sweep as ONE batch through swb_search_many (N = 1): queries are issued back to back on the stream,
-             queries of similar length share one scan (two-query kernel); device time = sum of the per-job CUDA-event
+             the queries share database scans as two streams (duo_pipeline_kernel); device time = sum of the per-job CUDA-event
              times the call returns (database already resident in HBM, packed once outside the timed region like the
              reference's load phase).  N > 1: the per-search path below (one all-gather per search).
   e2e        the same batch through the same C-ABI call with HOST buffers: host queries/matrix in, host hits out,
@@ -339,8 +339,8 @@ def main_native(args):
             head_value = total_cells * steps / (batch["dev_ms"] * 1e-3) / 1e9
             head_e2e = total_cells * steps / (batch["e2e_ms"] * 1e-3) / 1e9
             head_ms, head_launches, head_clocks = batch["e2e_ms"] / steps, batch["launches"], batch["clocks"]
-            api = "swb_search_many, one call per sweep (queries of similar length share a scan)"
-            kernel = "duo_pipeline_kernel (pairs of similar length) + pipeline_s16_kernel / wavefront_s16_kernel (the rest)"
+            api = "swb_search_many, one call per sweep (the queries share one database scan as two streams)"
+            kernel = "duo_pipeline_kernel (shared scan of the batch)"
         else:
             head_value, head_e2e, head_ms, head_launches, head_clocks = value, e2e, e2e_ms / steps, launches, clocks
             api = single["api"]
@@ -362,7 +362,7 @@ def main_native(args):
                          "achieved": head_value, "peak": roof,
                          "unit": "GCUPS", "frac": head_value / roof,
                          "peak_def": "P_dpx x 2 / 6 (SURVEY 8(d): 6 DPX instructions per two cells), P_dpx = measured "
-                                     "VIADDMNMX.S16x2 thread-instr/s (live, this run); the two-query kernel issues 3.5 ALU-pipe "
+                                     "VIADDMNMX.S16x2 thread-instr/s (live, this run); the two-stream kernel issues 3.5 ALU-pipe "
                                      "instructions per two cells and the others 4.5, so frac can exceed 1",
                          "p_dpx_ginst_per_s": p_dpx, "pipe_rates": rates,
                          "traffic": traffic.get("dram_bytes") if traffic else None, "traffic_detail": traffic,

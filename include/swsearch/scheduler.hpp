@@ -210,7 +210,7 @@ inline RankedResults run_search(const EncodedSequence& query, const SequenceData
 
 /// Several queries against the same database: the same results as a loop over run_search (which is what the
 /// reference's callers write), but issued to the GPU as one batch -- searches overlap each other's
-/// host preparation, and queries of similar length share one database scan (swb_search_many).  With the database
+/// host preparation, and the queries share database scans as two streams (swb_search_many).  With the database
 /// sharded over several GPUs this falls back to the loop.
 inline std::vector<RankedResults> run_search_batch(const std::vector<EncodedSequence>& queries, const SequenceDatabase& db,
                                                    const ScoringMatrix& matrix, const GapModel& gaps,

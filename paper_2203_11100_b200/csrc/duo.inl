@@ -162,7 +162,7 @@ bool duo_enabled(const swb_db* db) {
 
 // Deals the eligible queries of a batch over shared scans: longest first, each to the shortest stream so far, so that
 // the two streams of a scan end up equally long.  A scan whose streams differ too much (the padding would eat the
-// two-query kernel's ~15 % advantage) or that is too short to keep the pipeline busy is dissolved again: its queries
+// two-stream kernel's ~15 % advantage) or that is too short to keep the pipeline busy is dissolved again: its queries
 // go one by one.  `single` receives every query that is not part of a scan.
 void plan_duo_scans(const swb_db* db, const uint32_t* lens, uint32_t n_queries, const int32_t* matrix, int32_t open, int32_t ext,
                     std::vector<DuoScan>& scans, std::vector<uint32_t>& single) {
@@ -220,7 +220,7 @@ swb_status swb_score_all_duo(swb_db* db, const uint8_t* qa, uint32_t ma, const u
     std::lock_guard<std::mutex> lock(db->mu);
     DeviceGuard guard(db->device);
     const QueryPlan pl = make_plan(db, std::max(ma, mb), matrix, gap_open, gap_extend);
-    if (pl.main != kMainS16) return fail(SWB_ERR_UNSUPPORTED, "the two-query scan needs the packed int16 path");
+    if (pl.main != kMainS16) return fail(SWB_ERR_UNSUPPORTED, "the shared scan needs the packed int16 path");
     const uint8_t* two[2] = {qa, qb};
     const uint32_t two_len[2] = {ma, mb};
     DuoScan scan;

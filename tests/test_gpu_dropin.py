@@ -60,8 +60,8 @@ def test_cli_search_and_bench(lib, tmp_path, port):
 
 
 def test_run_search_batch_equals_a_loop_of_run_search(lib):
-    """include/swsearch/scheduler.hpp::run_search_batch (swb_search_many behind it, queries of similar length sharing
-    a scan): ranked lists, edit scripts and SearchStats identical to calling run_search per query."""
+    """include/swsearch/scheduler.hpp::run_search_batch (swb_search_many behind it, the queries sharing
+    database scans): ranked lists, edit scripts and SearchStats identical to calling run_search per query."""
     exe = ROOT / "tests" / "cpp" / "_build" / "batch_unit"
     assert exe.exists(), "tests/cpp/_build/batch_unit is built by __graft_entry__.build()"
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)

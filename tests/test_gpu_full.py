@@ -82,8 +82,8 @@ def test_sampled_score_parity_through_the_pipeline(full, port, b62):
 
 
 def test_batched_sweep_equals_single_searches(full, b62):
-    """swb_search_many over the whole 20-query sweep (queries of similar length share one scan through the
-    two-query kernel, the rest go one by one): every ranked list equals the one swb_search returns."""
+    """swb_search_many over the whole 20-query sweep (the queries share one database scan as two streams of the
+    two-stream kernel): every ranked list equals the one swb_search returns."""
     queries, sdb, db = full
     many, ms = db.search_many(queries, b62, GapModel(10, 2), 10)
     assert len(many) == len(queries) and (ms > 0).all()

@@ -464,7 +464,7 @@ def test_hybrid_scan_equals_each_kernel_alone(b62):
 
 
 def test_two_query_scan_against_the_oracle():
-    """swb_search_many with the two-query scan forced onto small random databases (tests/_duo_small.py, in a
+    """swb_search_many with its shared scans forced onto small random databases (tests/_duo_small.py, in a
     subprocess because the policy knobs are read once per process): every ranked list equals the oracle's, for
     query lengths around the tile and pass boundaries, four gap models, all routing thresholds."""
     import os, subprocess, sys
