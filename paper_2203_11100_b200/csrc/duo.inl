@@ -157,7 +157,11 @@ swb_status finish_duo_query(swb_db* db, const uint8_t* q_dev, uint32_t m, const 
 bool duo_enabled(const swb_db* db) {
     const ScanKnobs& k = scan_knobs();
     if (k.duo_ratio > 1.0 || db->scan_policy != SWB_SCAN_AUTO || db->force_intra) return false;
-    return static_cast<double>(db->meta.groups.size()) >= k.duo_min_groups_per_sm * static_cast<double>(db->sm_count);
+    if (static_cast<double>(db->meta.groups.size()) < k.duo_min_groups_per_sm * static_cast<double>(db->sm_count)) return false;
+    // every half-group is one CTA's item here: the tallest must fit a CTA's fair share of the scan (small shards of a
+    // database with a few very long sequences do not; their searches go one by one, where the tall groups get the
+    // wavefront kernel)
+    return static_cast<double>(db->max_rows) * db->sm_count <= k.duo_tall * 2.0 * static_cast<double>(db->meta.padded_rows);
 }
 
 // Deals the eligible queries of a batch over shared scans: longest first, each to the shortest stream so far, so that

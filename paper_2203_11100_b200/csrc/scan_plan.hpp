@@ -72,6 +72,8 @@ struct ScanKnobs {
                                      // two-stream kernel is ~15 % faster per padded cell: below 0.74 the padding eats the gain);
                                      // > 1: never
     uint32_t duo_stream_tiles = 704; // SWB200_DUO_TILES: tiles per stream of a shared scan at most (a tall group's item must not outlast the scan)
+    double duo_tall = 1.0;           // SWB200_DUO_TALL: ... and the tallest group's rows x SMs stay under this x the database's rows x 2
+                                     // (a half-group is one CTA's item: it must fit that CTA's fair share of the scan)
     double duo_min_groups_per_sm = 2.0; // SWB200_DUO_MINGROUPS: ... and the database has at least this many groups per SM
     double wave_thin = 4.0;          // SWB200_WAVE_THIN: next to the pipeline, the wavefront kernel runs 8 warps per SM instead of
                                      // 16 when max_rows exceeds this x a warp's fair share of the search, and 4 warps beyond 1.5 x
@@ -103,6 +105,7 @@ struct ScanKnobs {
         k.wave_thin = num("SWB200_WAVE_THIN", k.wave_thin);
         k.duo_ratio = num("SWB200_DUO", k.duo_ratio);
         k.duo_stream_tiles = std::max<uint32_t>(16, static_cast<uint32_t>(num("SWB200_DUO_TILES", k.duo_stream_tiles)));
+        k.duo_tall = num("SWB200_DUO_TALL", k.duo_tall);
         k.duo_min_groups_per_sm = num("SWB200_DUO_MINGROUPS", k.duo_min_groups_per_sm);
         return k;
     }
