@@ -80,6 +80,7 @@ struct DuoParams {
     uint32_t n_slots;
     uint32_t* ticket;
     uint32_t neg_open2, neg_ext2;
+    unsigned long long* stats;   // SWB_PIPE_STATS builds: [cta][warp][4] clocks waited on input / output / item fetch, total
 };
 
 template <int T, int kThreads>
@@ -114,9 +115,17 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
     tickets.group_first = 0;
     tickets.ticket = p.ticket;
 
+#ifdef SWB_PIPE_STATS
+    long long w_in = 0, w_out = 0, w_item = 0;
+    const long long t_begin = clock64();
+#define SWB_STAT(acc, stmt) { const long long t0__ = clock64(); stmt; acc += clock64() - t0__; }
+#else
+#define SWB_STAT(acc, stmt) { stmt; }
+#endif
     for (uint32_t slot = warp;; slot += kPipeWarps) {
         const uint32_t item = slot / p.n_tiles, tile = slot - item * p.n_tiles;
-        const uint32_t it = pipe_item(tickets, ctl, item, lane);
+        uint32_t it;
+        SWB_STAT(w_item, it = pipe_item(tickets, ctl, item, lane));
         if (it == kPipeEnd) break;
         if (lane == 0) ctl->warp_item[warp] = item;
         const uint32_t half = it & 1;
@@ -157,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
                 if (wrap_in) {
                     if (staged == in_pos) {
                         const uint32_t need = min(in_pos + 2, in_end);
-                        while (lds_acquire(&ctl->head[0]) < need) __nanosleep(20);
+                        SWB_STAT(w_in, while (lds_acquire(&ctl->head[0]) < need) __nanosleep(20));
                         stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
                                     gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
                         ++staged;
@@ -171,11 +180,11 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
                     }
                 } else {
                     const uint32_t need = min(chunk == 0 ? in_pos + lag : in_pos + 1, in_end);
-                    while (lds_acquire(&ctl->head[warp]) < need) __nanosleep(20);
+                    SWB_STAT(w_in, while (lds_acquire(&ctl->head[warp]) < need) __nanosleep(20));
                 }
             }
             if (!last && !wrap_out)
-                while (out_pos - lds_acquire(&ctl->tail[next]) >= p.ring_chunks) __nanosleep(20);
+                SWB_STAT(w_out, while (out_pos - lds_acquire(&ctl->tail[next]) >= p.ring_chunks) __nanosleep(20));
             const uint2* bin = reinterpret_cast<const uint2*>(ring_in + (in_pos & ring_mask) * kPipeChunkBytes);
             uint8_t* bout = wrap_out ? gborder + static_cast<size_t>(chunk) * kPipeChunkBytes
                                      : ring_out + (out_pos & ring_mask) * kPipeChunkBytes;
@@ -261,6 +270,13 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
         if (sb && td.qb != kDuoNone) atomicMax(p.scores + static_cast<size_t>(td.qb) * p.n_slots + sl, sb);
     }
     if (lane == 0) ctl->warp_item[warp] = kPipeEnd;
+#ifdef SWB_PIPE_STATS
+    if (lane == 0 && p.stats) {
+        unsigned long long* o = p.stats + (static_cast<size_t>(blockIdx.x) * kPipeWarps + warp) * 4;
+        o[0] = w_in, o[1] = w_out, o[2] = w_item, o[3] = clock64() - t_begin;
+    }
+#endif
+#undef SWB_STAT
 }
 
 }  // namespace swb
