@@ -44,7 +44,7 @@ def is_stale() -> bool:
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     if not force and not is_stale():
         return LIB
-    extra = [f"-D{k}={os.environ[k]}" for k in ("SWB_INTER_TILE", "SWB_INTER_THREADS", "SWB_PIPE_STATS") if k in os.environ]   # tuning only
+    extra = [f"-D{k}={os.environ[k]}" for k in ("SWB_INTER_TILE", "SWB_INTER_THREADS", "SWB_PIPE_STATS", "SWB_PIPE_POLL_NS") if k in os.environ]   # tuning only
     out = Path(os.environ.get("SWB_LIB_OUT", str(LIB)))
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-ccbin", "/usr/bin/g++", "-o", str(out)] + [str(CSRC / s) for s in SOURCES] + ["-ldl", "-lpthread"]
     if verbose:

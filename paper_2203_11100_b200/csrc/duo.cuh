@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
                 if (wrap_in) {
                     if (staged == in_pos) {
                         const uint32_t need = min(in_pos + 2, in_end);
-                        SWB_STAT(w_in, while (lds_acquire(&ctl->head[0]) < need) __nanosleep(20));
+                        SWB_STAT(w_in, while (lds_acquire(&ctl->head[0]) < need) __nanosleep(kPipePollNs));
                         stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
                                     gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
                         ++staged;
@@ -180,73 +180,83 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
                     }
                 } else {
                     const uint32_t need = min(chunk == 0 ? in_pos + lag : in_pos + 1, in_end);
-                    SWB_STAT(w_in, while (lds_acquire(&ctl->head[warp]) < need) __nanosleep(20));
+                    SWB_STAT(w_in, while (lds_acquire(&ctl->head[warp]) < need) __nanosleep(kPipePollNs));
                 }
             }
             if (!last && !wrap_out)
-                SWB_STAT(w_out, while (out_pos - lds_acquire(&ctl->tail[next]) >= p.ring_chunks) __nanosleep(20));
+                SWB_STAT(w_out, while (out_pos - lds_acquire(&ctl->tail[next]) >= p.ring_chunks) __nanosleep(kPipePollNs));
             const uint2* bin = reinterpret_cast<const uint2*>(ring_in + (in_pos & ring_mask) * kPipeChunkBytes);
             uint8_t* bout = wrap_out ? gborder + static_cast<size_t>(chunk) * kPipeChunkBytes
                                      : ring_out + (out_pos & ring_mask) * kPipeChunkBytes;
-            uint2 bnext = make_uint2(NO, NO);
-            if (!first) {
-                bnext = bin[0];
-                bnext.x = (bnext.x & keep) | edge, bnext.y = (bnext.y & keep) | edge;
-            }
             const uint32_t r_lo = half ? cur.z : cur.x, r_hi = half ? cur.w : cur.y;   // this half's 8 residues
-            // a row's first four substitution words are loaded while the previous row is computed
-            const uint4* prow_next = reinterpret_cast<const uint4*>(slice + (r_lo & 0xffu) * kDuoRowWords);
-            uint4 sw_next = prow_next[0];
+            // Two rows at a time, the second one column behind the first: its cell (r+1, k) needs (r, k) and (r, k-1),
+            // which the first row has just produced, and the two E -> H -> Hm chains are independent of each other,
+            // which doubles the instructions a warp can have in flight (the chains, not the ALU pipe, were what
+            // the single-row sweep waited on).  Both rows update Hm[k] and F[k] in place, the second after the first.
 #pragma unroll
-            for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
-                const uint4* prow = prow_next;
-                uint4 sw = sw_next;
-                if (r + 1 < static_cast<int>(kRowsPerChunk)) {
-                    const uint32_t an = (((r + 1) < 4 ? r_lo : r_hi) >> (8 * ((r + 1) & 3))) & 0xffu;
-                    prow_next = reinterpret_cast<const uint4*>(slice + an * kDuoRowWords);
-                    sw_next = prow_next[0];
+            for (int rp = 0; rp < static_cast<int>(kRowsPerChunk); rp += 2) {
+                const uint32_t aA = ((rp < 4 ? r_lo : r_hi) >> (8 * (rp & 3))) & 0xffu;
+                const uint32_t aB = ((rp + 1 < 4 ? r_lo : r_hi) >> (8 * ((rp + 1) & 3))) & 0xffu;
+                const uint4* prowA = reinterpret_cast<const uint4*>(slice + aA * kDuoRowWords);
+                const uint4* prowB = reinterpret_cast<const uint4*>(slice + aB * kDuoRowWords);
+                uint2 biA = make_uint2(NO, NO), biB = make_uint2(NO, NO);
+                if (!first) {
+                    biA = bin[rp * 32], biB = bin[(rp + 1) * 32];
+                    biA.x = (biA.x & keep) | edge, biA.y = (biA.y & keep) | edge;
+                    biB.x = (biB.x & keep) | edge, biB.y = (biB.y & keep) | edge;
                 }
-                const uint2 bi = bnext;
-                if (!first && r + 1 < static_cast<int>(kRowsPerChunk)) {
-                    bnext = bin[(r + 1) * 32];
-                    bnext.x = (bnext.x & keep) | edge, bnext.y = (bnext.y & keep) | edge;
-                }
-                uint32_t hl = bi.x, E = bi.y;
-                uint32_t d = __vadd2(diag_in, sw.x);
-                diag_in = hl;
+                uint32_t hlA = biA.x, EA = biA.y, hlB = biB.x, EB = biB.y;
+                uint4 swA = prowA[0], swB = prowB[0];
+                uint32_t dA = __vadd2(diag_in, swA.x);   // (row A, column 0): diagonal = the previous row's inbound Hm
+                uint32_t dB = __vadd2(hlA, swB.x);       // (row B, column 0): diagonal = row A's inbound Hm
+                diag_in = hlB;
+                uint32_t seenA = 0;
 #pragma unroll
-                for (int k = 0; k < T; k += 4) {
-                    const uint4 sn = k + 4 < T ? prow[k / 4 + 1] : sw;   // the next four columns' substitution words
-                    // column k
-                    E = __viaddmax_s16x2(E, NE, hl);
-                    F[k] = __viaddmax_s16x2(F[k], NE, Hm[k]);
-                    const uint32_t d0 = d;
-                    const uint32_t d1 = __vadd2(Hm[k], sw.y);
-                    hl = __vadd2(__vimax3_s16x2_relu(d0, E, F[k]), NO);
-                    Hm[k] = hl;
-                    // column k + 1
-                    E = __viaddmax_s16x2(E, NE, hl);
-                    F[k + 1] = __viaddmax_s16x2(F[k + 1], NE, Hm[k + 1]);
-                    const uint32_t d2 = __vadd2(Hm[k + 1], sw.z);
-                    hl = __vadd2(__vimax3_s16x2_relu(d1, E, F[k + 1]), NO);
-                    Hm[k + 1] = hl;
-                    best = __vimax3_s16x2(best, d0, d1);
-                    // column k + 2
-                    E = __viaddmax_s16x2(E, NE, hl);
-                    F[k + 2] = __viaddmax_s16x2(F[k + 2], NE, Hm[k + 2]);
-                    const uint32_t d3 = __vadd2(Hm[k + 2], sw.w);
-                    hl = __vadd2(__vimax3_s16x2_relu(d2, E, F[k + 2]), NO);
-                    Hm[k + 2] = hl;
-                    // column k + 3
-                    E = __viaddmax_s16x2(E, NE, hl);
-                    F[k + 3] = __viaddmax_s16x2(F[k + 3], NE, Hm[k + 3]);
-                    if (k + 4 < T) d = __vadd2(Hm[k + 3], sn.x);
-                    hl = __vadd2(__vimax3_s16x2_relu(d3, E, F[k + 3]), NO);
-                    Hm[k + 3] = hl;
-                    best = __vimax3_s16x2(best, d2, d3);
-                    sw = sn;
+                for (int k = 0; k <= T; ++k) {
+                    // row A, column k
+                    if (k < T) {
+                        const uint32_t sA = (k & 3) == 3 ? 0u : (k & 3) == 0 ? swA.y : (k & 3) == 1 ? swA.z : swA.w;   // column k + 1's word
+                        EA = __viaddmax_s16x2(EA, NE, hlA);
+                        F[k] = __viaddmax_s16x2(F[k], NE, Hm[k]);
+                        const uint32_t dcur = dA;
+                        if ((k & 3) == 3) {
+                            if (k + 1 < T) {
+                                swA = prowA[(k + 1) / 4];
+                                dA = __vadd2(Hm[k], swA.x);
+                            }
+                        } else {
+                            dA = __vadd2(Hm[k], sA);
+                        }
+                        hlA = __vadd2(__vimax3_s16x2_relu(dcur, EA, F[k]), NO);
+                        Hm[k] = hlA;
+                        if (k == 0) best = __vmaxs2(best, dcur);
+                        else seenA = dcur;
+                    }
+                    // row B, column k - 1
+                    if (k >= 1) {
+                        const int c = k - 1;
+                        const uint32_t sB = (c & 3) == 3 ? 0u : (c & 3) == 0 ? swB.y : (c & 3) == 1 ? swB.z : swB.w;
+                        EB = __viaddmax_s16x2(EB, NE, hlB);
+                        F[c] = __viaddmax_s16x2(F[c], NE, Hm[c]);
+                        const uint32_t dcur = dB;
+                        if ((c & 3) == 3) {
+                            if (c + 1 < T) {
+                                swB = prowB[(c + 1) / 4];
+                                dB = __vadd2(Hm[c], swB.x);
+                            }
+                        } else {
+                            dB = __vadd2(Hm[c], sB);
+                        }
+                        hlB = __vadd2(__vimax3_s16x2_relu(dcur, EB, F[c]), NO);
+                        Hm[c] = hlB;
+                        // the running maximum over the diagonal terms (exact, see sweep_unit_s16): one VIMNMX3 per two cells
+                        best = k < T ? __vimax3_s16x2(best, seenA, dcur) : __vmaxs2(best, dcur);
+                    }
                 }
-                if (!last) *reinterpret_cast<uint2*>(bout + r * 256) = make_uint2(hl, E);
+                if (!last) {
+                    *reinterpret_cast<uint2*>(bout + rp * 256) = make_uint2(hlA, EA);
+                    *reinterpret_cast<uint2*>(bout + (rp + 1) * 256) = make_uint2(hlB, EB);
+                }
             }
             __syncwarp();
             if (!first) {

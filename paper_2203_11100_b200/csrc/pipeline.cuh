@@ -36,6 +36,10 @@ constexpr uint32_t kPipeWarps = kInterThreads / 32;
 constexpr uint32_t kPipeItemRing = 64;                   // CTA-local ring of fetched items
 constexpr uint32_t kPipeChunkBytes = kRowsPerChunk * 32 * 8;   // one chunk of border rows: 8 rows x 32 lanes x (Hm, E)
 constexpr uint32_t kPipeEnd = 0xFFFFFFFFu;
+#ifndef SWB_PIPE_POLL_NS
+#define SWB_PIPE_POLL_NS 20
+#endif
+constexpr uint32_t kPipePollNs = SWB_PIPE_POLL_NS;   // back-off between two looks at a ring counter
 
 struct PipeParams {
     const uint4* codes;
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
                         // published, so that from here on the next chunk can always be requested while this one is
                         // being consumed
                         const uint32_t need = min(in_pos + 2, in_end);
-                        SWB_STAT(w_in, while (lds_acquire(&ctl->head[0]) < need) __nanosleep(20));
+                        SWB_STAT(w_in, while (lds_acquire(&ctl->head[0]) < need) __nanosleep(kPipePollNs));
                         stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
                                     gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
                         ++staged;
@@ -219,11 +223,11 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
                 } else {
                     // A tile starts `lag` chunks behind its left neighbour: a cushion against scheduling jitter.
                     const uint32_t need = min(chunk == 0 ? in_pos + lag : in_pos + 1, in_end);
-                    SWB_STAT(w_in, while (lds_acquire(&ctl->head[warp]) < need) __nanosleep(20));
+                    SWB_STAT(w_in, while (lds_acquire(&ctl->head[warp]) < need) __nanosleep(kPipePollNs));
                 }
             }
             if (!last && !wrap_out)
-                SWB_STAT(w_out, while (out_pos - lds_acquire(&ctl->tail[next]) >= p.ring_chunks) __nanosleep(20));
+                SWB_STAT(w_out, while (out_pos - lds_acquire(&ctl->tail[next]) >= p.ring_chunks) __nanosleep(kPipePollNs));
             const uint2* bin = reinterpret_cast<const uint2*>(ring_in + (in_pos & ring_mask) * kPipeChunkBytes);
             uint8_t* bout = wrap_out ? gborder + static_cast<size_t>(chunk) * kPipeChunkBytes
                                      : ring_out + (out_pos & ring_mask) * kPipeChunkBytes;
