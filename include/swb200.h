@@ -296,6 +296,14 @@ swb_status swb_scan_plan(const uint32_t* lens, uint32_t n, uint64_t length_thres
                          uint32_t shard_count, uint32_t query_len, uint32_t sm_count, int32_t policy,
                          swb_scan_plan_info* out);
 
+/* How swb_search_many would group a batch of queries (host arithmetic only, no device needed; for tests and
+ * tuning): scan_of_query[q] = number of the shared scan query q takes part in, or -1 when it is searched on its own;
+ * stream_of_query[q] = 0 / 1 for the stream (int16 half) it is laid out in, -1 when on its own.  Assumes a matrix
+ * and gap model the packed int16 kernels accept (BLOSUM-like). */
+swb_status swb_batch_plan(const uint32_t* lens, uint32_t n, uint64_t length_threshold, uint32_t shard_rank,
+                          uint32_t shard_count, const uint32_t* query_lens, uint32_t n_queries, uint32_t sm_count,
+                          int32_t* scan_of_query, int32_t* stream_of_query);
+
 #ifdef __cplusplus
 }
 #endif

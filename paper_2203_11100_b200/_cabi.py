@@ -123,6 +123,7 @@ SIGNATURES = {
     "swb_mdb_shard": (C.c_void_p, [C.c_void_p, C.c_uint32]),
     "swb_measure_pipe_rates": (C.c_int, [C.c_int32, C.c_double, C.POINTER(SwbPipeRates)]),
     "swb_shard_assignment": (C.c_int, [u32p, C.c_uint32, C.c_uint64, C.c_uint32, u32p]),
+    "swb_batch_plan": (C.c_int, [u32p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, u32p, C.c_uint32, C.c_uint32, i32p, i32p]),
     "swb_scan_plan": (C.c_int, [u32p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int32,
                                 C.POINTER(SwbScanPlanInfo)]),
 }

@@ -393,7 +393,7 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
     };
     std::vector<DuoScan> scans;
     std::vector<uint32_t> single;
-    plan_duo_scans(db, query_lens, n_queries, matrix, gap_open, gap_extend, scans, single);
+    plan_batch(scan_knobs(), duo_enabled(db, matrix, gap_open, gap_extend), query_lens, n_queries, scans, single);
     std::vector<Job> jobs;
     for (size_t i = 0; i < scans.size(); ++i) jobs.push_back(Job{static_cast<int>(i), 0});
     for (uint32_t q : single) jobs.push_back(Job{-1, q});
@@ -598,6 +598,32 @@ swb_status swb_scan_plan(const uint32_t* lens, uint32_t n, uint64_t length_thres
     out->chain_bound = sp.chain_bound ? 1 : 0;
     out->wavefront_rows = sp.wave_rows;
     out->pipeline_rows = padded_rows - sp.wave_rows;
+    return SWB_OK;
+}
+
+swb_status swb_batch_plan(const uint32_t* lens, uint32_t n, uint64_t length_threshold, uint32_t shard_rank, uint32_t shard_count,
+                          const uint32_t* query_lens, uint32_t n_queries, uint32_t sm_count, int32_t* scan_of_query,
+                          int32_t* stream_of_query) {
+    if ((n && !lens) || (n_queries && (!query_lens || !scan_of_query || !stream_of_query))) return fail(SWB_ERR_INVALID, "null argument");
+    if (shard_count < 1 || shard_rank >= shard_count) return fail(SWB_ERR_INVALID, "shard_rank must be < shard_count");
+    if (sm_count < 1) return fail(SWB_ERR_INVALID, "sm_count must be >= 1");
+    SeqSource src;
+    static const uint32_t kNoLens[1] = {0};
+    src.lens = n ? lens : kNoLens;
+    src.n = n;
+    std::vector<GroupDesc> groups;
+    uint64_t padded_rows = 0;
+    group_table(src, length_threshold, shard_rank, shard_count, groups, &padded_rows);
+    const uint32_t max_rows = groups.empty() ? 0 : groups[0].n_chunks * kRowsPerChunk;
+    const bool enabled = shared_scans_fit(scan_knobs(), static_cast<uint32_t>(groups.size()), max_rows, padded_rows, sm_count);
+    std::vector<DuoScan> scans;
+    std::vector<uint32_t> single;
+    plan_batch(scan_knobs(), enabled, query_lens, n_queries, scans, single);
+    for (uint32_t q : single) scan_of_query[q] = -1, stream_of_query[q] = -1;
+    for (size_t i = 0; i < scans.size(); ++i) {
+        for (uint32_t q : scans[i].a) scan_of_query[q] = static_cast<int32_t>(i), stream_of_query[q] = 0;
+        for (uint32_t q : scans[i].b) scan_of_query[q] = static_cast<int32_t>(i), stream_of_query[q] = 1;
+    }
     return SWB_OK;
 }
 

@@ -2,14 +2,6 @@
 
 namespace {
 
-// One shared scan: the two streams of queries (numbers into the caller's arrays), each in the order they are laid out.
-struct DuoScan {
-    std::vector<uint32_t> a, b;
-    uint32_t tiles_a = 0, tiles_b = 0;
-};
-
-inline uint32_t tiles_of(uint32_t m) { return (m + kInterTile - 1) / kInterTile; }
-
 // Scores every local sequence against every query of the scan; query number `scan_queries[i]` (a's members first, then
 // b's) gets the score array d_multi_scores + i * n_slots and the device copy d_multi_codes + code_off[i].
 // Asynchronous on db->stream.  Requires the packed int16 path (matrix + open within int8).
@@ -178,62 +170,12 @@ swb_status finish_duo_query(swb_db* db, const uint8_t* q_dev, uint32_t m, const 
     return select_topk(db, db->d_keys, db->n_slots, top_k, d_out);
 }
 
-// Can queries of this batch share scans at all on this handle?
-bool duo_enabled(const swb_db* db) {
-    const ScanKnobs& k = scan_knobs();
-    if (k.duo_ratio > 1.0 || db->scan_policy != SWB_SCAN_AUTO || db->force_intra) return false;
-    if (static_cast<double>(db->meta.groups.size()) < k.duo_min_groups_per_sm * static_cast<double>(db->sm_count)) return false;
-    // every half-group is one CTA's item here: the tallest must fit a CTA's fair share of the scan (small shards of a
-    // database with a few very long sequences do not; their searches go one by one, where the tall groups get the
-    // wavefront kernel)
-    return static_cast<double>(db->max_rows) * db->sm_count <= k.duo_tall * 2.0 * static_cast<double>(db->meta.padded_rows);
-}
-
-// Deals the eligible queries of a batch over shared scans: longest first, each to the shortest stream so far, so that
-// the two streams of a scan end up equally long.  A scan whose streams differ too much (the padding would eat the
-// two-stream kernel's ~15 % advantage) or that is too short to keep the pipeline busy is dissolved again: its queries
-// go one by one.  `single` receives every query that is not part of a scan.
-void plan_duo_scans(const swb_db* db, const uint32_t* lens, uint32_t n_queries, const int32_t* matrix, int32_t open, int32_t ext,
-                    std::vector<DuoScan>& scans, std::vector<uint32_t>& single) {
-    scans.clear();
-    single.clear();
-    const ScanKnobs& k = scan_knobs();
-    std::vector<uint32_t> eligible;
-    const bool enabled = duo_enabled(db) && make_plan(db, 64, matrix, open, ext).main == kMainS16;
-    for (uint32_t q = 0; q < n_queries; ++q) (enabled && lens[q] > 0 ? eligible : single).push_back(q);
-    if (eligible.size() < 2) {
-        single.insert(single.end(), eligible.begin(), eligible.end());
-        std::sort(single.begin(), single.end());
-        return;
-    }
-    std::stable_sort(eligible.begin(), eligible.end(), [&](uint32_t x, uint32_t y) { return lens[x] > lens[y]; });
-    uint64_t total_tiles = 0;
-    for (uint32_t q : eligible) total_tiles += tiles_of(lens[q]);
-    const uint32_t n_scans = static_cast<uint32_t>((total_tiles + 2ull * k.duo_stream_tiles - 1) / (2ull * k.duo_stream_tiles));
-    scans.resize(n_scans);
-    for (uint32_t q : eligible) {
-        DuoScan* best = nullptr;
-        bool high = false;
-        uint32_t least = ~0u;
-        for (DuoScan& sc : scans) {
-            if (sc.tiles_a < least) least = sc.tiles_a, best = &sc, high = false;
-            if (sc.tiles_b < least) least = sc.tiles_b, best = &sc, high = true;
-        }
-        (high ? best->b : best->a).push_back(q);
-        (high ? best->tiles_b : best->tiles_a) += tiles_of(lens[q]);
-    }
-    std::vector<DuoScan> kept;
-    for (DuoScan& sc : scans) {
-        const uint32_t lo = std::min(sc.tiles_a, sc.tiles_b), hi = std::max(sc.tiles_a, sc.tiles_b);
-        if (lo == 0 || static_cast<double>(lo) < k.duo_ratio * static_cast<double>(hi) || hi < k.pipe_min_tiles) {
-            single.insert(single.end(), sc.a.begin(), sc.a.end());
-            single.insert(single.end(), sc.b.begin(), sc.b.end());
-        } else {
-            kept.push_back(std::move(sc));
-        }
-    }
-    scans.swap(kept);
-    std::sort(single.begin(), single.end());
+// Can queries of a batch share scans at all on this handle?  (The rest of the decision is plan_batch in scan_plan.hpp.)
+bool duo_enabled(const swb_db* db, const int32_t* matrix, int32_t open, int32_t ext) {
+    if (db->scan_policy != SWB_SCAN_AUTO || db->force_intra) return false;
+    if (make_plan(db, 64, matrix, open, ext).main != kMainS16) return false;
+    return shared_scans_fit(scan_knobs(), static_cast<uint32_t>(db->meta.groups.size()), db->max_rows, db->meta.padded_rows,
+                            static_cast<uint32_t>(db->sm_count));
 }
 
 }  // namespace

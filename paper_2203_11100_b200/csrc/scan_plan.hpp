@@ -33,6 +33,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "pack.hpp"
 
@@ -251,6 +252,70 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
     unit_start[n_wave] = pl.n_units;
     for (uint32_t g = n_wave + 1; g <= n_groups; ++g) unit_start[g] = pl.n_units;
     return pl;
+}
+
+// ---- batches of queries (swb_search_many) -------------------------------------------------------------------------
+
+// One shared scan: the two streams of queries (numbers into the caller's arrays), each in the order they are laid out.
+struct DuoScan {
+    std::vector<uint32_t> a, b;
+    uint32_t tiles_a = 0, tiles_b = 0;
+};
+
+inline uint32_t tiles_of(uint32_t m) { return (m + 31) / 32; }
+
+// Shared scans give every half-group to one CTA: the database needs enough groups per SM, and its tallest group must
+// fit a CTA's fair share of the scan (small shards of a database with a few very long sequences do not; their
+// searches go one by one, where the tall groups get the wavefront kernel).
+inline bool shared_scans_fit(const ScanKnobs& k, uint32_t n_groups, uint32_t max_rows, uint64_t padded_rows, uint32_t sm_count) {
+    if (k.duo_ratio > 1.0) return false;
+    if (static_cast<double>(n_groups) < k.duo_min_groups_per_sm * static_cast<double>(sm_count)) return false;
+    return static_cast<double>(max_rows) * sm_count <= k.duo_tall * 2.0 * static_cast<double>(padded_rows);
+}
+
+// Deals the queries of a batch over shared scans: longest first, each to the shortest stream so far, so that the two
+// streams of a scan end up equally long.  A scan whose streams differ too much (the padding would eat the two-stream
+// kernel's ~15 % advantage) or that is too short to keep the pipeline busy is dissolved again: its queries go one by
+// one.  `single` receives every query that is not part of a scan (empty queries, and all of them when !enabled).
+inline void plan_batch(const ScanKnobs& k, bool enabled, const uint32_t* lens, uint32_t n_queries, std::vector<DuoScan>& scans,
+                       std::vector<uint32_t>& single) {
+    scans.clear();
+    single.clear();
+    std::vector<uint32_t> eligible;
+    for (uint32_t q = 0; q < n_queries; ++q) (enabled && lens[q] > 0 ? eligible : single).push_back(q);
+    if (eligible.size() < 2) {
+        single.insert(single.end(), eligible.begin(), eligible.end());
+        std::sort(single.begin(), single.end());
+        return;
+    }
+    std::stable_sort(eligible.begin(), eligible.end(), [&](uint32_t x, uint32_t y) { return lens[x] > lens[y]; });
+    uint64_t total_tiles = 0;
+    for (uint32_t q : eligible) total_tiles += tiles_of(lens[q]);
+    const uint32_t n_scans = static_cast<uint32_t>((total_tiles + 2ull * k.duo_stream_tiles - 1) / (2ull * k.duo_stream_tiles));
+    scans.resize(n_scans);
+    for (uint32_t q : eligible) {
+        DuoScan* best = nullptr;
+        bool high = false;
+        uint32_t least = ~0u;
+        for (DuoScan& sc : scans) {
+            if (sc.tiles_a < least) least = sc.tiles_a, best = &sc, high = false;
+            if (sc.tiles_b < least) least = sc.tiles_b, best = &sc, high = true;
+        }
+        (high ? best->b : best->a).push_back(q);
+        (high ? best->tiles_b : best->tiles_a) += tiles_of(lens[q]);
+    }
+    std::vector<DuoScan> kept;
+    for (DuoScan& sc : scans) {
+        const uint32_t lo = std::min(sc.tiles_a, sc.tiles_b), hi = std::max(sc.tiles_a, sc.tiles_b);
+        if (lo == 0 || static_cast<double>(lo) < k.duo_ratio * static_cast<double>(hi) || hi < k.pipe_min_tiles) {
+            single.insert(single.end(), sc.a.begin(), sc.a.end());
+            single.insert(single.end(), sc.b.begin(), sc.b.end());
+        } else {
+            kept.push_back(std::move(sc));
+        }
+    }
+    scans.swap(kept);
+    std::sort(single.begin(), single.end());
 }
 
 // Capacity of each border ring (chunks, a power of two) that fits next to a profile of `prof_bytes` in

@@ -349,6 +349,21 @@ def scan_plan(lengths, query_len: int, sm_count: int = 148, length_threshold: in
     return info.as_dict()
 
 
+def batch_plan(lengths, query_lengths, sm_count: int = 148, length_threshold: int = 3000, shard_rank: int = 0,
+               shard_count: int = 1):
+    """How swb_search_many would group a batch of queries (swb_batch_plan; host only): (scan_of_query, stream_of_query),
+    -1 where a query is searched on its own."""
+    lib = _cabi.load()
+    lens = np.ascontiguousarray(np.asarray(lengths, dtype=np.uint32))
+    ql = np.ascontiguousarray(np.asarray(query_lengths, dtype=np.uint32))
+    scan = np.full(max(1, len(ql)), -2, dtype=np.int32)
+    stream = np.full(max(1, len(ql)), -2, dtype=np.int32)
+    rc = lib.swb_batch_plan(_ptr(lens, _u32p), len(lens), int(length_threshold) & (2 ** 64 - 1), shard_rank, shard_count,
+                            _ptr(ql, _u32p), len(ql), sm_count, _ptr(scan, _i32p), _ptr(stream, _i32p))
+    _raise(lib, rc)
+    return scan[:len(ql)], stream[:len(ql)]
+
+
 def measure_pipe_rates(device: int = 0, seconds: float = 1.0) -> dict:
     lib = _cabi.load()
     r = _cabi.SwbPipeRates()

@@ -192,3 +192,30 @@ def test_scan_plan_policies_and_small_databases(lib):
         search.scan_plan(lens, 100, shard_rank=2, shard_count=2)
     with pytest.raises(ValueError, match="scan policy"):
         search.scan_plan(lens, 100, policy=7)
+
+
+def test_batch_plan_deals_queries_over_two_balanced_streams(lib):
+    """swb_search_many's grouping of a batch (plan_batch in scan_plan.hpp, previewed by swb_batch_plan): the config-2
+    sweep becomes one shared scan whose two streams differ by a few tiles; dissimilar pairs, empty queries, small
+    databases and shards whose tallest group exceeds a CTA's fair share fall back to one search per query."""
+    lens = _swissprot_lengths()
+    scan, stream = search.batch_plan(lens, synth.QUERY_LENGTHS)
+    assert (scan == 0).all() and set(stream.tolist()) == {0, 1}
+    tiles = np.array([(m + 31) // 32 for m in synth.QUERY_LENGTHS])
+    a, b = tiles[stream == 0].sum(), tiles[stream == 1].sum()
+    assert a + b == tiles.sum() and abs(int(a) - int(b)) <= tiles.min()
+    # many queries: several scans, each under the stream limit, every query placed exactly once
+    many = [int(x) for x in np.random.default_rng(5).integers(100, 6000, size=80)]
+    scan, stream = search.batch_plan(lens, many)
+    assert (scan >= 0).all() and scan.max() >= 1
+    for s in range(scan.max() + 1):
+        for half in (0, 1):
+            assert sum((m + 31) // 32 for m, sc, st in zip(many, scan, stream) if sc == s and st == half) <= 704 + 188
+    # two queries of very different length do not share a scan; an empty query never does
+    assert search.batch_plan(lens, [5000, 300])[0].tolist() == [-1, -1]
+    assert search.batch_plan(lens, [5000, 4000, 0, 100])[0].tolist() == [0, 0, -1, 0]
+    assert search.batch_plan(lens, [100, 120])[0].tolist() == [-1, -1]            # fewer than 9 tiles per stream
+    # small database / half of the database (its 35,213-row group no longer fits a CTA's share): one search per query
+    assert (search.batch_plan(lens[:10_000], synth.QUERY_LENGTHS)[0] == -1).all()
+    assert (search.batch_plan(lens, synth.QUERY_LENGTHS, shard_count=2)[0] == -1).all()
+    assert (search.batch_plan(np.minimum(lens, 2999), synth.QUERY_LENGTHS, shard_count=8)[0] == 0).all()   # no tall groups: shards share too
