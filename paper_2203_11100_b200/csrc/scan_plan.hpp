@@ -304,6 +304,41 @@ inline void plan_batch(const ScanKnobs& k, bool enabled, const uint32_t* lens, u
         (high ? best->b : best->a).push_back(q);
         (high ? best->tiles_b : best->tiles_a) += tiles_of(lens[q]);
     }
+    // then split each scan's queries as evenly as possible: subset sum over their tile counts (a few hundred
+    // tiles per scan at most, so the table is tiny)
+    for (DuoScan& sc : scans) {
+        std::vector<uint32_t> members(sc.a);
+        members.insert(members.end(), sc.b.begin(), sc.b.end());
+        std::stable_sort(members.begin(), members.end(), [&](uint32_t x, uint32_t y) { return lens[x] > lens[y]; });
+        const uint32_t total = sc.tiles_a + sc.tiles_b;
+        // ok[s]: some subset of the members seen so far has s tiles; reach[s]: the member that first made it so (sums
+        // are walked downwards, so ok[s - t] still refers to the members before the current one)
+        std::vector<uint32_t> reach(total / 2 + 1, 0);
+        std::vector<uint8_t> ok(total / 2 + 1, 0);
+        ok[0] = 1;
+        for (size_t i = 0; i < members.size(); ++i) {
+            const uint32_t t = tiles_of(lens[members[i]]);
+            for (uint32_t sum = total / 2; sum >= t; --sum)
+                if (!ok[sum] && ok[sum - t]) {
+                    ok[sum] = 1;
+                    reach[sum] = static_cast<uint32_t>(i);
+                }
+        }
+        uint32_t best = total / 2;
+        while (best > 0 && !ok[best]) --best;
+        std::vector<uint8_t> in_a(members.size(), 0);
+        for (uint32_t sum = best; sum > 0;) {
+            const uint32_t i = reach[sum];
+            in_a[i] = 1;
+            sum -= tiles_of(lens[members[i]]);
+        }
+        sc.a.clear(), sc.b.clear();
+        sc.tiles_a = sc.tiles_b = 0;
+        for (size_t i = 0; i < members.size(); ++i) {
+            (in_a[i] ? sc.a : sc.b).push_back(members[i]);
+            (in_a[i] ? sc.tiles_a : sc.tiles_b) += tiles_of(lens[members[i]]);
+        }
+    }
     std::vector<DuoScan> kept;
     for (DuoScan& sc : scans) {
         const uint32_t lo = std::min(sc.tiles_a, sc.tiles_b), hi = std::max(sc.tiles_a, sc.tiles_b);

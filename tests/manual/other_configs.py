@@ -48,3 +48,12 @@ else:
             print(f"  m={len(q)} GCUPS={st['cells']/st['ms_total']/1e6:.1f} ms={st['ms_total']:.1f} rescored={st['rescored_i32']} rescore_ms={st['ms_rescore']:.2f} top={idx[0]}:{sc[0]} planted={exact} exact_vs_oracle={ok}")
         print(f"  aggregate {tc/tt/1e6:.1f} GCUPS, sequences re-run in int32: {flagged}")
         assert flagged > 0
+        # the same queries as one batch (shared scans), checked against the single searches
+        batch = [queries[qi] for qi in (0, 9, 17, 18, 19, 20, 21)]
+        singles = [db.search(q, b50, g, 10)[:2] for q in batch]
+        db.search_many(batch, b50, g, 10)
+        many, ms = db.search_many(batch, b50, g, 10)
+        same = all((a[0] == b[0]).all() and (a[1] == b[1]).all() for a, b in zip(many, singles))
+        cells = sum(len(q) for q in batch) * sdb.residues
+        print(f"  batched (swb_search_many): {cells/ms.sum()/1e6:.1f} GCUPS, ranked lists equal to the single searches: {same}")
+        assert same
