@@ -1,6 +1,4 @@
-// duo.inl -- two streams of queries per scan (duo.cuh): host side.  Included by cabi.cu inside extern "C".
-
-namespace {
+// duo.inl -- two streams of queries per scan (duo.cuh): host side.  Included by cabi.cu inside its anonymous namespace.
 
 // Scores every local sequence against every query of the scan; query number `scan_queries[i]` (a's members first, then
 // b's) gets the score array d_multi_scores + i * n_slots and the device copy d_multi_codes + code_off[i].
@@ -176,48 +174,4 @@ bool duo_enabled(const swb_db* db, const int32_t* matrix, int32_t open, int32_t 
     if (make_plan(db, 64, matrix, open, ext).main != kMainS16) return false;
     return shared_scans_fit(scan_knobs(), static_cast<uint32_t>(db->meta.groups.size()), db->max_rows, db->meta.padded_rows,
                             static_cast<uint32_t>(db->sm_count));
-}
-
-}  // namespace
-
-// All scores of two queries from one scan, before any int32 re-run (tests/manual/duo_experiment.py: kernel parity and timing).
-swb_status swb_score_all_duo(swb_db* db, const uint8_t* qa, uint32_t ma, const uint8_t* qb, uint32_t mb, const int32_t* matrix,
-                             int32_t gap_open, int32_t gap_extend, int32_t* scores_a, int32_t* scores_b, swb_stats* stats) {
-    if (!db || !scores_a || !scores_b) return fail(SWB_ERR_INVALID, "null argument");
-    swb_status st = check_scoring_args(qa, ma, matrix, gap_open, gap_extend);
-    if (st == SWB_OK) st = check_scoring_args(qb, mb, matrix, gap_open, gap_extend);
-    if (st != SWB_OK) return st;
-    if (ma == 0 || mb == 0) return fail(SWB_ERR_INVALID, "empty query");
-    std::lock_guard<std::mutex> lock(db->mu);
-    DeviceGuard guard(db->device);
-    const QueryPlan pl = make_plan(db, std::max(ma, mb), matrix, gap_open, gap_extend);
-    if (pl.main != kMainS16) return fail(SWB_ERR_UNSUPPORTED, "the shared scan needs the packed int16 path");
-    const uint8_t* two[2] = {qa, qb};
-    const uint32_t two_len[2] = {ma, mb};
-    DuoScan scan;
-    scan.a = {0};
-    scan.b = {1};
-    scan.tiles_a = tiles_of(ma);
-    scan.tiles_b = tiles_of(mb);
-    std::vector<uint32_t> order, code_off;
-    st = score_streams_core(db, two, two_len, scan, matrix, gap_open, gap_extend, order, code_off);
-    if (st != SWB_OK) return st;
-    cudaStream_t s = db->stream;
-    const uint32_t n_total = db->meta.n_total;
-    if (!db->d_all_scores)
-        if ((st = dev_alloc(&db->d_all_scores, n_total, &db->device_bytes)) != SWB_OK) return st;
-    const unsigned blocks = std::max(1u, std::min(1024u, (db->n_slots + 255) / 256));
-    int32_t* outs[2] = {scores_a, scores_b};
-    for (int q = 0; q < 2; ++q) {
-        SWB_CUDA(cudaMemcpyAsync(db->d_all_scores, outs[q], static_cast<size_t>(n_total) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-        if (db->n_slots)
-            scatter_scores_kernel<<<blocks, 256, 0, s>>>(db->d_multi_scores + static_cast<size_t>(q) * db->n_slots, db->d_slot_index,
-                                                          db->n_slots, db->d_all_scores);
-        SWB_CUDA(cudaMemcpyAsync(outs[q], db->d_all_scores, static_cast<size_t>(n_total) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    }
-    SWB_CUDA(cudaEventRecord(db->ev[EV_TOPK], s));
-    SWB_CUDA(cudaEventRecord(db->ev[EV_END], s));
-    SWB_CUDA(cudaStreamSynchronize(s));
-    fill_stats(db, ma + mb, stats);
-    return SWB_OK;
 }
