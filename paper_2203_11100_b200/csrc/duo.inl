@@ -102,31 +102,12 @@ swb_status score_streams_core(swb_db* db, const uint8_t* const* queries, const u
     }
     const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(static_cast<uint32_t>(db->sm_count), dp.n_items));
 #ifdef SWB_PIPE_STATS
-    static unsigned long long* d_stats = nullptr;   // debug builds only: where do the warps wait?
-    if (!d_stats) cudaMalloc(&d_stats, sizeof(unsigned long long) * 4 * kPipeWarps * 1024);
-    cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4 * kPipeWarps * 1024, s);
-    dp.stats = d_stats;
+    dp.stats = pipe_stats_buffer(s);
 #endif
     duo_pipeline_kernel<kInterTile, kInterThreads><<<grid, kInterThreads, smem, s>>>(dp);
     ++db->launches;
 #ifdef SWB_PIPE_STATS
-    {
-        std::vector<unsigned long long> h(static_cast<size_t>(grid) * kPipeWarps * 4);
-        cudaStreamSynchronize(s);
-        cudaMemcpy(h.data(), d_stats, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-        double tot[kPipeWarps][4] = {};
-        for (uint32_t c = 0; c < grid; ++c)
-            for (uint32_t w = 0; w < kPipeWarps; ++w)
-                for (int k2 = 0; k2 < 4; ++k2) tot[w][k2] += static_cast<double>(h[(static_cast<size_t>(c) * kPipeWarps + w) * 4 + k2]);
-        std::fprintf(stderr, "duo stats tiles=%u grid=%u: warp  wait_in%%  wait_out%%  item%%\n", n_tiles, grid);
-        double si = 0, so = 0;
-        for (uint32_t w = 0; w < kPipeWarps; ++w) {
-            std::fprintf(stderr, "   %2u  %6.2f  %6.2f  %6.2f   life %.2f ms\n", w, 100 * tot[w][0] / tot[w][3], 100 * tot[w][1] / tot[w][3],
-                         100 * tot[w][2] / tot[w][3], tot[w][3] / grid / 1.9e6);
-            si += 100 * tot[w][0] / tot[w][3] / kPipeWarps, so += 100 * tot[w][1] / tot[w][3] / kPipeWarps;
-        }
-        std::fprintf(stderr, "   mean wait_in %.2f%% wait_out %.2f%%\n", si, so);
-    }
+    report_pipe_stats("two-stream", dp.stats, grid, n_tiles, s);
 #endif
     SWB_CUDA(cudaEventRecord(db->ev[EV_SCAN], s));
     SWB_CUDA(cudaEventRecord(db->ev[EV_RESCORE], s));

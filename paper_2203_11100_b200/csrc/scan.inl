@@ -53,6 +53,60 @@ swb_status run_intra(swb_db* db, const QueryPlan& pl, const uint32_t* list, cuda
     return SWB_OK;
 }
 
+#ifdef SWB_PIPE_STATS
+// Debug builds only (SWB_PIPE_STATS): where do the warps of a pipeline kernel wait?  [cta][warp][4] clocks.
+unsigned long long* pipe_stats_buffer(cudaStream_t s) {
+    static unsigned long long* d_stats = nullptr;
+    if (!d_stats) cudaMalloc(&d_stats, sizeof(unsigned long long) * 4 * kPipeWarps * 1024);
+    cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4 * kPipeWarps * 1024, s);
+    return d_stats;
+}
+
+void report_pipe_stats(const char* what, const unsigned long long* d_stats, uint32_t grid, uint32_t n_tiles, cudaStream_t s) {
+    std::vector<unsigned long long> h(static_cast<size_t>(grid) * kPipeWarps * 4);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), d_stats, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    double tot[kPipeWarps][4] = {};
+    for (uint32_t c = 0; c < grid; ++c)
+        for (uint32_t w = 0; w < kPipeWarps; ++w)
+            for (int k = 0; k < 4; ++k) tot[w][k] += static_cast<double>(h[(static_cast<size_t>(c) * kPipeWarps + w) * 4 + k]);
+    std::fprintf(stderr, "%s stats tiles=%u grid=%u: warp  wait_in%%  wait_out%%  item%%  (of the warp's lifetime)\n", what, n_tiles, grid);
+    double sum_in = 0, sum_out = 0;
+    for (uint32_t w = 0; w < kPipeWarps; ++w) {
+        std::fprintf(stderr, "   %2u  %6.2f  %6.2f  %6.2f   life %.2f ms\n", w, 100 * tot[w][0] / tot[w][3], 100 * tot[w][1] / tot[w][3],
+                     100 * tot[w][2] / tot[w][3], tot[w][3] / grid / 1.9e6);
+        sum_in += 100 * tot[w][0] / tot[w][3] / kPipeWarps, sum_out += 100 * tot[w][1] / tot[w][3] / kPipeWarps;
+    }
+    std::fprintf(stderr, "   mean wait_in %.2f%% wait_out %.2f%%\n", sum_in, sum_out);
+}
+#endif
+
+// The wavefront kernel.  The narrow-tile and row-block paths are only compiled into the variants that need them, so
+// that the plain 32-column sweep keeps its register allocation; a profile too large for shared memory is read from
+// global memory.
+swb_status launch_wavefront(swb_db* db, const WaveParams& wp, uint32_t grid, uint32_t threads, size_t smem, bool narrow,
+                            bool rowblock, cudaStream_t s) {
+    const bool in_smem = smem <= db->smem_optin;
+#define SWB_LAUNCH_S16(NARROW, RB)                                                                                 \
+    {                                                                                                              \
+        if (in_smem) {                                                                                             \
+            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB>,       \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,                             \
+                                          static_cast<int>(db->smem_optin)));                                      \
+            wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB><<<grid, threads, smem, s>>>(wp);      \
+        } else {                                                                                                   \
+            wavefront_s16_kernel<false, kInterTile, kInterThreads, NARROW, RB><<<grid, threads, 0, s>>>(wp);        \
+        }                                                                                                          \
+    }
+    if (narrow && rowblock) SWB_LAUNCH_S16(true, true)
+    else if (narrow) SWB_LAUNCH_S16(true, false)
+    else if (rowblock) SWB_LAUNCH_S16(false, true)
+    else SWB_LAUNCH_S16(false, false)
+#undef SWB_LAUNCH_S16
+    ++db->launches;
+    return SWB_OK;
+}
+
 // Scores every local sequence; results land in d_slot_scores.  Asynchronous on db->stream.
 swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_t* matrix, int32_t open,
                       int32_t ext) {
@@ -197,10 +251,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         const uint32_t wave_grid = pipe_first ? wave_sms : 0;
         const uint32_t side_grid = std::min<uint32_t>(static_cast<uint32_t>(db->sm_count) - wave_grid, n_pipe_items);
 #ifdef SWB_PIPE_STATS
-        static unsigned long long* d_stats = nullptr;   // debug builds only: where do the pipeline's warps wait?
-        if (!d_stats) cudaMalloc(&d_stats, sizeof(unsigned long long) * 4 * kPipeWarps * 1024);
-        cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 4 * kPipeWarps * 1024, s);
-        qp.stats = d_stats;
+        qp.stats = pipe_stats_buffer(s);
 #endif
         if (wave_grid) {
             SWB_CUDA(cudaEventRecord(db->ev_fork, s));
@@ -233,31 +284,9 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.ticket = db->d_counters;
         wp.neg_open2 = pack16(-open);
         wp.neg_ext2 = pack16(-ext);
-        const size_t smem = prof_elems;
         const uint32_t warps_per_cta = wave_threads / 32;
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(wave_sms, (n_units + warps_per_cta - 1) / warps_per_cta));
-        const bool in_smem = smem <= db->smem_optin;
-        {
-#define SWB_LAUNCH_S16(NARROW, RB)                                                                                 \
-    {                                                                                                              \
-        if (in_smem) {                                                                                             \
-            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB>,       \
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,                             \
-                                          static_cast<int>(db->smem_optin)));                                      \
-            wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB><<<grid, wave_threads, smem, s>>>(wp); \
-        } else {                                                                                                   \
-            wavefront_s16_kernel<false, kInterTile, kInterThreads, NARROW, RB><<<grid, wave_threads, 0, s>>>(wp); \
-        }                                                                                                          \
-    }
-            // the narrow-tile and row-block paths are only compiled into the variants that need them, so that the
-            // plain 32-column sweep keeps its register allocation
-            if (any_narrow && any_rowblock) SWB_LAUNCH_S16(true, true)
-            else if (any_narrow) SWB_LAUNCH_S16(true, false)
-            else if (any_rowblock) SWB_LAUNCH_S16(false, true)
-            else SWB_LAUNCH_S16(false, false)
-#undef SWB_LAUNCH_S16
-        }
-        ++db->launches;
+        if ((st = launch_wavefront(db, wp, grid, wave_threads, prof_elems, any_narrow, any_rowblock, s)) != SWB_OK) return st;
         if (n_pipe_items) {
             // the wavefront kernel's SMs are free now: let them help with whatever pipeline items are left
             pipeline_s16_kernel<kInterTile, kInterThreads><<<grid, kInterThreads, pipe_smem, s>>>(qp);
@@ -266,25 +295,9 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         }
     }
 #ifdef SWB_PIPE_STATS
-    if (packed && n_pipe_items) {
-        const uint32_t grid = std::min<uint32_t>(static_cast<uint32_t>(db->sm_count) - (pipe_first ? wave_sms : 0), n_pipe_items);
-        std::vector<unsigned long long> h(static_cast<size_t>(grid) * kPipeWarps * 4);
-        cudaStreamSynchronize(s);
-        cudaMemcpy(h.data(), qp.stats, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-        double tot[kPipeWarps][4] = {};
-        for (uint32_t c = 0; c < grid; ++c)
-            for (uint32_t w = 0; w < kPipeWarps; ++w)
-                for (int k = 0; k < 4; ++k) tot[w][k] += static_cast<double>(h[(static_cast<size_t>(c) * kPipeWarps + w) * 4 + k]);
-        std::fprintf(stderr, "pipe stats m=%u tiles=%u ring=%u grid=%u: warp  wait_in%%  wait_out%%  item%%  (of the warp's lifetime)\n", m, n_tiles,
-                     qp.ring_chunks, grid);
-        double sum_in = 0, sum_out = 0;
-        for (uint32_t w = 0; w < kPipeWarps; ++w) {
-            std::fprintf(stderr, "   %2u  %6.2f  %6.2f  %6.2f   life %.2f ms\n", w, 100 * tot[w][0] / tot[w][3], 100 * tot[w][1] / tot[w][3],
-                         100 * tot[w][2] / tot[w][3], tot[w][3] / grid / 1.9e6);
-            sum_in += 100 * tot[w][0] / tot[w][3] / kPipeWarps, sum_out += 100 * tot[w][1] / tot[w][3] / kPipeWarps;
-        }
-        std::fprintf(stderr, "   mean wait_in %.2f%% wait_out %.2f%%\n", sum_in, sum_out);
-    }
+    if (packed && n_pipe_items)
+        report_pipe_stats("pipeline", qp.stats, std::min<uint32_t>(static_cast<uint32_t>(db->sm_count) - (pipe_first ? wave_sms : 0), n_pipe_items),
+                          n_tiles, s);
 #endif
     SWB_CUDA(cudaEventRecord(db->ev[EV_SCAN], s));
 
