@@ -474,3 +474,24 @@ def test_two_query_scan_against_the_oracle():
     out = subprocess.run([sys.executable, str(root / "tests" / "_duo_small.py")], cwd=root, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "DUO-SMALL-OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
+
+
+def test_large_random_batch_shares_scans_and_equals_single_searches(b62):
+    """A batch of 60 queries of random lengths (with duplicates, an empty one and a one-residue one) on a database
+    where shared scans apply: swb_search_many's ranked lists equal swb_search's, query by query, and the plan it
+    follows (swb_batch_plan) puts every non-empty query into a shared scan."""
+    from paper_2203_11100_b200 import batch_plan
+    rng = np.random.default_rng(91)
+    lens = [300, 450, 800, 1200, 950, 1400] + [int(x) for x in rng.integers(50, 3000, size=50)] + [777, 777, 0, 1]
+    queries = [synth.random_residues(rng, m) for m in lens]
+    sdb = synth.make_database(40_000, target_residues=11_000_000, max_len=1500, queries=queries[:6], seed=91)
+    scan, stream = batch_plan(sdb.lengths(), lens)
+    assert scan[58] == -1 and (scan[:58] >= 0).all() and scan[59] >= 0
+    g = GapModel(11, 1)
+    with Database(sdb.codes, sdb.offsets) as db:
+        many, ms = db.search_many(queries, b62, g, 7)
+        for qi in list(range(0, 60, 7)) + [56, 57, 58, 59]:
+            idx, sc, _ = db.search(queries[qi], b62, g, 7)
+            assert (many[qi][0] == idx).all() and (many[qi][1] == sc).all(), f"query {qi} (m={lens[qi]})"
+        for qi in range(6):
+            assert many[qi][0][0] == sdb.planted[qi][0]
