@@ -26,6 +26,19 @@ def exchange_keys(local_keys: np.ndarray, device: torch.device | None = None, gr
     return recv.cpu().numpy().view(np.uint64)
 
 
+def merge_many(gathered: np.ndarray, world: int, n_queries: int, top_k: int):
+    """`gathered` = the ranks' (n_queries x top_k) key blocks, concatenated rank by rank.  -> per query the merged
+    (db_index, score) list: descending key order is (score desc, index asc) (scheduler.hpp:111-114), 0 pads."""
+    from .search import decode_keys
+    blocks = np.asarray(gathered, dtype=np.uint64).reshape(world, n_queries, top_k)
+    out = []
+    for q in range(n_queries):
+        keys = blocks[:, q, :].reshape(-1)
+        keys = np.sort(keys[keys != 0])[::-1][:top_k]
+        out.append(decode_keys(keys))
+    return out
+
+
 class ShardedSearch:
     """This rank's shard of the database plus the cross-rank merge."""
 
@@ -48,6 +61,20 @@ class ShardedSearch:
         gathered = exchange_keys(keys, torch.device("cuda", self.device_index), self.group)
         idx, sc = merge_keys(gathered, top_k, device=self.device_index)
         return idx, sc, stats
+
+    def search_many(self, queries, matrix, gaps, top_k: int = 10):
+        """A batch of queries (swb_search_many on this rank's shard: shared scans where they apply), then ONE
+        all-gather of n_queries x top_k keys per rank instead of one per query.  -> list of (db_index, score),
+        identical on every rank, and this rank's per-query device ms."""
+        from .search import encode_keys
+        local, ms = self.db.search_many(queries, matrix, gaps, top_k)
+        if self.world == 1:
+            return local, ms
+        keys = np.zeros((len(queries), top_k), dtype=np.uint64)
+        for q, (idx, sc) in enumerate(local):
+            keys[q, :len(idx)] = encode_keys(idx, sc)
+        gathered = exchange_keys(keys.reshape(-1), torch.device("cuda", self.device_index), self.group)
+        return merge_many(gathered, self.world, len(queries), top_k), ms
 
     def close(self):
         self.db.close()

@@ -54,6 +54,17 @@ def _worker(rank, world, port, result_dir):
         full = po.FlatDb(sdb.codes, sdb.offsets)
         ei, es, _ = oracle.run_search(queries[0], full, b62, 10, 2, top_k=top_k)
         ok = (gi == ei).all() and (gs == es).all()
+        # the batched flavour: three queries, ONE all-gather of 3 x k keys per rank, merged per query (merge_many)
+        from paper_2203_11100_b200.dist import merge_many
+        batch = synth.make_queries([40, 75, 130], seed=78)
+        block = np.zeros((len(batch), top_k), dtype=np.uint64)
+        for qn, q in enumerate(batch):
+            bi, bs = oracle.merge(mine.astype(np.uint32), oracle.score_all(q, local, b62, 10, 2), top_k)
+            block[qn, :len(bi)] = search.encode_keys(bi, bs)
+        merged_many = merge_many(exchange_keys(block.reshape(-1)), world, len(batch), top_k)
+        for q, (mi, ms_) in zip(batch, merged_many):
+            ti, ts, _ = oracle.run_search(q, full, b62, 10, 2, top_k=top_k)
+            ok = ok and (mi == ti).all() and (ms_ == ts).all()
         np.save(os.path.join(result_dir, f"ok{rank}.npy"), np.array([int(ok), len(mine)]))
     finally:
         dist.destroy_process_group()
