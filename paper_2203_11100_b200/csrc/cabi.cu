@@ -143,6 +143,8 @@ struct swb_db {
     size_t duo_tiles_cap = 0;
     uint32_t* d_prof2 = nullptr;
     size_t prof2_cap = 0;
+    uint32_t* d_duo_progress = nullptr;  // pass items: [half-groups][passes]
+    size_t duo_progress_cap = 0;
     bool duo_attr_set = false;
 
     // query side
@@ -280,7 +282,7 @@ void swb_db_destroy(swb_db* db) {
         if (db->own_stream) cudaStreamSynchronize(db->own_stream);
         if (db->side_stream) cudaStreamSynchronize(db->side_stream);
         void* ptrs[] = {db->d_codes,      db->d_groups,   db->d_slot_index, db->d_slot_len,    db->d_border0,
-                        db->d_border1,    db->d_iborder0, db->d_iborder1, db->d_multi_scores, db->d_multi_codes, db->d_duo_tiles, db->d_prof2,   db->d_slot_scores, db->d_flag_list,
+                        db->d_border1,    db->d_iborder0, db->d_iborder1, db->d_multi_scores, db->d_multi_codes, db->d_duo_tiles, db->d_prof2, db->d_duo_progress,   db->d_slot_scores, db->d_flag_list,
                         db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_vstate_off, db->d_vstate, db->d_progress, db->d_keys,        db->d_sel[0],
                         db->d_sel[1],     db->d_sort,     db->d_all_scores, db->d_query,       db->d_matrix,
                         db->d_prof8,      db->d_prof8i,   db->d_prof32i};
@@ -435,7 +437,7 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
     };
     std::vector<DuoScan> scans;
     std::vector<uint32_t> single;
-    plan_batch(scan_knobs(), duo_enabled(db, matrix, gap_open, gap_extend), query_lens, n_queries, scans, single);
+    plan_batch(scan_knobs(), duo_mode(db, matrix, gap_open, gap_extend), query_lens, n_queries, scans, single);
     std::vector<Job> jobs;
     for (size_t i = 0; i < scans.size(); ++i) jobs.push_back(Job{static_cast<int>(i), 0});
     for (uint32_t q : single) jobs.push_back(Job{-1, q});
@@ -657,7 +659,7 @@ swb_status swb_batch_plan(const uint32_t* lens, uint32_t n, uint64_t length_thre
     uint64_t padded_rows = 0;
     group_table(src, length_threshold, shard_rank, shard_count, groups, &padded_rows);
     const uint32_t max_rows = groups.empty() ? 0 : groups[0].n_chunks * kRowsPerChunk;
-    const bool enabled = shared_scans_fit(scan_knobs(), static_cast<uint32_t>(groups.size()), max_rows, padded_rows, sm_count);
+    const SharedScanMode enabled = shared_scan_mode(scan_knobs(), static_cast<uint32_t>(groups.size()), max_rows, padded_rows, sm_count);
     std::vector<DuoScan> scans;
     std::vector<uint32_t> single;
     plan_batch(scan_knobs(), enabled, query_lens, n_queries, scans, single);

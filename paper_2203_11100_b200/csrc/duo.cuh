@@ -68,7 +68,13 @@ __global__ void build_duo_profile_kernel(DuoProfileParams p) {
 struct DuoParams {
     const uint4* codes;
     const GroupDesc* groups;
-    uint32_t n_items;         // 2 x groups: item i = half (i & 1) of group (i >> 1), longest first
+    uint32_t n_items;         // whole items: 2 x groups, item i = half (i & 1) of group (i >> 1), longest first;
+                              // pass items: 2 x groups x n_passes
+    uint32_t pass_items;      // 1: an item is ONE PASS (16 tiles) of a half-group; consecutive passes of a half-group may
+                              // run on different CTAs, linked through the global border rows and `progress`
+    uint32_t n_passes;        // ceil(n_tiles / 16)
+    uint32_t window;          // pass items are handed out pass-major within windows of this many half-groups
+    uint32_t* progress;       // [2 x groups][n_passes]: chunks the pass's last warp has published, zeroed per scan
     const uint32_t* prof2;
     const DuoTile* tiles;     // [n_tiles]
     uint32_t n_tiles;         // tiles of the longer stream
@@ -83,7 +89,8 @@ struct DuoParams {
     unsigned long long* stats;   // SWB_PIPE_STATS builds: [cta][warp][4] clocks waited on input / output / item fetch, total
 };
 
-template <int T, int kThreads>
+// kPassItems: compile the pass-item form (DuoParams::pass_items); the whole-item form keeps its register allocation.
+template <int T, int kThreads, bool kPassItems>
 __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) {
     static_assert(T == 32, "the slice layout assumes 32-column tiles");
     extern __shared__ __align__(256) uint8_t smem[];
@@ -99,7 +106,6 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t next = (warp + 1) % kPipeWarps;
     const bool wrap = p.n_tiles > kPipeWarps;
-    const bool wrap_in = wrap && warp == 0, wrap_out = wrap && next == 0;
     const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
     const uint32_t ring_mask = p.ring_chunks - 1;
     const uint32_t ring_bytes = p.ring_chunks * kPipeChunkBytes;
@@ -122,15 +128,35 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
 #else
 #define SWB_STAT(acc, stmt) { stmt; }
 #endif
+    const uint32_t n_half_groups = kPassItems ? p.n_items / p.n_passes : p.n_items;
     for (uint32_t slot = warp;; slot += kPipeWarps) {
-        const uint32_t item = slot / p.n_tiles, tile = slot - item * p.n_tiles;
+        const uint32_t tiles_per_item = kPassItems ? kPipeWarps : p.n_tiles;
+        const uint32_t item = slot / tiles_per_item;
+        uint32_t tile = slot - item * tiles_per_item;
         uint32_t it;
         SWB_STAT(w_item, it = pipe_item(tickets, ctl, item, lane));
         if (it == kPipeEnd) break;
         if (lane == 0) ctl->warp_item[warp] = item;
-        const uint32_t half = it & 1;
-        const GroupDesc gd = p.groups[it >> 1];
+        uint32_t hg = it, pass = 0;
+        if (kPassItems) {
+            // ticket -> (half-group, pass): pass-major within a window of half-groups, so that by the time pass p + 1 of
+            // a half-group is handed out its pass p has been running for a whole window of tickets
+            const uint32_t per_window = p.window * p.n_passes;
+            const uint32_t w = it / per_window, r = it - w * per_window;
+            const uint32_t in_window = min(p.window, n_half_groups - w * p.window);
+            pass = r / in_window;
+            hg = w * p.window + (r - pass * in_window);
+            tile += pass * kPipeWarps;
+            if (tile >= p.n_tiles) continue;   // the last pass is shorter: nothing for this warp
+        }
+        const uint32_t half = hg & 1;
+        const GroupDesc gd = p.groups[hg >> 1];
         const bool first = tile == 0, last = tile + 1 == p.n_tiles;
+        // pass items: the link into the pass's first warp comes from another item (maybe another CTA)
+        const bool wrap_in = kPassItems ? (warp == 0 && pass > 0) : (wrap && warp == 0);
+        const bool wrap_out = kPassItems ? (next == 0 && !last) : (wrap && next == 0);
+        const uint32_t* prog_in = p.progress + static_cast<size_t>(hg) * p.n_passes + (pass ? pass - 1 : 0);
+        uint32_t* prog_out = p.progress + static_cast<size_t>(hg) * p.n_passes + pass;
         const DuoTile td = p.tiles[tile];
         // a half that starts a query here takes the matrix edge instead of its left neighbour's border
         const uint32_t keep = ((td.reset & 1u) ? 0u : 0x0000FFFFu) | ((td.reset & 2u) ? 0u : 0xFFFF0000u);
@@ -164,16 +190,19 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
             if (chunk + 1 < gd.n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
             if (!first) {
                 if (wrap_in) {
+                    // published chunks of the inbound link, as a position on it: the ring's head counter, or (pass
+                    // items) the producing pass's progress counter in global memory
+                    auto published = [&]() { return kPassItems ? in_base + ld_poll(prog_in) : lds_acquire(&ctl->head[0]); };
                     if (staged == in_pos) {
                         const uint32_t need = min(in_pos + 2, in_end);
-                        SWB_STAT(w_in, while (lds_acquire(&ctl->head[0]) < need) __nanosleep(kPipePollNs));
+                        SWB_STAT(w_in, while (published() < need) __nanosleep(kPipePollNs));
                         stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
                                     gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
                         ++staged;
                     }
                     asm volatile("cp.async.wait_all;" ::: "memory");
                     __syncwarp();
-                    if (staged < in_end && lds_acquire(&ctl->head[0]) > staged) {
+                    if (staged < in_end && published() > staged) {
                         stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
                                     gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
                         ++staged;
@@ -266,8 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
             if (!last) {
                 ++out_pos;
                 if (lane == 0) {
-                    if (wrap_out) __threadfence();
-                    sts_release(&ctl->head[next], out_pos);
+                    if (wrap_out && kPassItems) st_release(prog_out, chunk + 1);   // release.gpu: the rows are in L2 first
+                    else {
+                        if (wrap_out) __threadfence();
+                        sts_release(&ctl->head[next], out_pos);
+                    }
                 }
             }
         }

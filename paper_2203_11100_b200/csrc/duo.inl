@@ -1,5 +1,10 @@
 // duo.inl -- two streams of queries per scan (duo.cuh): host side.  Included by cabi.cu inside its anonymous namespace.
 
+inline SharedScanMode shared_mode(const swb_db* db) {
+    return shared_scan_mode(scan_knobs(), static_cast<uint32_t>(db->meta.groups.size()), db->max_rows, db->meta.padded_rows,
+                            static_cast<uint32_t>(db->sm_count));
+}
+
 // Scores every local sequence against every query of the scan; query number `scan_queries[i]` (a's members first, then
 // b's) gets the score array d_multi_scores + i * n_slots and the device copy d_multi_codes + code_off[i].
 // Asynchronous on db->stream.  Requires the packed int16 path (matrix + open within int8).
@@ -81,6 +86,17 @@ swb_status score_streams_core(swb_db* db, const uint8_t* const* queries, const u
     dp.codes = reinterpret_cast<const uint4*>(db->d_codes);
     dp.groups = db->d_groups;
     dp.n_items = n_groups * 2;
+    if (shared_mode(db) == kSharedPass && n_tiles > kPipeWarps) {
+        // pass items: one item per half-group and pass of 16 tiles, pass-major over the whole shard (duo.cuh)
+        dp.pass_items = 1;
+        dp.n_passes = (n_tiles + kPipeWarps - 1) / kPipeWarps;
+        dp.window = n_groups * 2;
+        dp.n_items = n_groups * 2 * dp.n_passes;
+        const size_t counters = static_cast<size_t>(n_groups) * 2 * dp.n_passes;
+        if ((st = ensure_dev(&db->d_duo_progress, &db->duo_progress_cap, counters, &db->device_bytes)) != SWB_OK) return st;
+        SWB_CUDA(cudaMemsetAsync(db->d_duo_progress, 0, counters * sizeof(uint32_t), s));
+        dp.progress = db->d_duo_progress;
+    }
     dp.prof2 = db->d_prof2;
     dp.tiles = reinterpret_cast<const DuoTile*>(db->d_duo_tiles);
     dp.n_tiles = n_tiles;
@@ -96,7 +112,9 @@ swb_status score_streams_core(swb_db* db, const uint8_t* const* queries, const u
     const size_t smem = sizeof(PipeCtl) + static_cast<size_t>(kPipeWarps) * kDuoSliceBytes +
                         static_cast<size_t>(kPipeWarps) * dp.ring_chunks * kPipeChunkBytes;
     if (!db->duo_attr_set) {
-        SWB_CUDA(cudaFuncSetAttribute(duo_pipeline_kernel<kInterTile, kInterThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SWB_CUDA(cudaFuncSetAttribute(duo_pipeline_kernel<kInterTile, kInterThreads, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(db->smem_optin)));
+        SWB_CUDA(cudaFuncSetAttribute(duo_pipeline_kernel<kInterTile, kInterThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(db->smem_optin)));
         db->duo_attr_set = true;
     }
@@ -104,7 +122,8 @@ swb_status score_streams_core(swb_db* db, const uint8_t* const* queries, const u
 #ifdef SWB_PIPE_STATS
     dp.stats = pipe_stats_buffer(s);
 #endif
-    duo_pipeline_kernel<kInterTile, kInterThreads><<<grid, kInterThreads, smem, s>>>(dp);
+    if (dp.pass_items) duo_pipeline_kernel<kInterTile, kInterThreads, true><<<grid, kInterThreads, smem, s>>>(dp);
+    else duo_pipeline_kernel<kInterTile, kInterThreads, false><<<grid, kInterThreads, smem, s>>>(dp);
     ++db->launches;
 #ifdef SWB_PIPE_STATS
     report_pipe_stats("two-stream", dp.stats, grid, n_tiles, s);
@@ -149,10 +168,9 @@ swb_status finish_duo_query(swb_db* db, const uint8_t* q_dev, uint32_t m, const 
     return select_topk(db, db->d_keys, db->n_slots, top_k, d_out);
 }
 
-// Can queries of a batch share scans at all on this handle?  (The rest of the decision is plan_batch in scan_plan.hpp.)
-bool duo_enabled(const swb_db* db, const int32_t* matrix, int32_t open, int32_t ext) {
-    if (db->scan_policy != SWB_SCAN_AUTO || db->force_intra) return false;
-    if (make_plan(db, 64, matrix, open, ext).main != kMainS16) return false;
-    return shared_scans_fit(scan_knobs(), static_cast<uint32_t>(db->meta.groups.size()), db->max_rows, db->meta.padded_rows,
-                            static_cast<uint32_t>(db->sm_count));
+// Can queries of a batch share scans on this handle, and in which form?  (The rest is plan_batch in scan_plan.hpp.)
+SharedScanMode duo_mode(const swb_db* db, const int32_t* matrix, int32_t open, int32_t ext) {
+    if (db->scan_policy != SWB_SCAN_AUTO || db->force_intra) return kSharedNone;
+    if (make_plan(db, 64, matrix, open, ext).main != kMainS16) return kSharedNone;
+    return shared_mode(db);
 }

@@ -73,6 +73,8 @@ struct ScanKnobs {
                                      // two-stream kernel is ~15 % faster per padded cell: below 0.74 the padding eats the gain);
                                      // > 1: never
     uint32_t duo_stream_tiles = 704; // SWB200_DUO_TILES: tiles per stream of a shared scan at most (a tall group's item must not outlast the scan)
+    uint32_t duo_pass_items = 1;     // SWB200_DUO_PASS: shared scans hand out one pass (16 tiles) of a half-group per item:
+                                     // 1 (default) where whole items do not fit, 2 always, 0 ("off") never
     double duo_tall = 1.0;           // SWB200_DUO_TALL: ... and the tallest group's rows x SMs stay under this x the database's rows x 2
                                      // (a half-group is one CTA's item: it must fit that CTA's fair share of the scan)
     double duo_min_groups_per_sm = 2.0; // SWB200_DUO_MINGROUPS: ... and the database has at least this many groups per SM
@@ -107,6 +109,7 @@ struct ScanKnobs {
         k.duo_ratio = num("SWB200_DUO", k.duo_ratio);
         k.duo_stream_tiles = std::max<uint32_t>(16, static_cast<uint32_t>(num("SWB200_DUO_TILES", k.duo_stream_tiles)));
         k.duo_tall = num("SWB200_DUO_TALL", k.duo_tall);
+        if (const char* e = std::getenv("SWB200_DUO_PASS")) k.duo_pass_items = std::string(e) == "off" ? 0u : static_cast<uint32_t>(std::atoi(e));
         k.duo_min_groups_per_sm = num("SWB200_DUO_MINGROUPS", k.duo_min_groups_per_sm);
         return k;
     }
@@ -264,21 +267,31 @@ struct DuoScan {
 
 inline uint32_t tiles_of(uint32_t m) { return (m + 31) / 32; }
 
-// Shared scans give every half-group to one CTA: the database needs enough groups per SM, and its tallest group must
-// fit a CTA's fair share of the scan (small shards of a database with a few very long sequences do not; their
-// searches go one by one, where the tall groups get the wavefront kernel).
-inline bool shared_scans_fit(const ScanKnobs& k, uint32_t n_groups, uint32_t max_rows, uint64_t padded_rows, uint32_t sm_count) {
-    if (k.duo_ratio > 1.0) return false;
-    if (static_cast<double>(n_groups) < k.duo_min_groups_per_sm * static_cast<double>(sm_count)) return false;
-    return static_cast<double>(max_rows) * sm_count <= k.duo_tall * 2.0 * static_cast<double>(padded_rows);
+// How shared scans hand out their work.  Whole items (a half-group with all its tiles on one CTA) are the faster form,
+// but the tallest half-group must fit a CTA's fair share of the scan; small shards of a database with a few very long
+// sequences do not satisfy that (one 35,213-row item would outlast the scan several times), and take pass items:
+// one pass of 16 tiles per item, pass-major over the whole shard, so that a tall half-group's passes run on many CTAs
+// one behind the other (3 % slower per cell, but 48 instead of 35 TCUPS-equivalent on eight 1/8 shards of Swiss-Prot).
+enum SharedScanMode : int { kSharedNone = 0, kSharedWhole = 1, kSharedPass = 2 };
+
+inline SharedScanMode shared_scan_mode(const ScanKnobs& k, uint32_t n_groups, uint32_t max_rows, uint64_t padded_rows, uint32_t sm_count) {
+    if (k.duo_ratio > 1.0) return kSharedNone;
+    if (static_cast<double>(n_groups) < k.duo_min_groups_per_sm * static_cast<double>(sm_count)) return kSharedNone;
+    const bool whole_fits = static_cast<double>(max_rows) * sm_count <= k.duo_tall * 2.0 * static_cast<double>(padded_rows);
+    if (k.duo_pass_items >= 2) return kSharedPass;
+    if (whole_fits) return kSharedWhole;
+    return k.duo_pass_items >= 1 ? kSharedPass : kSharedNone;
 }
 
 // Deals the queries of a batch over shared scans: longest first, each to the shortest stream so far, so that the two
 // streams of a scan end up equally long.  A scan whose streams differ too much (the padding would eat the two-stream
 // kernel's ~15 % advantage) or that is too short to keep the pipeline busy is dissolved again: its queries go one by
 // one.  `single` receives every query that is not part of a scan (empty queries, and all of them when !enabled).
-inline void plan_batch(const ScanKnobs& k, bool enabled, const uint32_t* lens, uint32_t n_queries, std::vector<DuoScan>& scans,
+inline void plan_batch(const ScanKnobs& k, SharedScanMode mode, const uint32_t* lens, uint32_t n_queries, std::vector<DuoScan>& scans,
                        std::vector<uint32_t>& single) {
+    const bool enabled = mode != kSharedNone;
+    // pass items need more than one pass; whole items the pipeline's usual minimum
+    const uint32_t min_tiles = mode == kSharedPass ? 17u : k.pipe_min_tiles;
     scans.clear();
     single.clear();
     std::vector<uint32_t> eligible;
@@ -342,7 +355,7 @@ inline void plan_batch(const ScanKnobs& k, bool enabled, const uint32_t* lens, u
     std::vector<DuoScan> kept;
     for (DuoScan& sc : scans) {
         const uint32_t lo = std::min(sc.tiles_a, sc.tiles_b), hi = std::max(sc.tiles_a, sc.tiles_b);
-        if (lo == 0 || static_cast<double>(lo) < k.duo_ratio * static_cast<double>(hi) || hi < k.pipe_min_tiles) {
+        if (lo == 0 || static_cast<double>(lo) < k.duo_ratio * static_cast<double>(hi) || hi < min_tiles) {
             single.insert(single.end(), sc.a.begin(), sc.a.end());
             single.insert(single.end(), sc.b.begin(), sc.b.end());
         } else {

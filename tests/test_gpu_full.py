@@ -96,6 +96,22 @@ def test_batched_sweep_equals_single_searches(full, b62):
         assert (i1 == i2).all() and (s1 == s2).all()
 
 
+def test_batched_sweep_on_a_shard_uses_pass_items(full, b62):
+    """A quarter of the database still holds a 35,213-residue sequence: as one item it would outlast the shared scan,
+    so swb_search_many hands out single passes of 16 tiles (consecutive passes of a half-group on different CTAs,
+    linked through global border rows and progress counters).  Ranked lists equal the single searches'."""
+    from paper_2203_11100_b200 import batch_plan
+    queries, sdb, _ = full
+    assert (batch_plan(sdb.lengths(), [len(q) for q in queries], shard_rank=1, shard_count=4)[0] == 0).all()
+    with Database(sdb.codes, sdb.offsets, shard_rank=1, shard_count=4) as shard:
+        many, ms = shard.search_many(queries, b62, GapModel(10, 2), 10)
+        for qi in (0, 5, 11, 19):
+            idx, sc, _ = shard.search(queries[qi], b62, GapModel(10, 2), 10)
+            assert (many[qi][0] == idx).all() and (many[qi][1] == sc).all(), f"query {qi}"
+        single_ms = sum(shard.search(q, b62, GapModel(10, 2), 10)[2]["ms_total"] for q in queries)
+        assert ms.sum() < single_ms        # and it is faster than one scan per query
+
+
 def test_two_query_scan_with_overflow(port):
     """BLOSUM50 12/2 with two long queries whose planted copies leave the int16 range: the shared scan flags them
     and each query's flagged lanes come back exact from the int32 re-run."""

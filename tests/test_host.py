@@ -215,7 +215,12 @@ def test_batch_plan_deals_queries_over_two_balanced_streams(lib):
     assert search.batch_plan(lens, [5000, 300])[0].tolist() == [-1, -1]
     assert search.batch_plan(lens, [5000, 4000, 0, 100])[0].tolist() == [0, 0, -1, 0]
     assert search.batch_plan(lens, [100, 120])[0].tolist() == [-1, -1]            # fewer than 9 tiles per stream
-    # small database / half of the database (its 35,213-row group no longer fits a CTA's share): one search per query
+    # small database (fewer than two groups per SM): one search per query
     assert (search.batch_plan(lens[:10_000], synth.QUERY_LENGTHS)[0] == -1).all()
-    assert (search.batch_plan(lens, synth.QUERY_LENGTHS, shard_count=2)[0] == -1).all()
-    assert (search.batch_plan(np.minimum(lens, 2999), synth.QUERY_LENGTHS, shard_count=8)[0] == 0).all()   # no tall groups: shards share too
+    # half / an eighth of the database: its 35,213-row group no longer fits a CTA's share as one item, so the scan
+    # hands out single passes instead -- still one shared scan
+    assert (search.batch_plan(lens, synth.QUERY_LENGTHS, shard_count=2)[0] == 0).all()
+    assert (search.batch_plan(lens, synth.QUERY_LENGTHS, shard_count=8)[0] == 0).all()
+    # ... which needs more than one pass (16 tiles): two 400-residue queries share a scan on the whole database only
+    assert search.batch_plan(lens, [400, 410])[0].tolist() == [0, 0]
+    assert search.batch_plan(lens, [400, 410], shard_count=8)[0].tolist() == [-1, -1]
