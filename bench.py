@@ -23,8 +23,9 @@ one full sweep: 20 searches, 8.5e12 cell updates.  GCUPS = sum(query_len x db_re
   cpu_baseline  the unmodified reference (oracle/_ref/libswref.so, run_search without traceback) on the host
              cores, on a bounded subsample of the same workload (N=1, rank 0 only).
 
-N > 1 (torchrun, one rank per GPU): the same database is sharded by residue count (strong scaling); every
-search ends with one all-gather of k packed keys per rank (NCCL) and a device-side merge.
+N > 1 (torchrun, one rank per GPU): the same database is sharded by residue count (strong scaling).  The batched
+sweep ends with one all-gather of 20 x k packed keys per rank (NCCL); the per-search path has one all-gather of k keys
+per search and a device-side merge.  If the batched sweep fails on any rank the per-search numbers are the headline.
 """
 from __future__ import annotations
 
@@ -253,13 +254,13 @@ def main_native(args):
         _, _, _, hits, _ = one_step()
         first_hits = first_hits or hits
 
-    # ---- the sweep as one batch (swb_search_many): the headline at N = 1 ---------------------------------
+    # ---- the sweep as one batch (swb_search_many on every rank's shard, ONE all-gather per sweep): the headline -------
     batch = None
-    if world == 1:
+    try:
         for _ in range(max(args.warmup, 0)):
-            engine.db.search_many(queries, b62, gaps, TOP_K)
+            engine.search_many(queries, b62, gaps, TOP_K)
         bsampler = ClockSampler(local_rank)
-        torch.cuda.synchronize(device)
+        barrier()
         bsampler.start()
         launches0 = engine.db.info()["kernel_launches_total"]
         b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -267,17 +268,32 @@ def main_native(args):
         batch_dev_ms = 0.0
         batch_jobs = None
         for _ in range(args.steps):
-            many, ms = engine.db.search_many(queries, b62, gaps, TOP_K)
+            many, ms = engine.search_many(queries, b62, gaps, TOP_K)
             batch_dev_ms += float(ms.sum())
             batch_jobs = ms
             for (a, b), (c, e) in zip(many, first_hits or many):     # determinism check of SPEC.md:377
                 if not ((a == c).all() and (b == e).all()):
-                    raise SystemExit("determinism_error: the batched sweep returned a different ranked list")
+                    raise RuntimeError("determinism_error: the batched sweep returned a different ranked list")
         b1.record(stream)
-        torch.cuda.synchronize(device)
-        batch = {"dev_ms": batch_dev_ms, "e2e_ms": b0.elapsed_time(b1), "clocks": bsampler.stop(),
+        barrier()
+        batch = {"ok": 1.0, "dev_ms": batch_dev_ms, "e2e_ms": b0.elapsed_time(b1), "clocks": bsampler.stop(),
                  "launches": engine.db.info()["kernel_launches_total"] - launches0,
                  "per_query_ms": [float(x) for x in batch_jobs]}
+    except Exception as exc:      # keep the per-search numbers below as the headline, say why
+        if world == 1:
+            raise
+        batch = {"ok": 0.0, "dev_ms": 0.0, "e2e_ms": 0.0, "clocks": None, "launches": 0, "per_query_ms": [], "error": repr(exc)}
+    if world > 1:
+        # all ranks agree on whether the batched sweep counts; times are the max over ranks, launches the sum
+        flag = torch.tensor([batch["ok"]], dtype=torch.float64, device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        bt = torch.tensor([batch["dev_ms"], batch["e2e_ms"]], dtype=torch.float64, device=device)
+        dist.all_reduce(bt, op=dist.ReduceOp.MAX)
+        bl = torch.tensor([batch["launches"]], dtype=torch.int64, device=device)
+        dist.all_reduce(bl)
+        batch["dev_ms"], batch["e2e_ms"], batch["launches"] = float(bt[0]), float(bt[1]), int(bl.item())
+        if float(flag.item()) < 1.0:
+            batch = None
 
     sampler = ClockSampler(local_rank)
     barrier()
@@ -330,7 +346,8 @@ def main_native(args):
             traffic = json.loads(tfile.read_text())
         single = {"value": value, "e2e": e2e, "unit": "GCUPS", "ms_per_step": e2e_ms / steps, "gpu_launches": launches,
                   "scan_kernel_gcups": scan_gcups,
-                  "api": "swb_search, one call per query (what swsearch::run_search forwards to)",
+                  "api": "swb_search, one call per query (what swsearch::run_search forwards to)" +
+                         ("" if world == 1 else " + one all-gather of k keys per search"),
                   "per_query": [{"m": m, "gcups": m * sdb.residues / (ms * 1e-3) / 1e9, "ms": ms, "scan_ms": sms,
                                  "rescored_i32": int(r), "units": int(u)} for (m, ms, sms, r, u) in per_query]}
         h2d = int(sum(len(q) + 2304 + 4 * (info["n_groups"] + 1) for q in queries))
@@ -339,7 +356,8 @@ def main_native(args):
             head_value = total_cells * steps / (batch["dev_ms"] * 1e-3) / 1e9
             head_e2e = total_cells * steps / (batch["e2e_ms"] * 1e-3) / 1e9
             head_ms, head_launches, head_clocks = batch["e2e_ms"] / steps, batch["launches"], batch["clocks"]
-            api = "swb_search_many, one call per sweep (the queries share one database scan as two streams)"
+            api = ("swb_search_many, one call per sweep (the queries share one database scan as two streams)" if world == 1 else
+                   "swb_search_many on every rank's shard + one all-gather of the sweep's keys per rank")
             kernel = "duo_pipeline_kernel (shared scan of the batch)"
         else:
             head_value, head_e2e, head_ms, head_launches, head_clocks = value, e2e, e2e_ms / steps, launches, clocks
