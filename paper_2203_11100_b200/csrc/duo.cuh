@@ -198,13 +198,25 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
                         SWB_STAT(w_in, while (published() < need) __nanosleep(kPipePollNs));
                         stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
                                     gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
+                        asm volatile("cp.async.commit_group;" ::: "memory");
                         ++staged;
                     }
-                    asm volatile("cp.async.wait_all;" ::: "memory");
+                    // chunk in_pos must have landed; the one behind it may stay in flight (one commit group per chunk)
+                    if (staged - in_pos >= 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+                    else asm volatile("cp.async.wait_group 0;" ::: "memory");
                     __syncwarp();
-                    if (staged < in_end && published() > staged) {
+                    // keep up to two chunks requested beyond the current one (ring of 4; one beyond for a ring of 2)
+                    const uint32_t upto = min(min(published(), in_end), in_pos + min(3u, p.ring_chunks));
+                    if (staged < upto) {
                         stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
                                     gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
+                        asm volatile("cp.async.commit_group;" ::: "memory");
+                        ++staged;
+                    }
+                    if (staged < upto) {
+                        stage_chunk(ring_stage + (staged & ring_mask) * kPipeChunkBytes,
+                                    gstage + static_cast<size_t>(staged - in_base) * kPipeChunkBytes);
+                        asm volatile("cp.async.commit_group;" ::: "memory");
                         ++staged;
                     }
                 } else {
