@@ -345,13 +345,30 @@ def main_native(args):
         if tfile.exists():
             traffic = json.loads(tfile.read_text())
         single = {"value": value, "e2e": e2e, "unit": "GCUPS", "ms_per_step": e2e_ms / steps, "gpu_launches": launches,
+                  "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                   "scan_kernel_gcups": scan_gcups,
                   "api": "swb_search, one call per query (what swsearch::run_search forwards to)" +
                          ("" if world == 1 else " + one all-gather of k keys per search"),
                   "per_query": [{"m": m, "gcups": m * sdb.residues / (ms * 1e-3) / 1e9, "ms": ms, "scan_ms": sms,
                                  "rescored_i32": int(r), "units": int(u)} for (m, ms, sms, r, u) in per_query]}
-        h2d = int(sum(len(q) + 2304 + 4 * (info["n_groups"] + 1) for q in queries))
-        d2h = int(len(queries) * (TOP_K * 8 + 16))
+        # bytes copied per sweep.  One search at a time: matrix + query + the wavefront kernel's unit tables up, k keys +
+        # counters down, per query.  Batched: per shared scan the matrix, the queries and a 32-byte tile descriptor per
+        # tile of the longer stream up; k keys per query down (queries left out of the scans copy as single searches do).
+        h2d_single = int(sum(len(q) + 2304 + 9 * (info["n_groups"] + 1) for q in queries))
+        d2h_single = int(len(queries) * (TOP_K * 8 + 16))
+        h2d, d2h = h2d_single, d2h_single
+        if batch:
+            from paper_2203_11100_b200 import batch_plan
+            scan_of, stream_of = batch_plan(sdb.lengths(), [len(q) for q in queries], sm_count=rates["sm_count"],
+                                            shard_rank=rank, shard_count=world)
+            h2d, d2h = 0, int(len(queries) * TOP_K * 8)
+            for sc in sorted(set(int(x) for x in scan_of)):
+                members = [i for i in range(len(queries)) if scan_of[i] == sc]
+                if sc < 0:
+                    h2d += sum(len(queries[i]) + 2304 + 9 * (info["n_groups"] + 1) for i in members)
+                    continue
+                tiles = [sum((len(queries[i]) + 31) // 32 for i in members if stream_of[i] == half) for half in (0, 1)]
+                h2d += 2304 + sum((len(queries[i]) + 15) // 16 * 16 for i in members) + 32 * max(tiles)
         if batch:
             head_value = total_cells * steps / (batch["dev_ms"] * 1e-3) / 1e9
             head_e2e = total_cells * steps / (batch["e2e_ms"] * 1e-3) / 1e9
@@ -390,6 +407,7 @@ def main_native(args):
                                  "def": "packed-database stream: 1 byte per residue per search / scan-kernel time"}},
             "single_query": single,
         }
+        line["single_query"]["h2d_bytes_per_step"], line["single_query"]["d2h_bytes_per_step"] = h2d_single, d2h_single
         if batch:
             line["batched_per_query_ms"] = [{"m": len(q), "ms": ms} for q, ms in zip(queries, batch["per_query_ms"])]
             line["single_query"]["clocks"] = clocks
