@@ -495,3 +495,28 @@ def test_large_random_batch_shares_scans_and_equals_single_searches(b62):
             assert (many[qi][0] == idx).all() and (many[qi][1] == sc).all(), f"query {qi} (m={lens[qi]})"
         for qi in range(6):
             assert many[qi][0][0] == sdb.planted[qi][0]
+
+
+def test_search_many_edge_cases(port, b62):
+    """Batches the shared scans cannot or need not serve: no queries, only empty queries, top_k beyond the database,
+    a matrix outside the packed int16 range (every query falls back to the int32 kernel, one by one), duplicates."""
+    rng = np.random.default_rng(97)
+    seqs = [synth.random_residues(rng, int(rng.integers(1, 200))) for _ in range(40)]
+    fdb = po.FlatDb.from_list(seqs)
+    g = GapModel(10, 2)
+    q1, q2 = synth.random_residues(rng, 300), synth.random_residues(rng, 310)
+    with Database(fdb.codes, fdb.offsets) as db:
+        out, ms = db.search_many([], b62, g, 5)
+        assert out == [] and len(ms) == 0
+        out, _ = db.search_many([enc(""), enc("")], b62, g, 5)
+        assert all(len(i) == 5 and (s == 0).all() for i, s in out)                # every sequence is a hit with score 0
+        out, _ = db.search_many([q1, q2, q1], b62, g, 100)                        # top_k > n: all 40, duplicates equal
+        assert len(out[0][0]) == 40 and (out[0][0] == out[2][0]).all() and (out[0][1] == out[2][1]).all()
+        for q, (idx, sc) in zip([q1, q2], out):
+            ei, es, _ = port.run_search(q, fdb, b62, 10, 2, top_k=100)
+            assert (idx == ei).all() and (sc == es).all()
+        wide = (b62 * 40).astype(np.int32)                                        # entries + open outside int8
+        out, _ = db.search_many([q1[:80], q2[:90]], wide, GapModel(400, 80), 6)
+        for q, (idx, sc) in zip([q1[:80], q2[:90]], out):
+            ei, es, _ = port.run_search(q, fdb, wide, 400, 80, top_k=6)
+            assert (idx == ei).all() and (sc == es).all()
