@@ -115,12 +115,6 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
     uint32_t* const slice = reinterpret_cast<uint32_t*>(slices + warp * kDuoSliceBytes);
     uint32_t in_pos = 0, out_pos = 0;
 
-    // pipe_item() hands out tickets against n_items / group_first of a PipeParams
-    PipeParams tickets{};
-    tickets.n_items = p.n_items;
-    tickets.group_first = 0;
-    tickets.ticket = p.ticket;
-
 #ifdef SWB_PIPE_STATS
     long long w_in = 0, w_out = 0, w_item = 0;
     const long long t_begin = clock64();
@@ -134,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
         const uint32_t item = slot / tiles_per_item;
         uint32_t tile = slot - item * tiles_per_item;
         uint32_t it;
-        SWB_STAT(w_item, it = pipe_item(tickets, ctl, item, lane));
+        SWB_STAT(w_item, it = pipe_item(p.ticket, p.n_items, 0u, ctl, item, lane));
         if (it == kPipeEnd) break;
         if (lane == 0) ctl->warp_item[warp] = item;
         uint32_t hg = it, pass = 0;

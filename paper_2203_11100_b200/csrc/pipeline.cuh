@@ -97,8 +97,10 @@ __device__ __forceinline__ void sts_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(v) : "memory");
 }
 
-// Item `item` of this CTA -> group index, or kPipeEnd.  Called by whole warps; lane 0 does the work.
-__device__ __forceinline__ uint32_t pipe_item(const PipeParams& p, PipeCtl* ctl, uint32_t item, uint32_t lane) {
+// Item `item` of this CTA -> first_id + its ticket (tickets 0 .. n_items - 1 are handed out once each, GPU-wide), or
+// kPipeEnd.  Called by whole warps; lane 0 does the work.
+__device__ __forceinline__ uint32_t pipe_item(uint32_t* ticket, uint32_t n_items, uint32_t first_id, PipeCtl* ctl, uint32_t item,
+                                              uint32_t lane) {
     uint32_t g = 0;
     if (lane == 0) {
         while (lds_acquire(&ctl->fetched) <= item) {
@@ -113,8 +115,8 @@ __device__ __forceinline__ uint32_t pipe_item(const PipeParams& p, PipeCtl* ctl,
                                 if (at == kPipeEnd || at + kPipeItemRing > f) break;
                                 __nanosleep(100);
                             }
-                    const uint32_t t = atomicAdd(p.ticket, 1u);
-                    ctl->item_group[f % kPipeItemRing] = t < p.n_items ? p.group_first + t : kPipeEnd;
+                    const uint32_t t = atomicAdd(ticket, 1u);
+                    ctl->item_group[f % kPipeItemRing] = t < n_items ? first_id + t : kPipeEnd;
                     sts_release(&ctl->fetched, f + 1);
                 }
                 sts_release(&ctl->lock, 0u);
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
     for (uint32_t slot = warp;; slot += kPipeWarps) {
         const uint32_t item = slot / p.n_tiles, tile = slot - item * p.n_tiles;
         uint32_t g;
-        SWB_STAT(w_item, g = pipe_item(p, ctl, item, lane));
+        SWB_STAT(w_item, g = pipe_item(p.ticket, p.n_items, p.group_first, ctl, item, lane));
         if (g == kPipeEnd) break;
         if (lane == 0) ctl->warp_item[warp] = item;
         const GroupDesc gd = p.groups[g];
