@@ -250,6 +250,10 @@ swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len
 swb_status swb_mdb_align_hits(swb_mdb* mdb, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
                               int32_t gap_open, int32_t gap_extend, const swb_hit* hits, uint32_t n_hits,
                               uint64_t memory_cap, swb_alignment* out, uint8_t* ops, const uint64_t* ops_offset);
+/* swb_search_many on every shard at once (one host thread per shard), merged per query on the host; same results. */
+swb_status swb_mdb_search_many(swb_mdb* mdb, const uint8_t* const* queries, const uint32_t* query_lens,
+                               uint32_t n_queries, const int32_t* matrix, int32_t gap_open, int32_t gap_extend,
+                               uint32_t top_k, swb_hit* hits, uint32_t* n_hits, float* ms_per_query);
 uint32_t swb_mdb_shard_count(const swb_mdb* mdb);
 swb_db* swb_mdb_shard(swb_mdb* mdb, uint32_t i);
 

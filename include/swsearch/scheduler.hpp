@@ -210,8 +210,8 @@ inline RankedResults run_search(const EncodedSequence& query, const SequenceData
 
 /// Several queries against the same database: the same results as a loop over run_search (which is what the
 /// reference's callers write), but issued to the GPU as one batch -- searches overlap each other's
-/// host preparation, and the queries share database scans as two streams (swb_search_many).  With the database
-/// sharded over several GPUs this falls back to the loop.
+/// host preparation, and the queries share database scans as two streams (swb_search_many; on every GPU at once
+/// when the database is sharded over several, swb_mdb_search_many).
 inline std::vector<RankedResults> run_search_batch(const std::vector<EncodedSequence>& queries, const SequenceDatabase& db,
                                                    const ScoringMatrix& matrix, const GapModel& gaps,
                                                    const SearchConfig& config, SearchStats* stats = nullptr) {
@@ -223,11 +223,10 @@ inline std::vector<RankedResults> run_search_batch(const std::vector<EncodedSequ
     swb_mdb* resident = gpu::resident(db, config.length_threshold);
     const std::size_t want = std::min<std::size_t>(config.top_k, db.num_sequences());
     if (queries.empty()) return all;
-    if (swb_mdb_shard_count(resident) != 1 || want == 0) {
+    if (want == 0) {
         for (std::size_t q = 0; q < queries.size(); ++q) all[q] = run_search(queries[q], db, matrix, gaps, config, stats);
         return all;
     }
-    swb_db* shard = swb_mdb_shard(resident, 0);
     std::vector<const std::uint8_t*> rows(queries.size());
     std::vector<std::uint32_t> lengths(queries.size());
     for (std::size_t q = 0; q < queries.size(); ++q) {
@@ -236,11 +235,15 @@ inline std::vector<RankedResults> run_search_batch(const std::vector<EncodedSequ
     }
     std::vector<swb_hit> hits(queries.size() * want);
     std::vector<std::uint32_t> found(queries.size(), 0);
-    gpu::check(swb_search_many(shard, rows.data(), lengths.data(), static_cast<std::uint32_t>(queries.size()),
-                               gpu::matrix_table(matrix), gaps.open(), gaps.extend(), static_cast<std::uint32_t>(want),
-                               hits.data(), found.data(), nullptr));
-    swb_db_info info{};
-    gpu::check(swb_db_info_get(shard, &info));
+    gpu::check(swb_mdb_search_many(resident, rows.data(), lengths.data(), static_cast<std::uint32_t>(queries.size()),
+                                   gpu::matrix_table(matrix), gaps.open(), gaps.extend(), static_cast<std::uint32_t>(want),
+                                   hits.data(), found.data(), nullptr));
+    swb_db_info info{};   // counters for SearchStats: summed over the shards
+    for (std::uint32_t r = 0; r < swb_mdb_shard_count(resident); ++r) {
+        swb_db_info one{};
+        gpu::check(swb_db_info_get(swb_mdb_shard(resident, r), &one));
+        info.n_short += one.n_short, info.n_long += one.n_long, info.n_groups += one.n_groups;
+    }
     for (std::size_t q = 0; q < queries.size(); ++q) {
         all[q].hits.resize(found[q]);
         for (std::uint32_t i = 0; i < found[q]; ++i) {

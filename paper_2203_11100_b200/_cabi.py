@@ -119,6 +119,8 @@ SIGNATURES = {
     "swb_mdb_destroy": (None, [C.c_void_p]),
     "swb_mdb_search": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32,
                                  C.POINTER(SwbHit), u32p, C.POINTER(SwbStats)]),
+    "swb_mdb_search_many": (C.c_int, [C.c_void_p, C.POINTER(u8p), u32p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32,
+                                      C.POINTER(SwbHit), u32p, C.POINTER(C.c_float)]),
     "swb_mdb_shard_count": (C.c_uint32, [C.c_void_p]),
     "swb_mdb_shard": (C.c_void_p, [C.c_void_p, C.c_uint32]),
     "swb_measure_pipe_rates": (C.c_int, [C.c_int32, C.c_double, C.POINTER(SwbPipeRates)]),

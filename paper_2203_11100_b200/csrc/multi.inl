@@ -218,6 +218,59 @@ swb_status swb_mdb_align_hits(swb_mdb* mdb, const uint8_t* query, uint32_t query
     return SWB_OK;
 }
 
+// A batch of queries on every shard at once (one host thread per shard, each running swb_search_many: shared scans
+// where they apply), then a host-side merge per query: top-k of the union = top-k of the per-shard top-k's
+// (scheduler.hpp:106-117; the order on packed keys is exactly (score desc, db_index asc)).  n_queries x k x G keys
+// are a few kilobytes, so unlike the per-search path this needs no collective.
+swb_status swb_mdb_search_many(swb_mdb* mdb, const uint8_t* const* queries, const uint32_t* query_lens, uint32_t n_queries,
+                               const int32_t* matrix, int32_t gap_open, int32_t gap_extend, uint32_t top_k, swb_hit* hits,
+                               uint32_t* n_hits, float* ms_per_query) {
+    if (!mdb) return fail(SWB_ERR_INVALID, "mdb is null");
+    if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
+    if (n_queries && (!queries || !query_lens || !hits || !n_hits)) return fail(SWB_ERR_INVALID, "null argument");
+    const size_t G = mdb->shards.size();
+    if (G == 1)
+        return swb_search_many(mdb->shards[0], queries, query_lens, n_queries, matrix, gap_open, gap_extend, top_k, hits, n_hits,
+                               ms_per_query);
+    std::lock_guard<std::mutex> lock(mdb->mu);
+    std::vector<swb_status> sts(G, SWB_OK);
+    std::vector<std::string> errs(G);
+    std::vector<std::vector<swb_hit>> shard_hits(G, std::vector<swb_hit>(static_cast<size_t>(n_queries) * top_k));
+    std::vector<std::vector<uint32_t>> shard_counts(G, std::vector<uint32_t>(n_queries, 0));
+    std::vector<std::vector<float>> shard_ms(G, std::vector<float>(n_queries, 0.f));
+    std::vector<std::thread> pool;
+    for (size_t r = 0; r < G; ++r)
+        pool.emplace_back([&, r] {
+            sts[r] = swb_search_many(mdb->shards[r], queries, query_lens, n_queries, matrix, gap_open, gap_extend, top_k,
+                                     shard_hits[r].data(), shard_counts[r].data(), shard_ms[r].data());
+            if (sts[r] != SWB_OK) errs[r] = g_error;
+        });
+    for (auto& t : pool) t.join();
+    for (size_t r = 0; r < G; ++r)
+        if (sts[r] != SWB_OK) return fail(sts[r], "shard " + std::to_string(r) + ": " + errs[r]);
+    std::vector<uint64_t> keys;
+    for (uint32_t q = 0; q < n_queries; ++q) {
+        keys.clear();
+        for (size_t r = 0; r < G; ++r)
+            for (uint32_t i = 0; i < shard_counts[r][q]; ++i) {
+                const swb_hit& h = shard_hits[r][static_cast<size_t>(q) * top_k + i];
+                keys.push_back((static_cast<uint64_t>(static_cast<uint32_t>(h.score)) << 32) | (0xFFFFFFFFu - h.db_index));
+            }
+        std::sort(keys.begin(), keys.end(), std::greater<uint64_t>());
+        const uint32_t cnt = static_cast<uint32_t>(std::min<size_t>(keys.size(), top_k));
+        for (uint32_t i = 0; i < cnt; ++i) {
+            hits[static_cast<size_t>(q) * top_k + i].db_index = 0xFFFFFFFFu - static_cast<uint32_t>(keys[i] & 0xFFFFFFFFu);
+            hits[static_cast<size_t>(q) * top_k + i].score = static_cast<int32_t>(keys[i] >> 32);
+        }
+        n_hits[q] = cnt;
+        if (ms_per_query) {
+            ms_per_query[q] = 0.f;
+            for (size_t r = 0; r < G; ++r) ms_per_query[q] = std::max(ms_per_query[q], shard_ms[r][q]);   // shards run side by side
+        }
+    }
+    return SWB_OK;
+}
+
 uint32_t swb_mdb_shard_count(const swb_mdb* mdb) { return mdb ? static_cast<uint32_t>(mdb->shards.size()) : 0; }
 
 swb_db* swb_mdb_shard(swb_mdb* mdb, uint32_t i) {

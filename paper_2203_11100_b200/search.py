@@ -409,6 +409,30 @@ class MultiGpuDatabase:
         sc = np.array([hits[i].score for i in range(n.value)], dtype=np.int32)
         return idx, sc, st.as_dict()
 
+    def search_many(self, queries, matrix, gaps: GapModel, top_k: int = 10):
+        """A batch on every shard at once (swb_mdb_search_many), merged per query: -> list of (db_index, score), ms."""
+        mat = _mat(matrix)
+        qs = [_u8(q) for q in queries]
+        n = len(qs)
+        dummy = np.zeros(1, np.uint8)
+        ptrs = (_u8p * max(1, n))()
+        lens = np.zeros(max(1, n), dtype=np.uint32)
+        for i, q in enumerate(qs):
+            ptrs[i] = _ptr(q if len(q) else dummy, _u8p)
+            lens[i] = len(q)
+        hits = (_cabi.SwbHit * max(1, n * top_k))()
+        counts = np.zeros(max(1, n), dtype=np.uint32)
+        ms = np.zeros(max(1, n), dtype=np.float32)
+        rc = self._lib.swb_mdb_search_many(self._h, ptrs, _ptr(lens, _u32p), n, _ptr(mat, _i32p), gaps.open, gaps.extend,
+                                           top_k, hits, _ptr(counts, _u32p), ms.ctypes.data_as(C.POINTER(C.c_float)))
+        _raise(self._lib, rc)
+        out = []
+        for qi in range(n):
+            c = int(counts[qi])
+            out.append((np.array([hits[qi * top_k + i].db_index for i in range(c)], dtype=np.uint32),
+                        np.array([hits[qi * top_k + i].score for i in range(c)], dtype=np.int32)))
+        return out, ms[:n].copy()
+
     def align_hits(self, query, matrix, gaps: GapModel, index, score, subject_lengths, memory_cap: int = 256 << 20):
         return _align_hits(self._lib.swb_mdb_align_hits, self._lib, self._h, query, matrix, gaps, index, score,
                            subject_lengths, memory_cap)

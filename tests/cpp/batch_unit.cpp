@@ -1,5 +1,6 @@
 // tests/cpp/batch_unit.cpp -- GPU check of swsearch::run_search_batch: identical to a loop over run_search
-// (ranked lists and edit scripts), on a database large enough for queries of similar length to share a scan.
+// (ranked lists and edit scripts), on a database large enough for the queries to share scans.  Run a second time
+// with SWB200_DEVICES=0,0 it covers the sharded flavour (swb_mdb_search_many).
 #include <cstdio>
 #include <random>
 

@@ -66,3 +66,7 @@ def test_run_search_batch_equals_a_loop_of_run_search(lib):
     assert exe.exists(), "tests/cpp/_build/batch_unit is built by __graft_entry__.build()"
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
     assert out.returncode == 0 and "batch_unit: ok" in out.stdout, out.stdout + out.stderr
+    # the same program with the database sharded over two handles (both on device 0): swb_mdb_search_many
+    import os
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900, env=dict(os.environ, SWB200_DEVICES="0,0"))
+    assert out.returncode == 0 and "batch_unit: ok" in out.stdout, out.stdout + out.stderr

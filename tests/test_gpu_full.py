@@ -112,6 +112,22 @@ def test_batched_sweep_on_a_shard_uses_pass_items(full, b62):
         assert ms.sum() < single_ms        # and it is faster than one scan per query
 
 
+def test_multi_shard_batched_sweep_equals_single_gpu(full, b62):
+    """swb_mdb_search_many: the batch on four shards at once (one host thread per shard, here all on device 0; pass
+    items on each), merged per query on the host: the same ranked lists as the unsharded database."""
+    queries, sdb, db = full
+    batch = [queries[i] for i in (0, 4, 9, 12, 16, 19)]
+    mdb = MultiGpuDatabase(sdb.codes, sdb.offsets, [0, 0, 0, 0])
+    try:
+        many, ms = mdb.search_many(batch, b62, GapModel(10, 2), 25)
+    finally:
+        mdb.close()
+    assert (ms > 0).all()
+    for q, (idx, sc) in zip(batch, many):
+        ei, es, _ = db.search(q, b62, GapModel(10, 2), 25)
+        assert (idx == ei).all() and (sc == es).all()
+
+
 def test_two_query_scan_with_overflow(port):
     """BLOSUM50 12/2 with two long queries whose planted copies leave the int16 range: the shared scan flags them
     and each query's flagged lanes come back exact from the int32 re-run."""
