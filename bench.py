@@ -406,6 +406,9 @@ def main_native(args):
                          "peak_def": "P_dpx x 2 / 6 (SURVEY 8(d): 6 DPX instructions per two cells), P_dpx = measured "
                                      "VIADDMNMX.S16x2 thread-instr/s (live, this run); the two-stream kernel issues 3.5 ALU-pipe "
                                      "instructions per two cells and the others 4.5, so frac can exceed 1",
+                         # the same pipe rate over the ALU-pipe instructions the kernel actually issues per two cells
+                         "peak_executed_mix": p_dpx * 2.0 / (3.5 if batch else 4.5) * world,
+                         "frac_executed_mix": head_value / (p_dpx * 2.0 / (3.5 if batch else 4.5) * world),
                          "p_dpx_ginst_per_s": p_dpx, "pipe_rates": rates,
                          "traffic": traffic.get("dram_bytes") if traffic else None, "traffic_detail": traffic,
                          "hbm": {"bound": "hbm", "achieved": db_stream_gbs, "peak": hbm_peak, "unit": "GB/s",
