@@ -211,10 +211,18 @@ def main_native(args):
     rank, local_rank, world = env_rank()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device: the native path has no CPU fallback")
+    # Rehearsal of the N > 1 code path on a box with one GPU (tests only, never a bench value): every rank on device 0,
+    # collectives over gloo, because NCCL refuses two ranks on one device.
+    rehearsal = os.environ.get("SWB_BENCH_REHEARSAL") == "1"
+    if rehearsal:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if rehearsal:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
 
     b62 = synth.blosum62()
     gaps = GapModel(*GAPS)
@@ -418,6 +426,8 @@ def main_native(args):
             "single_query": single,
         }
         line["single_query"]["h2d_bytes_per_step"], line["single_query"]["d2h_bytes_per_step"] = h2d_single, d2h_single
+        if rehearsal:
+            line["rehearsal"] = "all ranks on device 0, collectives over gloo: exercises the N > 1 code path, not a bench value"
         if batch:
             line["batched_per_query_ms"] = [{"m": len(q), "ms": ms} for q, ms in zip(queries, batch["per_query_ms"])]
             line["single_query"]["clocks"] = clocks
