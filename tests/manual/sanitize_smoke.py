@@ -57,6 +57,12 @@ with Database(fdb.codes, fdb.offsets) as db:
 print("pair", score_wavefront(seqs[0][:2300], seqs[0], b62, g, 64), "batch", score_batch(seqs[3], [seqs[3], None, seqs[4]], 4, b62, g).tolist())
 mdb = MultiGpuDatabase(fdb.codes, fdb.offsets, [0, 0, 0])
 print("mdb", mdb.search(seqs[1][:100], b62, g, 5)[:2])
+many, _ = mdb.search_many(qs, b62, g, 20)             # every shard at once, one host thread per shard
+for q, (mi, ms_) in zip(qs, many):
+    ei, es, _ = port.run_search(q, fdb, b62, 10, 2, top_k=20)
+    good = bool((mi == ei).all() and (ms_ == es).all())
+    ok &= good
+    print(f"mdb search_many m={len(q)} parity={good}")
 mdb.close()
 print("ALL OK" if ok else "MISMATCH")
 sys.exit(0 if ok else 1)
