@@ -2,7 +2,11 @@
 (no compute without a GPU), argument validation that happens before any CUDA call, the deterministic
 sharding rule, the packed-key encoding, the synthetic data generator."""
 import ctypes as C
+import json
+import os
 import re
+import subprocess
+import sys
 from pathlib import Path
 
 import numpy as np
@@ -224,3 +228,41 @@ def test_batch_plan_deals_queries_over_two_balanced_streams(lib):
     # ... which needs more than one pass (16 tiles): two 400-residue queries share a scan on the whole database only
     assert search.batch_plan(lens, [400, 410])[0].tolist() == [0, 0]
     assert search.batch_plan(lens, [400, 410], shard_count=8)[0].tolist() == [-1, -1]
+
+
+def _bench(*argv, env=None):
+    root = Path(__file__).resolve().parents[1]
+    e = dict(os.environ)
+    e.update(env or {})
+    return subprocess.run([sys.executable, str(root / "bench.py"), *argv], cwd=root, env=e, capture_output=True, text=True,
+                          timeout=600)
+
+
+def test_bench_reference_arm_prints_the_contract_line():
+    """bench.py --impl reference: one JSON line on rank 0 with the native arm's metric/unit/config keys, the CPU
+    baseline description and an e2e object equal to the line's own value; other ranks print nothing and exit 0."""
+    out = _bench("--impl", "reference", "--scale", "0.002", "--steps", "1", "--warmup", "0")
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["metric"] == "GCUPS" and line["unit"] == "GCUPS"
+    assert line["higher_is_better"] is True and line["vs_baseline"] is None and line["n_gpus"] == 1
+    assert line["value"] > 0 and line["ms_per_step"] > 0
+    assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
+    assert line["cpu_baseline"]["value"] == line["value"] and line["cpu_baseline"]["sample"]
+    assert line["e2e"] == {"value": line["value"], "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert "workload" in line["config"] and "model" not in line["config"]
+    other = _bench("--impl", "reference", "--gpus", "2", "--scale", "0.002", "--steps", "1", "--warmup", "0",
+                   env={"RANK": "1", "LOCAL_RANK": "1", "WORLD_SIZE": "2"})
+    assert other.returncode == 0 and other.stdout.strip() == ""
+
+
+def test_bench_native_arm_refuses_to_run_without_a_gpu():
+    """No CPU fallback: without a CUDA device the native arm exits non-zero and says why."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    out = _bench("--scale", "0.002", "--steps", "1", "--warmup", "0")
+    assert out.returncode != 0 and out.stdout.strip() == ""
+    assert "no CPU fallback" in out.stderr
