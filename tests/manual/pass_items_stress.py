@@ -25,6 +25,11 @@ def main():
             for rep in range(reps):
                 many, ms = shard.search_many(queries, b62, g, 10)
                 times.append(float(ms.sum()))
+                for qi in ((7 * rep) % len(queries), (7 * rep + 3) % len(queries)):   # single searches in between, as callers mix them
+                    idx1, sc1, _ = shard.search(queries[qi], b62, g, 10)
+                    if not ((idx1 == singles[qi][0]).all() and (sc1 == singles[qi][1]).all()):
+                        bad += 1
+                        print(f"SINGLE MISMATCH shard {shard_rank}/{shard_count} rep {rep} query {qi}", flush=True)
                 for qi, (idx, sc, _) in enumerate(singles):
                     if not ((many[qi][0] == idx).all() and (many[qi][1] == sc).all()):
                         bad += 1
