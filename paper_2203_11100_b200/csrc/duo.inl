@@ -64,7 +64,13 @@ swb_status score_streams_core(swb_db* db, const uint8_t* const* queries, const u
         return st;
     if ((st = ensure_dev(&db->d_prof2, &db->prof2_cap, static_cast<size_t>(n_tiles) * kDuoSliceWords, &db->device_bytes)) != SWB_OK)
         return st;
-    SWB_CUDA(cudaEventRecord(db->ev[EV_START], s));
+    // pass items: one item per half-group and pass of 16 tiles, pass-major over the whole shard (duo.cuh)
+    const bool pass_items = shared_mode(db) == kSharedPass && n_tiles > kPipeWarps;
+    const uint32_t n_passes = (n_tiles + kPipeWarps - 1) / kPipeWarps;
+    const size_t progress_counters = static_cast<size_t>(n_groups) * 2 * n_passes;
+    if (pass_items && (st = ensure_dev(&db->d_duo_progress, &db->duo_progress_cap, progress_counters, &db->device_bytes)) != SWB_OK)
+        return st;
+    SWB_CUDA(cudaEventRecord(db->ev[EV_START], s));   // every allocation is above this line: none inside the timed scan
     SWB_CUDA(cudaMemsetAsync(db->d_multi_scores, 0, static_cast<size_t>(nq) * std::max<uint32_t>(db->n_slots, 1) * sizeof(int32_t), s));
     SWB_CUDA(cudaMemsetAsync(db->d_counters, 0, 4 * sizeof(uint32_t), s));
     SWB_CUDA(cudaMemcpyAsync(db->d_matrix, stage, off_codes, cudaMemcpyHostToDevice, s));
@@ -86,15 +92,12 @@ swb_status score_streams_core(swb_db* db, const uint8_t* const* queries, const u
     dp.codes = reinterpret_cast<const uint4*>(db->d_codes);
     dp.groups = db->d_groups;
     dp.n_items = n_groups * 2;
-    if (shared_mode(db) == kSharedPass && n_tiles > kPipeWarps) {
-        // pass items: one item per half-group and pass of 16 tiles, pass-major over the whole shard (duo.cuh)
+    if (pass_items) {
         dp.pass_items = 1;
-        dp.n_passes = (n_tiles + kPipeWarps - 1) / kPipeWarps;
+        dp.n_passes = n_passes;
         dp.window = n_groups * 2;
         dp.n_items = n_groups * 2 * dp.n_passes;
-        const size_t counters = static_cast<size_t>(n_groups) * 2 * dp.n_passes;
-        if ((st = ensure_dev(&db->d_duo_progress, &db->duo_progress_cap, counters, &db->device_bytes)) != SWB_OK) return st;
-        SWB_CUDA(cudaMemsetAsync(db->d_duo_progress, 0, counters * sizeof(uint32_t), s));
+        SWB_CUDA(cudaMemsetAsync(db->d_duo_progress, 0, progress_counters * sizeof(uint32_t), s));
         dp.progress = db->d_duo_progress;
     }
     dp.prof2 = db->d_prof2;
