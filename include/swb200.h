@@ -120,7 +120,26 @@ swb_status swb_db_create_flat(const uint8_t* codes, const uint64_t* offsets, uin
  * interleaved, with its index tables -- so that a later process skips parsing, sorting and packing.
  * Little-endian, versioned; swb_db_load rejects files of another version or with a damaged header. */
 swb_status swb_db_save(swb_db* db, const char* path);
+/* Maps the file read-only, validates every table against the invariants the kernels rely on (sizes bounded by the
+ * file size, contiguous longest-first groups, unique in-range db_index values, lengths within their group's rows,
+ * residue codes within the alphabet, header counters equal to what the tables say) and uploads the residues straight
+ * from the mapping.  A stale, truncated or edited file gives SWB_ERR_INVALID, never an out-of-bounds access. */
 swb_status swb_db_load(const char* path, int32_t device, swb_db** out);
+/* Pack on the host and write the file without touching a GPU (replaces parse + encode of fasta.hpp:80-86 for every
+ * later run): same content as swb_db_create + swb_db_save.  names: optional, n NUL-terminated sequence headers that are
+ * stored behind the residues so that a later run needs no FASTA at all (include/swsearch/packed.hpp).
+ *
+ * File layout, little-endian (version 2):
+ *   96-byte header  "SWB200DB", u32 version, u32 n_total n_local n_short n_long shard_rank shard_count max_length,
+ *                   u64 residues padded_rows total_chunks length_threshold n_groups codes_bytes names_bytes
+ *   n_groups x { u64 chunk_base, u32 n_chunks, u32 first_slot }      groups of 64 sequences, longest first
+ *   n_groups*64 x u32 slot_index (db_index, 0xFFFFFFFF = unused)     then n_groups*64 x u32 slot_len
+ *   codes_bytes of residues: codes[((chunk_base + row/8)*32 + slot%32)*16 + (slot/32)*8 + row%8], pad code 24
+ *   optional names: (n_total + 1) x u64 offsets, then the header strings */
+swb_status swb_pack_file(const uint8_t* const* seqs, const uint32_t* lens, uint32_t n, uint64_t length_threshold,
+                         uint32_t shard_rank, uint32_t shard_count, const char* const* names, const char* path);
+swb_status swb_pack_file_flat(const uint8_t* codes, const uint64_t* offsets, uint32_t n, uint64_t length_threshold,
+                              uint32_t shard_rank, uint32_t shard_count, const char* const* names, const char* path);
 
 void swb_db_destroy(swb_db* db);
 swb_status swb_db_info_get(const swb_db* db, swb_db_info* info);
@@ -166,6 +185,17 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
 swb_status swb_score_all_duo(swb_db* db, const uint8_t* query_a, uint32_t len_a, const uint8_t* query_b, uint32_t len_b,
                              const int32_t* matrix, int32_t gap_open, int32_t gap_extend, int32_t* scores_a,
                              int32_t* scores_b, swb_stats* stats);
+
+/* The scores behind swb_search_many: the batch goes through the SAME plan and kernels (shared scans of two query
+ * streams where they apply, single scans for the rest, int32 re-run of flagged lanes included), but every query's
+ * whole score vector is returned in database order: scores[q * n_total + db_index].  Entries of sequences held by
+ * other shards are left as the caller set them.  This is the "sequential scalar scan" of scheduler.hpp:179-183 for
+ * a batch; the parity tests compare it with the oracle at full size.
+ *   scan_of_query  optional [n_queries]: the shared scan each query ran in, -1 = a scan of its own
+ *   rescored_i32   optional [n_queries]: lanes of this shard re-run in int32 for that query (align.hpp:149-153) */
+swb_status swb_score_many(swb_db* db, const uint8_t* const* queries, const uint32_t* query_lens, uint32_t n_queries,
+                          const int32_t* matrix, int32_t gap_open, int32_t gap_extend, int32_t* scores,
+                          int32_t* scan_of_query, uint32_t* rescored_i32);
 
 /* As swb_search, but returns the shard's top_k as packed 64-bit keys
  *   key = (uint64(score) << 32) | (0xFFFFFFFF - db_index)
@@ -242,6 +272,8 @@ swb_status swb_mdb_create_flat(const uint8_t* codes, const uint64_t* offsets, ui
 swb_status swb_mdb_create(const uint8_t* const* seqs, const uint32_t* lens, uint32_t n,
                           uint64_t length_threshold, const int32_t* devices, uint32_t n_devices,
                           swb_mdb** out);
+/* A packed file holding the whole database (shard_count 1) as a one-device swb_mdb: no parsing, sorting or packing. */
+swb_status swb_mdb_load(const char* path, int32_t device, swb_mdb** out);
 void swb_mdb_destroy(swb_mdb* mdb);
 swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len,
                           const int32_t* matrix, int32_t gap_open, int32_t gap_extend,

@@ -11,9 +11,9 @@ loudly if libswb200.so has not been built.  There is no CPU fallback.
 """
 from . import synth  # noqa: F401
 from .search import (Database, GapModel, MultiGpuDatabase, SearchConfig, SwbError, align_traceback, batch_plan, decode_keys,  # noqa: F401
-                     encode_keys, measure_pipe_rates, merge_keys, run_search, score_batch, score_wavefront,
+                     encode_keys, measure_pipe_rates, merge_keys, pack_file, run_search, score_batch, score_wavefront,
                      scan_plan, shard_assignment)
 
 __all__ = ["align_traceback", "batch_plan", "Database", "GapModel", "MultiGpuDatabase", "SearchConfig", "SwbError", "decode_keys", "encode_keys",
-           "measure_pipe_rates", "merge_keys", "run_search", "score_batch", "score_wavefront", "scan_plan", "shard_assignment",
+           "measure_pipe_rates", "merge_keys", "pack_file", "run_search", "score_batch", "score_wavefront", "scan_plan", "shard_assignment",
            "synth"]

@@ -90,6 +90,8 @@ SIGNATURES = {
     "swb_db_destroy": (None, [C.c_void_p]),
     "swb_db_save": (C.c_int, [C.c_void_p, C.c_char_p]),
     "swb_db_load": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    "swb_pack_file": (C.c_int, [C.POINTER(u8p), u32p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_char_p), C.c_char_p]),
+    "swb_pack_file_flat": (C.c_int, [u8p, u64p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_char_p), C.c_char_p]),
     "swb_db_info_get": (C.c_int, [C.c_void_p, C.POINTER(SwbDbInfo)]),
     "swb_db_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "swb_db_set_scan_policy": (C.c_int, [C.c_void_p, C.c_int32]),
@@ -99,6 +101,7 @@ SIGNATURES = {
                                   C.POINTER(SwbHit), u32p, C.POINTER(C.c_float)]),
     "swb_search_keys": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32, u64p,
                                   C.POINTER(C.c_void_p), C.POINTER(SwbStats)]),
+    "swb_score_many": (C.c_int, [C.c_void_p, C.POINTER(u8p), u32p, C.c_uint32, i32p, C.c_int32, C.c_int32, i32p, i32p, u32p]),
     "swb_score_all_duo": (C.c_int, [C.c_void_p, u8p, C.c_uint32, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, i32p, i32p,
                                     C.POINTER(SwbStats)]),
     "swb_merge_keys": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.c_int32, C.c_uint32, C.POINTER(SwbHit), u32p]),
@@ -116,6 +119,7 @@ SIGNATURES = {
     "swb_mdb_create_flat": (C.c_int, [u8p, u64p, C.c_uint32, C.c_uint64, i32p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "swb_mdb_create": (C.c_int, [C.POINTER(u8p), u32p, C.c_uint32, C.c_uint64, i32p, C.c_uint32,
                                  C.POINTER(C.c_void_p)]),
+    "swb_mdb_load": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),
     "swb_mdb_destroy": (None, [C.c_void_p]),
     "swb_mdb_search": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32,
                                  C.POINTER(SwbHit), u32p, C.POINTER(SwbStats)]),

@@ -18,6 +18,10 @@
 //   multi.inl    several GPUs in one process (NCCL)
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
@@ -27,6 +31,7 @@
 #include <cstring>
 #include <functional>
 #include <mutex>
+#include <new>
 #include <string>
 #include <thread>
 #include <vector>
@@ -526,6 +531,76 @@ swb_status swb_search_many(swb_db* db, const uint8_t* const* queries, const uint
             for (const std::vector<uint32_t>* stream : {&sc.a, &sc.b})
                 for (uint32_t q : *stream) ms_per_query[q] = static_cast<float>(ms * query_lens[q] / std::max(columns, 1.0));
         }
+    return SWB_OK;
+}
+
+// The scores behind swb_search_many: the batch goes through the same plan (shared scans of two streams where they
+// apply, single scans for the rest) and the same kernels, and every query's whole score vector comes back in
+// database order -- what the parity tests compare with the oracle (scheduler.hpp:179-183: "sequential scalar scan").
+swb_status swb_score_many(swb_db* db, const uint8_t* const* queries, const uint32_t* query_lens, uint32_t n_queries,
+                          const int32_t* matrix, int32_t gap_open, int32_t gap_extend, int32_t* scores, int32_t* scan_of_query,
+                          uint32_t* rescored_i32) {
+    if (!db) return fail(SWB_ERR_INVALID, "db is null");
+    if (n_queries && (!queries || !query_lens || !scores)) return fail(SWB_ERR_INVALID, "null argument");
+    swb_status st;
+    for (uint32_t q = 0; q < n_queries; ++q)
+        if ((st = check_scoring_args(queries[q], query_lens[q], matrix, gap_open, gap_extend)) != SWB_OK) return st;
+    if (n_queries == 0) return SWB_OK;
+    std::lock_guard<std::mutex> lock(db->mu);
+    DeviceGuard guard(db->device);
+    cudaStream_t s = db->stream;
+    const size_t n_groups = db->meta.groups.size();
+    const uint32_t n_total = db->meta.n_total;
+    std::vector<DuoScan> scans;
+    std::vector<uint32_t> single;
+    plan_batch(scan_knobs(), duo_mode(db, matrix, gap_open, gap_extend), query_lens, n_queries, scans, single);
+    size_t stage = 576 * sizeof(int32_t) + 256 + (n_groups + 1) * 9;
+    uint32_t longest = 0;
+    for (uint32_t q = 0; q < n_queries; ++q) longest = std::max(longest, query_lens[q]);
+    stage += longest;
+    for (const DuoScan& sc : scans) {
+        size_t need = 576 * sizeof(int32_t) + 256 + static_cast<size_t>(std::max(sc.tiles_a, sc.tiles_b)) * sizeof(DuoTile);
+        for (uint32_t q : sc.a) need += (query_lens[q] + 15) & ~15u;
+        for (uint32_t q : sc.b) need += (query_lens[q] + 15) & ~15u;
+        stage = std::max(stage, need);
+    }
+    if ((st = ensure_stage(db, stage)) != SWB_OK) return st;
+    if (!db->d_all_scores)
+        if ((st = dev_alloc(&db->d_all_scores, n_total, &db->device_bytes)) != SWB_OK) return st;
+    const unsigned blocks = std::max(1u, std::min(1024u, (db->n_slots + 255) / 256));
+    // one query's slot scores -> database order -> the caller's row (entries of other shards stay as they were)
+    auto deliver = [&](uint32_t q, const int32_t* slot_scores) -> swb_status {
+        int32_t* row = scores + static_cast<size_t>(q) * n_total;
+        SWB_CUDA(cudaMemcpyAsync(db->d_all_scores, row, static_cast<size_t>(n_total) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        if (db->n_slots) {
+            scatter_scores_kernel<<<blocks, 256, 0, s>>>(slot_scores, db->d_slot_index, db->n_slots, db->d_all_scores);
+            ++db->launches;
+        }
+        SWB_CUDA(cudaMemcpyAsync(row, db->d_all_scores, static_cast<size_t>(n_total) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SWB_CUDA(cudaMemcpyAsync(db->h_counters, db->d_counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        SWB_CUDA(cudaStreamSynchronize(s));   // the staging area is reused by the next job
+        if (rescored_i32) rescored_i32[q] = db->h_counters[1];
+        return SWB_OK;
+    };
+    std::vector<uint32_t> scan_queries, code_off;
+    for (size_t i = 0; i < scans.size(); ++i) {
+        if ((st = score_streams_core(db, queries, query_lens, scans[i], matrix, gap_open, gap_extend, scan_queries, code_off)) != SWB_OK)
+            return st;
+        for (size_t j = 0; j < scan_queries.size(); ++j) {
+            const uint32_t q = scan_queries[j];
+            int32_t* slot_scores = db->d_multi_scores + j * static_cast<size_t>(db->n_slots);
+            SWB_CUDA(cudaMemsetAsync(db->d_counters + 1, 0, sizeof(uint32_t), s));
+            if ((st = rescore_duo_query(db, db->d_multi_codes + code_off[j], query_lens[q], matrix, gap_open, gap_extend, slot_scores)) != SWB_OK)
+                return st;
+            if ((st = deliver(q, slot_scores)) != SWB_OK) return st;
+            if (scan_of_query) scan_of_query[q] = static_cast<int32_t>(i);
+        }
+    }
+    for (uint32_t q : single) {
+        if ((st = score_core(db, queries[q], query_lens[q], matrix, gap_open, gap_extend)) != SWB_OK) return st;
+        if ((st = deliver(q, db->d_slot_scores)) != SWB_OK) return st;
+        if (scan_of_query) scan_of_query[q] = -1;
+    }
     return SWB_OK;
 }
 

@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
         uint4 cw = __ldg(gcodes);
         const uint32_t in_base = in_pos;
         uint32_t staged = in_pos;
+        uint32_t seen = in_pos;   // pass items: the inbound link's published position, as last ACQUIRED
 
         for (uint32_t chunk = 0; chunk < gd.n_chunks; ++chunk) {
             const uint4 cur = cw;
@@ -186,7 +187,14 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
                 if (wrap_in) {
                     // published chunks of the inbound link, as a position on it: the ring's head counter, or (pass
                     // items) the producing pass's progress counter in global memory
-                    auto published = [&]() { return kPassItems ? in_base + ld_poll(prog_in) : lds_acquire(&ctl->head[0]); };
+                    // Pass items: relaxed polls, and ONE ld.acquire.gpu per observed advance (kernels.cuh, wait_progress):
+                    // rows are only ever staged up to an acquired value of the counter, so every cp.async below is
+                    // ordered after the producing warp's stores + st.release.gpu.  All lanes do the same loads.
+                    auto published = [&]() {
+                        if (!kPassItems) return lds_acquire(&ctl->head[0]);
+                        if (in_base + ld_poll(prog_in) > seen) seen = in_base + ld_acquire_gpu(prog_in);
+                        return seen;
+                    };
                     if (staged == in_pos) {
                         const uint32_t need = min(in_pos + 2, in_end);
                         SWB_STAT(w_in, while (published() < need) __nanosleep(kPipePollNs));

@@ -137,34 +137,41 @@ swb_status score_streams_core(swb_db* db, const uint8_t* const* queries, const u
     return SWB_OK;
 }
 
-// After score_streams_core: exact re-run of one query's flagged lanes, its keys and its top k.  `q_dev` is the query's
+// After score_streams_core: exact re-run of one query's flagged lanes (align.hpp:149-153).  `q_dev` is the query's
 // device copy, `scores` its slot scores.
-swb_status finish_duo_query(swb_db* db, const uint8_t* q_dev, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext,
-                            int32_t* scores, uint32_t top_k, const uint64_t** d_out) {
+swb_status rescore_duo_query(swb_db* db, const uint8_t* q_dev, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext,
+                             int32_t* scores) {
     cudaStream_t s = db->stream;
     swb_status st;
     const QueryPlan pl = make_plan(db, m, matrix, open, ext);
-    if (pl.may_overflow) {
-        // the int32 kernel's profile of this query, then the flagged lanes (align.hpp:149-153)
-        const size_t profi_elems = static_cast<size_t>(kProfRows) * pl.n_lane_tiles * 8;
-        if ((st = ensure_dev(&db->d_prof8i, &db->prof8i_cap, profi_elems, &db->device_bytes)) != SWB_OK) return st;
-        ProfileParams pp{};
-        pp.query = q_dev;
-        pp.matrix = db->d_matrix;
-        pp.m = m;
-        pp.shift_main = open;
-        pp.shift_intra = open;
-        pp.pstride = 0;
-        pp.intra_t = pl.intra_t;
-        pp.n_lane_tiles = pl.n_lane_tiles;
-        pp.prof8i = db->d_prof8i;
-        build_profile_kernel<<<64, 256, 0, s>>>(pp);
-        SWB_CUDA(cudaMemsetAsync(db->d_counters + 1, 0, sizeof(uint32_t), s));
-        collect_flagged_kernel<<<std::max(1u, std::min(1024u, (db->n_slots + 255) / 256)), 256, 0, s>>>(
-            scores, db->n_slots, pl.limit, db->d_flag_list, db->d_counters + 1);
-        db->launches += 2;
-        if ((st = run_intra(db, pl, db->d_flag_list, s, scores)) != SWB_OK) return st;
-    }
+    if (!pl.may_overflow) return SWB_OK;
+    // the int32 kernel's profile of this query, then the flagged lanes
+    const size_t profi_elems = static_cast<size_t>(kProfRows) * pl.n_lane_tiles * 8;
+    if ((st = ensure_dev(&db->d_prof8i, &db->prof8i_cap, profi_elems, &db->device_bytes)) != SWB_OK) return st;
+    ProfileParams pp{};
+    pp.query = q_dev;
+    pp.matrix = db->d_matrix;
+    pp.m = m;
+    pp.shift_main = open;
+    pp.shift_intra = open;
+    pp.pstride = 0;
+    pp.intra_t = pl.intra_t;
+    pp.n_lane_tiles = pl.n_lane_tiles;
+    pp.prof8i = db->d_prof8i;
+    build_profile_kernel<<<64, 256, 0, s>>>(pp);
+    SWB_CUDA(cudaMemsetAsync(db->d_counters + 1, 0, sizeof(uint32_t), s));
+    collect_flagged_kernel<<<std::max(1u, std::min(1024u, (db->n_slots + 255) / 256)), 256, 0, s>>>(
+        scores, db->n_slots, pl.limit, db->d_flag_list, db->d_counters + 1);
+    db->launches += 2;
+    return run_intra(db, pl, db->d_flag_list, s, scores);
+}
+
+// ... and then its keys and its top k.
+swb_status finish_duo_query(swb_db* db, const uint8_t* q_dev, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext,
+                            int32_t* scores, uint32_t top_k, const uint64_t** d_out) {
+    cudaStream_t s = db->stream;
+    const swb_status st = rescore_duo_query(db, q_dev, m, matrix, open, ext, scores);
+    if (st != SWB_OK) return st;
     build_keys_kernel<<<std::max(1u, std::min(1024u, (db->n_slots + 255) / 256)), 256, 0, s>>>(scores, db->d_slot_index, db->n_slots,
                                                                                             db->d_keys);
     ++db->launches;

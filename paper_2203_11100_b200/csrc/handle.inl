@@ -24,7 +24,8 @@ void fill_stats(swb_db* db, uint32_t m, swb_stats* st) {
     st->ms_total = span(EV_START, EV_END);
 }
 
-swb_status upload_db(swb_db* db) {
+// codes_src: the interleaved residues when they are not in meta.codes (a memory-mapped packed file, persist.inl).
+swb_status upload_db(swb_db* db, const uint8_t* codes_src = nullptr, size_t codes_bytes = 0) {
     PackedDb& m = db->meta;
     db->n_slots = static_cast<uint32_t>(m.groups.size() * kGroupSeqs);
     db->max_rows = m.groups.empty() ? 0 : m.groups[0].n_chunks * kRowsPerChunk;
@@ -34,7 +35,19 @@ swb_status upload_db(swb_db* db) {
     if ((st = dev_alloc(&(dptr), (vec).size(), tally)) != SWB_OK) return st;                         \
     if (!(vec).empty())                                                                              \
         SWB_CUDA(cudaMemcpy((dptr), (vec).data(), (vec).size() * sizeof((vec)[0]), cudaMemcpyHostToDevice));
-    ALLOC_COPY(db->d_codes, m.codes);
+    if (codes_src) {
+        if ((st = dev_alloc(&db->d_codes, codes_bytes, tally)) != SWB_OK) return st;
+        if (codes_bytes) {
+            // pin the mapping for the copy where the driver allows it (read-only mapping); else a pageable copy
+            const bool pinned = cudaHostRegister(const_cast<uint8_t*>(codes_src), codes_bytes, cudaHostRegisterReadOnly) == cudaSuccess;
+            if (!pinned) cudaGetLastError();
+            const cudaError_t e = cudaMemcpy(db->d_codes, codes_src, codes_bytes, cudaMemcpyHostToDevice);
+            if (pinned) cudaHostUnregister(const_cast<uint8_t*>(codes_src));
+            if (e != cudaSuccess) return fail(SWB_ERR_CUDA, std::string("upload of the packed residues: ") + cudaGetErrorString(e));
+        }
+    } else {
+        ALLOC_COPY(db->d_codes, m.codes);
+    }
     ALLOC_COPY(db->d_groups, m.groups);
     ALLOC_COPY(db->d_slot_index, m.slot_index);
     ALLOC_COPY(db->d_slot_len, m.slot_len);

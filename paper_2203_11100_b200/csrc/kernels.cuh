@@ -146,14 +146,31 @@ struct WaveParams {
 // cooperating warps); the host decides per search (unit_budget in cabi.cu) and the kernel reads the
 // decision back from unit_start.
 
-// Polling load of a progress counter.  Relaxed on purpose: an acquire load makes ptxas invalidate the whole
-// L1 (CCTL.IVALL) on every poll.  Ordering is still safe here: the data the counter guards is only ever read
-// with ld.global.cg (served by L2, the point of coherence), those loads are issued after the poll loop's branch
-// has resolved, and the producer's release store made its border rows visible at L2 before the counter.
+// Cross-CTA hand-off through a progress counter (PTX memory model, scope .gpu).
+//   producer: its 32 lanes store the guarded rows (weak stores), __syncwarp, then lane 0 publishes the counter with
+//             st.release.gpu -- cumulative over the other lanes' stores through the barrier.
+//   consumer: polls with ld.relaxed.gpu (an acquire load makes ptxas emit CCTL.IVALL, an L1 invalidate, per poll:
+//             4.6 % of all stall samples when every poll was an acquire) and, once the wanted value has been seen,
+//             reads the counter ONE more time with ld.acquire.gpu.  The counter only grows, so that load observes
+//             the same or a later release: release -> acquire synchronises, and every later load of the guarded rows
+//             (by lane 0 in program order, by the other lanes after the __syncwarp that follows) happens after the
+//             producer's stores.  One acquire per completed wait, none per poll.
 __device__ __forceinline__ uint32_t ld_poll(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Wait until *p >= need; returns an acquired value (>= need).  Called by one lane; the caller follows with __syncwarp.
+__device__ __forceinline__ uint32_t wait_progress(const uint32_t* p, uint32_t need) {
+    while (ld_poll(p) < need) __nanosleep(64);
+    return ld_acquire_gpu(p);
 }
 
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
@@ -193,8 +210,7 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
         uint32_t diag_in = NO;
         if (kRowBlock && dep != nullptr) {
             // the block above must have finished this tile; then take over its register state
-            if (lane == 0)
-                while (ld_poll(dep) < tile + 1) __nanosleep(64);
+            if (lane == 0) wait_progress(dep, tile + 1);
             __syncwarp();
             const uint4* slot = vstate + static_cast<size_t>(tile) * (kVStateWords / 4) * 32 + lane;
 #pragma unroll
@@ -223,12 +239,10 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
             if (wait) {
                 const uint32_t need = min(rows, static_cast<uint32_t>(row0) + kRowsPerChunk + D);
                 if (P == 1) {          // the producer publishes every chunk: poll every chunk, keep no state
-                    if (lane == 0)
-                        while (ld_poll(dep) < need) __nanosleep(64);
+                    if (lane == 0) wait_progress(dep, need);
                     __syncwarp();
                 } else if (known < need) {
-                    if (lane == 0)
-                        while ((known = ld_poll(dep)) < need) __nanosleep(64);
+                    if (lane == 0) known = wait_progress(dep, need);
                     known = __shfl_sync(0xffffffffu, known, 0);
                 }
             }
@@ -678,7 +692,12 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) traceback_fill_kernel(Tra
                 diag = Hm[k];
                 hl = h + NO;
                 Hm[k] = hl;
-                if (h > best && in_range && col0 + k < p.m) best = h, best_t = static_cast<uint32_t>(r) + 1, best_q = col0 + k + 1;
+                // first maximum in (row, column) order (align.hpp:308).  A thread meets its cells pass by pass, so a
+                // later pass can reach an equal score at an EARLIER row: ties are broken by position, not by arrival
+                if (in_range && col0 + k < p.m) {
+                    const uint32_t ct = static_cast<uint32_t>(r) + 1, cq = col0 + k + 1;
+                    if (h > best || (h == best && h > 0 && (ct < best_t || (ct == best_t && cq < best_q)))) best = h, best_t = ct, best_q = cq;
+                }
             }
             out_h = hl, out_e = E;
 

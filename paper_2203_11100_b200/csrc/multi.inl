@@ -160,6 +160,25 @@ swb_status swb_mdb_create(const uint8_t* const* seqs, const uint32_t* lens, uint
     return mdb_build(src, length_threshold, devices, n_devices, out);
 }
 
+// A packed file (swb_pack_file / swb_db_save, one shard holding the whole database) as a one-device swb_mdb, so that
+// the drop-in's run_search can start from the file instead of parsing and packing (fasta.hpp:80-86).
+swb_status swb_mdb_load(const char* path, int32_t device, swb_mdb** out) {
+    if (!out) return fail(SWB_ERR_INVALID, "out is null");
+    *out = nullptr;
+    swb_db* db = nullptr;
+    const swb_status st = swb_db_load(path, device, &db);
+    if (st != SWB_OK) return st;
+    if (db->meta.shard_count != 1) {
+        swb_db_destroy(db);
+        return fail(SWB_ERR_INVALID, std::string(path) + " holds one shard of several; swb_mdb_load needs an unsharded file");
+    }
+    auto* mdb = new swb_mdb();
+    mdb->devices.assign(1, device);
+    mdb->shards.assign(1, db);
+    *out = mdb;
+    return SWB_OK;
+}
+
 void swb_mdb_destroy(swb_mdb* mdb) {
     if (!mdb) return;
     for (size_t r = 0; r < mdb->comms.size(); ++r)

@@ -184,6 +184,27 @@ class Database:
             out.append((idx, sc))
         return out, ms[:n].copy()
 
+    def score_many(self, queries, matrix, gaps: GapModel):
+        """The score vectors behind search_many (swb_score_many: same plan, same kernels, int32 re-run included):
+        -> (scores[int32, n_queries x n_total] in db order, scan_of_query[int32] (-1: a scan of its own),
+        rescored_i32[uint32] per query)."""
+        mat = _mat(matrix)
+        qs = [_u8(q) for q in queries]
+        n = len(qs)
+        dummy = np.zeros(1, np.uint8)
+        ptrs = (_u8p * max(1, n))()
+        lens = np.zeros(max(1, n), dtype=np.uint32)
+        for i, q in enumerate(qs):
+            ptrs[i] = _ptr(q if len(q) else dummy, _u8p)
+            lens[i] = len(q)
+        scores = np.zeros((max(1, n), max(1, self.n_total)), dtype=np.int32)
+        scan_of = np.full(max(1, n), -2, dtype=np.int32)
+        rescored = np.zeros(max(1, n), dtype=np.uint32)
+        rc = self._lib.swb_score_many(self._h, ptrs, _ptr(lens, _u32p), n, _ptr(mat, _i32p), gaps.open, gaps.extend,
+                                      _ptr(scores, _i32p), _ptr(scan_of, _i32p), _ptr(rescored, _u32p))
+        _raise(self._lib, rc)
+        return scores[:n, :self.n_total], scan_of[:n], rescored[:n]
+
     def search_keys(self, query, matrix, gaps: GapModel, top_k: int = 10):
         """-> (keys[uint64, top_k] zero padded, device pointer or None, stats)."""
         q, mat = _u8(query), _mat(matrix)
@@ -235,6 +256,23 @@ def _align_hits(fn, lib, handle, query, matrix, gaps, index, score, subject_leng
                         score=int(a.score), capped=bool(a.capped),
                         ops=ops[int(offsets[i]):int(offsets[i]) + int(a.n_ops)].copy()))
     return res
+
+
+def pack_file(codes, offsets, path: str, length_threshold: int = 3000, shard_rank: int = 0, shard_count: int = 1, names=None):
+    """Pack a database on the host and write the packed file (swb_pack_file_flat; no GPU needed).  Database.load opens it.
+    names: optional sequence headers, stored behind the residues."""
+    lib = _cabi.load()
+    codes = _u8(codes)
+    offsets = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+    keep = codes if len(codes) else np.zeros(1, np.uint8)
+    n = len(offsets) - 1
+    cnames = None
+    if names is not None:
+        assert len(names) == n
+        cnames = (C.c_char_p * max(1, n))(*[s.encode() for s in names])
+    rc = lib.swb_pack_file_flat(_ptr(keep, _u8p), _ptr(offsets, _u64p), n, int(length_threshold) & (2 ** 64 - 1),
+                                shard_rank, shard_count, cnames, str(path).encode())
+    _raise(lib, rc)
 
 
 def merge_keys(keys, top_k: int, device: int = 0):

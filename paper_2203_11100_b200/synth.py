@@ -270,3 +270,32 @@ def config2(seed: int = 0x5357_4442_02, scale: float = 1.0):
     n = max(64, int(SWISSPROT_SEQS * scale))
     db = make_database(n, target_residues=int(SWISSPROT_RESIDUES * scale), queries=queries, seed=seed)
     return queries, db
+
+
+def config3(seed: int = 0x5357_4442_02):
+    """BASELINE config 3: the long-sequence (intra-task) pool -- the config-2 queries of 3,005 residues and more
+    against only the config-2 database entries of 3,000 residues and more (SearchConfig::length_threshold's default,
+    scheduler.hpp:24).  -> (queries, database, query numbers in config 2)."""
+    queries, db = config2(seed)
+    keep = np.nonzero(db.lengths() >= 3000)[0]
+    sub = db.subset(keep)
+    where = {int(old): new for new, old in enumerate(keep)}
+    qids = [i for i, q in enumerate(queries) if len(q) >= 3005]
+    sub.planted = {k: [where[i] for i in db.planted[qi] if i in where] for k, qi in enumerate(qids)}
+    return [queries[i] for i in qids], sub, qids
+
+
+CONFIG5_SEQS = 2_800_000
+CONFIG5_RESIDUES = 1_000_000_000
+CONFIG5_QUERY_LENGTHS = [144, 1000, 3005, 5147, 5478, 8000, 9000]
+
+
+def config5_share(shards: int = 8, seed: int = 0x5357_4442_05):
+    """BASELINE config 5, one GPU's share: a TrEMBL-shaped database (2.8 M sequences / 1.0 G residues, same length
+    model) is dealt over `shards` GPUs by residue count; one share is a database of 1/shards of the sequences and
+    residues with the same length distribution, generated directly at that size.  BLOSUM50, gap 12/2; the queries
+    include two beyond the reference's 5,478 so that planted copies leave the int16 range and the int32 re-run is
+    exercised.  -> (queries, database)."""
+    queries = make_queries(CONFIG5_QUERY_LENGTHS, seed)
+    db = make_database(CONFIG5_SEQS // shards, target_residues=CONFIG5_RESIDUES // shards, queries=queries, seed=seed)
+    return queries, db

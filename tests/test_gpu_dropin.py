@@ -59,6 +59,45 @@ def test_cli_search_and_bench(lib, tmp_path, port):
     assert lines[1].startswith("0,120,3,") and len(lines) == 2
 
 
+def test_cli_search_from_a_packed_file_equals_the_oracle(lib, tmp_path, port):
+    """SURVEY 8(f) rank 4 as a feature: `swsearch pack` once, then `search --packed` with no FASTA -- the residues go
+    from the mapped file to the device as they are (swb_db_load), headers come from the file.  Ranked hits are checked
+    against the ORACLE (not against the in-memory database), and the output is byte-identical to the FASTA run's."""
+    import numpy as np
+    from oracle import pyoracle as po
+    from paper_2203_11100_b200 import Database, GapModel, synth
+    cli = ROOT / "tests" / "cpp" / "_build" / "swsearch"
+    rng = np.random.default_rng(77)
+    letters = lambda codes: "".join(synth.ALPHABET[c] for c in codes)
+    qs = [synth.random_residues(rng, 150), synth.random_residues(rng, 420)]
+    seqs = [synth.random_residues(rng, int(n)) for n in list(rng.integers(1, 600, 400)) + [0, 1, 3500, 2999, 3000]]
+    seqs[17] = synth.mutate(rng, qs[0], 0.1, 1)
+    seqs[230] = synth.mutate(rng, qs[1], 0.2, 2)
+    (tmp_path / "q.fa").write_text("".join(f">query{i}\n{letters(q)}\n" for i, q in enumerate(qs)))
+    (tmp_path / "db.fa").write_text("".join(f">s{i} d\n{letters(s)}\n" for i, s in enumerate(seqs)))
+    packed = tmp_path / "db.swb"
+    assert subprocess.run([str(cli), "pack", "-d", str(tmp_path / "db.fa"), "-o", str(packed)], capture_output=True).returncode == 0
+    a = subprocess.run([str(cli), "search", "-q", str(tmp_path / "q.fa"), "--packed", str(packed), "--top-k", "6"],
+                       capture_output=True, text=True, timeout=600)
+    b = subprocess.run([str(cli), "search", "-q", str(tmp_path / "q.fa"), "-d", str(tmp_path / "db.fa"), "--top-k", "6"],
+                       capture_output=True, text=True, timeout=600)
+    assert a.returncode == 0 and b.returncode == 0, a.stderr + b.stderr
+    assert a.stdout == b.stdout
+    fdb = po.FlatDb.from_list(seqs)
+    rows = [l.split("\t") for l in a.stdout.splitlines() if l.startswith("  ") and "\t" in l]
+    expect = []
+    for q in qs:
+        ei, es, _ = port.run_search(q, fdb, synth.blosum62(), 10, 2, top_k=6)
+        expect += [(f"s{i} d", int(s)) for i, s in zip(ei, es)]
+    assert [(r[1], int(r[2])) for r in rows] == expect
+    # the same file through the Python binding: score vector of the LOADED database against the oracle
+    with Database.load(packed) as db:
+        got, _ = db.score_all(qs[1], synth.blosum62(), GapModel(10, 2))
+        assert (got == port.score_all(qs[1], fdb, synth.blosum62(), 10, 2)).all()
+        info = db.info()
+        assert info["n_total"] == len(seqs) and info["n_long"] == 2 and info["length_threshold"] == 3000
+
+
 def test_run_search_batch_equals_a_loop_of_run_search(lib):
     """include/swsearch/scheduler.hpp::run_search_batch (swb_search_many behind it, the queries sharing
     database scans): ranked lists, edit scripts and SearchStats identical to calling run_search per query."""

@@ -81,7 +81,52 @@ def test_sampled_score_parity_through_the_pipeline(full, port, b62):
     assert (got == alone).all()
 
 
-def test_batched_sweep_equals_single_searches(full, b62):
+@pytest.fixture(scope="module")
+def oracle_sample(full, port, b62):
+    """Seeded sample of the config-2 database (3,000 random sequences + the 40 longest + empties + length-1 records +
+    every planted homolog of every query) and the oracle's scores of ALL 20 queries against it (~1e11 cells on the
+    host cores)."""
+    queries, sdb, _ = full
+    rng = np.random.default_rng(20)
+    lens = sdb.lengths()
+    planted = np.array([i for qi in range(len(queries)) for i in sdb.planted[qi]])
+    sample = np.unique(np.concatenate([rng.choice(sdb.n, 3000, replace=False), np.argsort(lens)[-40:],
+                                       np.nonzero(lens == 0)[0], np.nonzero(lens == 1)[0], planted]))
+    sub = po.FlatDb.from_list([sdb.seq(int(i)) for i in sample])
+    expected = np.stack([port.score_all(q, sub, b62, 10, 2) for q in queries])
+    return sample, expected
+
+
+def test_batched_sweep_score_vectors_against_the_oracle(full, oracle_sample, b62):
+    """The timed path of bench.py on the timed configuration: the whole 20-query sweep through swb_search_many's plan
+    (one shared scan of two query streams, duo_pipeline_kernel) -- score VECTORS, not ranked lists, against
+    oracle/sw_oracle.c for all 20 queries on the sample."""
+    queries, sdb, db = full
+    sample, expected = oracle_sample
+    scores, scan_of, _ = db.score_many(queries, b62, GapModel(10, 2))
+    assert (scan_of >= 0).all(), f"every query of the sweep is planned into a shared scan, got {scan_of}"
+    assert scores.shape == (len(queries), sdb.n)
+    for qi, q in enumerate(queries):
+        bad = np.nonzero(scores[qi][sample] != expected[qi])[0]
+        assert len(bad) == 0, f"query {qi} (m={len(q)}): {len(bad)} of {len(sample)} sampled scores differ, first db_index {sample[bad[0]]}"
+        assert scores[qi][sdb.planted[qi][0]] == scores[qi].max()      # the exact copy carries the self score
+    assert (scores >= 0).all()
+
+
+def test_single_search_score_vectors_against_the_oracle(full, oracle_sample, b62):
+    """The drop-in path (one swb_search per query: pipeline_s16_kernel + wavefront_s16_kernel): score vectors of all
+    20 queries against the oracle on the sample, and equal to the batched path's everywhere."""
+    queries, sdb, db = full
+    sample, expected = oracle_sample
+    batched, _, _ = db.score_many(queries, b62, GapModel(10, 2))
+    for qi, q in enumerate(queries):
+        got, st = db.score_all(q, b62, GapModel(10, 2))
+        bad = np.nonzero(got[sample] != expected[qi])[0]
+        assert len(bad) == 0, f"query {qi} (m={len(q)}): {len(bad)} sampled scores differ, first db_index {sample[bad[0]]}"
+        assert (got == batched[qi]).all(), f"query {qi}: single and batched score vectors differ"
+
+
+def test_batched_sweep_equals_single_searches(full, b62):def test_batched_sweep_equals_single_searches(full, b62):
     """swb_search_many over the whole 20-query sweep (the queries share one database scan as two streams of the
     two-stream kernel): every ranked list equals the one swb_search returns."""
     queries, sdb, db = full

@@ -285,6 +285,28 @@ def test_traceback_random_against_reference(ref, b62):
             assert got["ops"].tolist() == exp["ops"].tolist(), (m, n, gaps)
 
 
+def test_traceback_equal_maxima_across_passes(ref, b62):
+    """Two equal maxima that ONE thread of the fill kernel meets in the wrong order: the query is wider than one pass
+    (m > 2048), the copy in its second pass ends at an earlier subject row than the copy in its first pass, and both end
+    in columns owned by the same thread (8-column lane tiles 12 and 256 + 12).  The end point must be the first maximum
+    in row-major order (align.hpp:308), so bounds and edit script equal the reference's."""
+    from paper_2203_11100_b200 import align_traceback
+    rng = np.random.default_rng(8)
+    W, P = synth.ALPHABET.index("W"), synth.ALPHABET.index("P")
+    d1 = synth.random_residues(rng, 100)
+    d2 = d1[::-1].copy()                                  # same composition: the same self score
+    q = np.full(2300, W, np.uint8)
+    q[0:100] = d2                                         # ends in column 100   (lane tile 12, pass 0)
+    q[2048:2148] = d1                                     # ends in column 2148  (lane tile 268 = 256 + 12, pass 1)
+    s = np.full(800, P, np.uint8)
+    s[10:110] = d1                                        # matches the pass-1 copy, ends in row 110
+    s[500:600] = d2                                       # matches the pass-0 copy, ends in row 600
+    exp = ref.traceback(q, s, b62, 10, 2)
+    got = align_traceback(q, s, b62, GapModel(10, 2))
+    assert exp["bounds"][1] == 2148 and exp["bounds"][3] == 110       # the reference picks the earlier row
+    assert got["score"] == exp["score"] and got["bounds"] == exp["bounds"] and got["ops"].tolist() == exp["ops"].tolist()
+
+
 def test_packed_database_file_round_trip(tmp_path, b62):
     qs, sdb = synth.config1()
     g = GapModel(10, 2)

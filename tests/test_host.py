@@ -149,6 +149,35 @@ def test_cli_usage_and_exit_codes(lib, tmp_path):
     assert run("stats", "-d", str(bad)).returncode == 4                    # format error
 
 
+def test_cli_pack_and_packed_stats_round_trip(lib, tmp_path):
+    """`swsearch pack` writes the packed database on the host (no GPU); `stats --packed` reads sequences and headers
+    back from it without any FASTA (include/swsearch/packed.hpp), and a write_fasta of the loaded copy would be the
+    original: checked here through the stats line and through Python's reading of the file."""
+    import subprocess
+    cli = str(_cpp_build() / "swsearch")
+    run = lambda *a: subprocess.run([cli, *a], capture_output=True, text=True)
+    rng = np.random.default_rng(5)
+    letters = lambda codes: "".join(synth.ALPHABET[c] for c in codes)
+    seqs = [synth.random_residues(rng, int(n)) for n in [12, 0, 700, 3, 64, 65, 1] + list(rng.integers(1, 500, 90))]
+    fa = tmp_path / "db.fa"
+    fa.write_text("".join(f">s{i} some description\n{letters(s)}\n" for i, s in enumerate(seqs)))
+    packed = tmp_path / "db.swb"
+    out = run("pack", "-d", str(fa), "-o", str(packed), "--threshold", "300")
+    assert out.returncode == 0 and out.stdout.startswith(f"packed {len(seqs)} sequences"), out.stderr
+    assert run("stats", "--packed", str(packed)).stdout == run("stats", "-d", str(fa)).stdout
+    assert run("stats", "--packed", str(packed), "-d", str(fa)).returncode == 2          # one source only
+    assert run("pack", "-d", str(fa)).returncode == 2                                      # no output
+    assert run("stats", "--packed", str(fa)).returncode == 4                               # a FASTA is not a packed file
+    assert run("search", "--packed", str(packed), "-q", str(fa), "--threshold", "100").returncode in (1, 2)   # wrong threshold or no GPU
+    # the file equals what the Python binding packs from the same sequences
+    db = synth.from_sequences(seqs)
+    other = tmp_path / "py.swb"
+    search.pack_file(db.codes, db.offsets, other, length_threshold=300, names=[f"s{i} some description" for i in range(db.n)])
+    assert other.read_bytes() == packed.read_bytes()
+
+
+
+
 def _swissprot_lengths():
     rng = np.random.Generator(np.random.PCG64(0x5357_4442_02))
     return synth.random_lengths(rng, synth.SWISSPROT_SEQS, synth.SWISSPROT_RESIDUES, synth.SWISSPROT_MAXLEN)
@@ -266,3 +295,70 @@ def test_bench_native_arm_refuses_to_run_without_a_gpu():
     out = _bench("--scale", "0.002", "--steps", "1", "--warmup", "0")
     assert out.returncode != 0 and out.stdout.strip() == ""
     assert "no CPU fallback" in out.stderr
+
+
+def _packed_file(tmp_path, name="db.swb"):
+    rng = np.random.default_rng(11)
+    seqs = [synth.random_residues(rng, int(n)) for n in [0, 1, 5, 64, 200, 333, 90, 17, 0, 801] + list(rng.integers(2, 400, 150))]
+    db = synth.from_sequences(seqs)
+    path = tmp_path / name
+    search.pack_file(db.codes, db.offsets, path, length_threshold=300, names=[f"seq{i} test" for i in range(db.n)])
+    return path, db
+
+
+def test_packed_file_layout_and_validation_on_the_host(lib, tmp_path):
+    """swb_pack_file_flat writes the packed shard without a GPU; swb_db_load validates the file on the host before it
+    asks for a device: a sound file gets as far as 'no CUDA device', every damaged one is SWB_ERR_INVALID."""
+    import struct
+    import torch
+    path, db = _packed_file(tmp_path)
+    raw = bytearray(path.read_bytes())
+    magic, version, n_total, n_local, n_short, n_long, rank, count, max_len = struct.unpack_from("<8sIIIIIIII", raw, 0)
+    residues, padded_rows, total_chunks, threshold, n_groups, codes_bytes, names_bytes = struct.unpack_from("<QQQQQQQ", raw, 40)
+    assert magic == b"SWB200DB" and version == 2 and n_total == n_local == db.n and max_len == 801
+    assert residues == db.residues and threshold == 300 and n_short + n_long == db.n and n_long == int((db.lengths() >= 300).sum())
+    assert n_groups == (db.n + 63) // 64 and codes_bytes == total_chunks * 512
+    assert len(raw) == 96 + n_groups * 16 + 2 * n_groups * 64 * 4 + codes_bytes + names_bytes
+    off_groups, off_index = 96, 96 + n_groups * 16
+    off_len, off_codes = off_index + n_groups * 64 * 4, off_index + 2 * n_groups * 64 * 4
+    # the interleaved layout of pack.hpp: slot s of group g, row r -> codes[((chunk_base + r/8)*32 + s%32)*16 + (s/32)*8 + r%8]
+    slot_index = np.frombuffer(raw, np.uint32, n_groups * 64, off_index)
+    slot_len = np.frombuffer(raw, np.uint32, n_groups * 64, off_len)
+    groups = np.frombuffer(raw, np.dtype([("base", "<u8"), ("chunks", "<u4"), ("first", "<u4")]), n_groups, off_groups)
+    codes = np.frombuffer(raw, np.uint8, codes_bytes, off_codes)
+    for slot in (0, 1, 37, 64, 100, db.n - 1):
+        g, s = divmod(slot, 64)
+        seq = db.seq(int(slot_index[slot]))
+        assert len(seq) == slot_len[slot]
+        r = np.arange(len(seq))
+        got = codes[((int(groups[g]["base"]) + r // 8) * 32 + s % 32) * 16 + (s // 32) * 8 + r % 8]
+        assert (got == seq).all()
+    name_off = np.frombuffer(raw, np.uint64, n_total + 1, off_codes + codes_bytes)
+    blob = bytes(raw[off_codes + codes_bytes + 8 * (n_total + 1):])
+    assert names_bytes == 8 * (n_total + 1) + len(blob) and blob[int(name_off[7]):int(name_off[8])] == b"seq7 test"
+    if not torch.cuda.is_available():
+        with pytest.raises(search.SwbError, match="no CUDA device"):
+            search.Database.load(path)
+
+    def damaged(edit, why):
+        bad = bytearray(raw)
+        edit(bad)
+        p = tmp_path / "bad.swb"
+        p.write_bytes(bytes(bad))
+        with pytest.raises(ValueError, match="not a valid swb200 packed database"):
+            search.Database.load(p)
+
+    damaged(lambda b: b.__setitem__(slice(0, 4), b"XXXX"), "magic")
+    damaged(lambda b: struct.pack_into("<I", b, 8, 1), "version")
+    damaged(lambda b: b.__delitem__(slice(len(b) - 512, len(b))), "truncated")
+    damaged(lambda b: struct.pack_into("<Q", b, 72, 1 << 26), "n_groups beyond the file")
+    damaged(lambda b: struct.pack_into("<I", b, 36, 100), "understated max_length (would skip the int32 re-run)")
+    damaged(lambda b: struct.pack_into("<Q", b, 40, residues - 1), "residues")
+    damaged(lambda b: struct.pack_into("<I", b, off_index + 4, struct.unpack_from("<I", b, off_index)[0]), "duplicate db_index")
+    damaged(lambda b: struct.pack_into("<I", b, off_index, n_total + 5), "db_index beyond n_total")
+    damaged(lambda b: struct.pack_into("<I", b, off_len, 100000), "slot_len beyond the group's rows")
+    damaged(lambda b: struct.pack_into("<I", b, off_groups + 12, 64), "first_slot")
+    damaged(lambda b: struct.pack_into("<I", b, off_groups + 16 + 8, 1 << 20), "group order / chunk continuity")
+    damaged(lambda b: b.__setitem__(off_codes + 3, 77), "residue code beyond the alphabet")
+    with pytest.raises(ValueError, match="cannot open"):
+        search.Database.load(tmp_path / "missing.swb")

@@ -5,6 +5,9 @@
 //   swsearch bench  -q query.fa -d db.fa [options]     CSV per SPEC.md:414 (20 repetitions by default)
 //   swsearch sweep  -q query.fa -d db.fa --param lane_width|chunk_width --values 4,8,16 [options]
 //   swsearch stats  -d db.fa                           "<n> sequences, <r> residues, max <l>"
+//   swsearch pack   -d db.fa -o db.swb [--threshold N] pack once on the host (no GPU): sorted, interleaved, with headers
+//   ... --packed db.swb instead of -d db.fa            search / bench / sweep / stats straight from the packed file:
+//                                                      no FASTA parsing, no sort, no pack
 //
 // Exit codes: 0 ok, 2 usage, 3 I/O, 4 format, 5 determinism violation, 1 anything else.
 #include <cstdio>
@@ -17,6 +20,7 @@
 
 #include "swsearch/bench.hpp"
 #include "swsearch/fasta.hpp"
+#include "swsearch/packed.hpp"
 #include "swsearch/scheduler.hpp"
 
 using namespace swsearch;
@@ -28,7 +32,8 @@ struct usage_error : std::runtime_error {
 };
 
 struct CliInvocation {
-    std::string command, query_path, db_path, matrix = "BLOSUM62", output;
+    std::string command, query_path, db_path, packed_path, matrix = "BLOSUM62", output;
+    bool threshold_given = false;
     std::int32_t gap_open = 10, gap_extend = 2;
     SearchConfig config;
     std::size_t repetitions = 20;
@@ -38,9 +43,10 @@ struct CliInvocation {
 };
 
 const char* kUsage =
-    "usage: swsearch <search|bench|sweep|stats> -d DB.fa [-q QUERY.fa] [options]\n"
+    "usage: swsearch <search|bench|sweep|stats|pack> (-d DB.fa | --packed DB.swb) [-q QUERY.fa] [options]\n"
     "  -q, --query PATH        query FASTA (search, bench, sweep)\n"
     "  -d, --db PATH           database FASTA\n"
+    "  --packed PATH           packed database written by 'swsearch pack' (instead of -d)\n"
     "  --matrix NAME|PATH      BLOSUM62 (default) or an NCBI-format matrix file\n"
     "  --gap-open N            default 10\n"
     "  --gap-extend N          default 2\n"
@@ -80,13 +86,14 @@ CliInvocation parse_args(const std::vector<std::string>& argv) {
         if (flag == "-h" || flag == "--help") inv.help = true;
         else if (flag == "-q" || flag == "--query") inv.query_path = value();
         else if (flag == "-d" || flag == "--db") inv.db_path = value();
+        else if (flag == "--packed") inv.packed_path = value();
         else if (flag == "--matrix") inv.matrix = value();
         else if (flag == "--gap-open") inv.gap_open = static_cast<std::int32_t>(number(flag, value()));
         else if (flag == "--gap-extend") inv.gap_extend = static_cast<std::int32_t>(number(flag, value()));
         else if (flag == "-T" || flag == "--workers") inv.config.worker_count = number(flag, value());
         else if (flag == "--lane-width") inv.config.lane_width = number(flag, value());
         else if (flag == "--chunk-width") inv.config.chunk_width = number(flag, value());
-        else if (flag == "--threshold") inv.config.length_threshold = number(flag, value());
+        else if (flag == "--threshold") inv.config.length_threshold = number(flag, value()), inv.threshold_given = true;
         else if (flag == "--top-k") inv.config.top_k = number(flag, value());
         else if (flag == "--no-align") inv.config.compute_alignments = false;
         else if (flag == "--repetitions") inv.repetitions = number(flag, value());
@@ -98,9 +105,13 @@ CliInvocation parse_args(const std::vector<std::string>& argv) {
         else throw usage_error("unknown flag '" + flag + "'");
     }
     if (inv.help) return inv;
-    if (inv.command != "search" && inv.command != "bench" && inv.command != "sweep" && inv.command != "stats")
-        throw usage_error("expected a command: search, bench, sweep or stats");
-    if (inv.db_path.empty()) throw usage_error("a database (-d) is required");
+    if (inv.command != "search" && inv.command != "bench" && inv.command != "sweep" && inv.command != "stats" && inv.command != "pack")
+        throw usage_error("expected a command: search, bench, sweep, stats or pack");
+    if (inv.command == "pack") {
+        if (inv.db_path.empty() || inv.output.empty()) throw usage_error("pack needs a FASTA database (-d) and an output file (-o)");
+        return inv;
+    }
+    if (inv.db_path.empty() == inv.packed_path.empty()) throw usage_error("exactly one of -d and --packed is required");
     if (inv.command != "stats" && inv.query_path.empty()) throw usage_error("a query (-q) is required");
     if (inv.command == "sweep") {
         if (inv.sweep_param != "lane_width" && inv.sweep_param != "chunk_width")
@@ -127,8 +138,22 @@ void print_alignment(std::ostream& out, const Alignment& a, const EncodedSequenc
         out << "    " << top.substr(at, 60) << "\n    " << mid.substr(at, 60) << "\n    " << bottom.substr(at, 60) << "\n";
 }
 
-int run(const CliInvocation& inv, std::ostream& out) {
-    const SequenceDatabase db = load_database(inv.db_path);
+int run(const CliInvocation& inv_in, std::ostream& out) {
+    CliInvocation inv = inv_in;
+    std::unique_ptr<SequenceDatabase> holder;
+    if (!inv.packed_path.empty()) {
+        // stats needs the host copy only; everything else also wants the device copy, made from the same file
+        std::size_t threshold = 0;
+        if (inv.command == "stats") holder = std::make_unique<SequenceDatabase>(load_packed_database(inv.packed_path, &threshold));
+        else holder = open_packed_database(inv.packed_path, &threshold);
+        if (inv.threshold_given && inv.config.length_threshold != threshold)
+            throw usage_error("--threshold " + std::to_string(inv.config.length_threshold) + " differs from the threshold the file was packed with (" +
+                              std::to_string(threshold) + ")");
+        inv.config.length_threshold = threshold;
+    } else {
+        holder = std::make_unique<SequenceDatabase>(load_database(inv.db_path));
+    }
+    const SequenceDatabase& db = *holder;
     if (inv.command == "stats") {
         out << db.num_sequences() << " sequences, " << db.total_residues << " residues, max " << db.max_length << "\n";
         return 0;
@@ -174,6 +199,13 @@ int main(int argc, char** argv) {
         const CliInvocation inv = parse_args(std::vector<std::string>(argv + 1, argv + argc));
         if (inv.help) {
             std::cout << kUsage;
+            return 0;
+        }
+        if (inv.command == "pack") {
+            const SequenceDatabase db = load_database(inv.db_path);
+            save_packed_database(db, inv.output, inv.config.length_threshold);
+            std::cout << "packed " << db.num_sequences() << " sequences, " << db.total_residues << " residues (threshold "
+                      << inv.config.length_threshold << ") -> " << inv.output << "\n";
             return 0;
         }
         if (inv.output.empty()) return run(inv, std::cout);
