@@ -126,7 +126,7 @@ def test_single_search_score_vectors_against_the_oracle(full, oracle_sample, b62
         assert (got == batched[qi]).all(), f"query {qi}: single and batched score vectors differ"
 
 
-def test_batched_sweep_equals_single_searches(full, b62):def test_batched_sweep_equals_single_searches(full, b62):
+def test_batched_sweep_equals_single_searches(full, b62):
     """swb_search_many over the whole 20-query sweep (the queries share one database scan as two streams of the
     two-stream kernel): every ranked list equals the one swb_search returns."""
     queries, sdb, db = full
