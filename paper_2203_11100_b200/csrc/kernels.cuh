@@ -330,6 +330,112 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
     return best;
 }
 
+// Narrow units (kGroupNarrow): one 8-column tile over all rows of a very tall group, for searches whose duration is
+// bounded by that group's chain of rows (short query, 35,213-residue sequence).  A block of 8 rows x 8 columns is swept
+// in ANTI-DIAGONAL order: cell (r, c) needs (r-1, c), (r, c-1) and (r-1, c-1), all on the two previous anti-diagonals, so
+// the eight cells of an anti-diagonal are independent and a block's dependent chain is 15 cell steps instead of 64
+// (the reference's intra-task schedule, align.hpp:194-226, inside one thread).  Everything is unrolled: Hm and F live
+// per column, E and the left neighbour's Hm per row, and d[r] holds the diagonal term of row r's next cell, formed from
+// Hm[c] = H(r-1, c) before cell (r, c) overwrites that register.  With the chain gone a warp is bound by its issue
+// slots (~60 clk per row instead of ~270), so such units want a scheduler of their own: wavefront_s16_kernel hands its
+// first round of units out statically, one per SM at a time.
+__device__ __forceinline__ uint32_t sweep_unit_narrow_s16(const WaveParams& p, const int8_t* prof, const GroupDesc& gd, uint32_t tile,
+                                                          uint32_t n_tiles, const uint32_t* dep, uint32_t* pub, uint32_t lane) {
+    constexpr int T = kNarrowTile, R = static_cast<int>(kRowsPerChunk), P = 4;
+    static_assert(T == 8 && R == 8, "the block sweep is written for 8 x 8");
+    const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
+    const uint32_t n_chunks = gd.n_chunks, rows = n_chunks * kRowsPerChunk;
+    if (n_chunks == 0) return 0;
+    const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
+    const size_t brow0 = static_cast<size_t>(gd.chunk_base) * kRowsPerChunk * 32 + lane;
+    const int8_t* ptile = prof + tile * T;
+    const bool first = tile == 0, last = tile + 1 == n_tiles;
+    const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + brow0;
+    uint2* bout = ((tile & 1) ? p.border1 : p.border0) + brow0;
+
+    uint32_t Hm[T], F[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
+    uint32_t diag_in = NO, best = 0;
+    uint32_t known = 0;   // producer progress (rows), as last acquired
+    uint4 cw = __ldg(gcodes);
+    uint2 q[R];           // inbound border rows of the chunk about to be computed, fetched one chunk ahead
+#pragma unroll
+    for (int i = 0; i < R; ++i) q[i] = make_uint2(NO, NO);
+    if (!first) {
+        if (dep != nullptr) {
+            if (lane == 0) known = wait_progress(dep, min(rows, 2u * kRowsPerChunk));
+            known = __shfl_sync(0xffffffffu, known, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) q[i] = __ldcg(bin + static_cast<size_t>(i) * 32);
+    }
+
+    for (uint32_t chunk = 0; chunk < n_chunks; ++chunk) {
+        const uint4 cur = cw;
+        if (chunk + 1 < n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
+        const size_t row0 = static_cast<size_t>(chunk) * kRowsPerChunk;
+        uint32_t E[R], hl[R], d[R];
+        uint2 pa[R], pb[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t a1 = ((r < 4 ? cur.x : cur.y) >> (8 * (r & 3))) & 0xffu;
+            const uint32_t a2 = ((r < 4 ? cur.z : cur.w) >> (8 * (r & 3))) & 0xffu;
+            pa[r] = *reinterpret_cast<const uint2*>(ptile + a1 * p.pstride);
+            pb[r] = *reinterpret_cast<const uint2*>(ptile + a2 * p.pstride);
+        }
+        // substitution word of (row r, column c): the two sequences' int8 entries, sign-extended into the halves
+        auto sub = [&](int r, int c) {
+            const uint32_t sel = (c & 3) == 0 ? 0xC480u : (c & 3) == 1 ? 0xD591u : (c & 3) == 2 ? 0xE6A2u : 0xF7B3u;
+            return prmt(c < 4 ? pa[r].x : pa[r].y, c < 4 ? pb[r].x : pb[r].y, sel);
+        };
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            hl[r] = q[r].x, E[r] = q[r].y;
+            d[r] = __vadd2(r == 0 ? diag_in : q[r - 1].x, sub(r, 0));   // diagonal of column 0: the row above's inbound Hm
+        }
+        diag_in = q[R - 1].x;
+        // the next chunk's inbound rows travel while this one is computed
+        if (!first && chunk + 1 < n_chunks) {
+            const uint32_t need = min(rows, static_cast<uint32_t>(row0) + 3u * kRowsPerChunk);
+            if (dep != nullptr && known < need) {
+                if (lane == 0) known = wait_progress(dep, need);
+                known = __shfl_sync(0xffffffffu, known, 0);
+            }
+#pragma unroll
+            for (int i = 0; i < R; ++i) q[i] = __ldcg(bin + (row0 + kRowsPerChunk + i) * 32);
+        }
+        uint32_t pend = 0;
+        bool have = false;
+#pragma unroll
+        for (int dd = 0; dd < R + T - 1; ++dd) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int c = dd - r;
+                if (c < 0 || c >= T) continue;
+                E[r] = __viaddmax_s16x2(E[r], NE, hl[r]);
+                F[c] = __viaddmax_s16x2(F[c], NE, Hm[c]);
+                const uint32_t dcur = d[r];
+                if (c + 1 < T) d[r] = __vadd2(Hm[c], sub(r, c + 1));
+                hl[r] = __vadd2(__vimax3_s16x2_relu(dcur, E[r], F[c]), NO);
+                Hm[c] = hl[r];
+                // running maximum over the diagonal terms (exact, see sweep_unit_s16): one VIMNMX3 per two cells
+                if (have) best = __vimax3_s16x2(best, pend, dcur), have = false;
+                else pend = dcur, have = true;
+            }
+        }
+        if (!last) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) bout[(row0 + r) * 32] = make_uint2(hl[r], E[r]);
+        }
+        if (pub != nullptr && ((chunk + 1) % P == 0 || chunk + 1 == n_chunks)) {
+            __syncwarp();
+            if (lane == 0) st_release(pub, static_cast<uint32_t>(row0) + kRowsPerChunk);
+        }
+    }
+    return best;
+}
+
 // Group modes (GroupMode, kNarrowTile): scan_plan.hpp, where the host decides them per search.
 
 // kNarrow: compile the 8-column path in.  Searches without narrow groups (all long queries) launch the variant
@@ -352,10 +458,17 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
 
     const uint32_t lane = threadIdx.x & 31;
 
-    for (;;) {
-        uint32_t u = 0;
-        if (lane == 0) u = atomicAdd(p.ticket, 1u);
-        u = __shfl_sync(0xffffffffu, u, 0);
+    // First round: static, unit (warp, CTA) -> warp x gridDim + CTA, so that consecutive units -- the tiles of the
+    // tallest groups, whose warps are bound by their own chain -- start on different SMs instead of on the sixteen warps
+    // of whichever CTA came up first.  After that, tickets.  Either way a unit's producer (the unit before it) is held
+    // by a resident warp or was handed out earlier: waiting on it cannot deadlock (the grid never exceeds the SM count).
+    const uint32_t static_units = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t round = 0;; ++round) {
+        uint32_t u = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+        if (round > 0) {
+            if (lane == 0) u = static_units + atomicAdd(p.ticket, 1u);
+            u = __shfl_sync(0xffffffffu, u, 0);
+        }
         if (u >= p.n_units) break;
 
         // group of this unit: largest g with unit_start[g] <= u
@@ -386,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
             const uint32_t* dep = t0 > 0 ? p.progress + (u - 1) : nullptr;
             uint32_t* pub = t1 < n_tiles ? p.progress + u : nullptr;
             if (kNarrow && mode == kGroupNarrow)
-                best = sweep_unit_s16<kNarrowTile, 8, 4, false>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane, 0, gd.n_chunks, nullptr);
+                best = sweep_unit_narrow_s16(p, prof, gd, t0, n_tiles, dep, pub, lane);
             else
                 best = sweep_unit_s16<T, 2, 1, false>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane, 0, gd.n_chunks, nullptr);
         }

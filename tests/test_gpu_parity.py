@@ -498,6 +498,18 @@ def test_two_query_scan_against_the_oracle():
     assert out.returncode == 0 and "DUO-SMALL-OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
 
 
+def test_narrow_block_sweep_against_the_oracle():
+    """The wavefront kernel's narrow units (8 x 8 blocks in anti-diagonal order, for groups whose chain of rows bounds
+    the search) forced onto small databases: whole score vectors equal the oracle's (tests/_narrow_small.py)."""
+    import os, subprocess, sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, SWB200_NARROW="0.0001")
+    out = subprocess.run([sys.executable, str(root / "tests" / "_narrow_small.py")], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0 and "NARROW-SMALL-OK" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
+
+
 def test_large_random_batch_shares_scans_and_equals_single_searches(b62):
     """A batch of 60 queries of random lengths (with duplicates, an empty one and a one-residue one) on a database
     where shared scans apply: swb_search_many's ranked lists equal swb_search's, query by query, and the plan it
