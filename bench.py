@@ -54,6 +54,7 @@ def parse_args():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--scale", type=float, default=1.0, help="database size relative to Swiss-Prot (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-workloads", action="store_true", help="skip the config3 / config5_share sub-records")
     return ap.parse_args()
 
 
@@ -197,6 +198,69 @@ def main_reference(args):
     }
     print(json.dumps(line))
     return 0
+
+
+def measure_extra_workload(name, queries, sdb, matrix, gaps, p_dpx, steps, warmup, device_index, stream):
+    """One of BASELINE's other single-GPU workloads (configs[2], configs[4]'s per-GPU share), measured like the headline:
+    `warmup` untimed sweeps, then `steps` sweeps one query at a time (swb_search, device-timed per search and end to
+    end with host buffers) and as one batch (swb_search_many), clocks sampled during the timed region.  Hits of every
+    repetition are compared with the first and the planted exact copy must be the top hit."""
+    import torch
+    from paper_2203_11100_b200 import Database, GapModel
+    g = GapModel(*gaps)
+    cells = sum(len(q) for q in queries) * sdb.residues
+    with Database(sdb.codes, sdb.offsets, device=device_index) as db:
+        db.set_stream(stream.cuda_stream)
+        info = db.info()
+        first = None
+        for _ in range(max(warmup, 1)):
+            first = [db.search(q, matrix, g, TOP_K)[:2] for q in queries]
+            db.search_many(queries, matrix, g, TOP_K)
+        for qi, (idx, sc) in enumerate(first):
+            if idx[0] != sdb.planted[qi][0]:
+                raise SystemExit(f"{name}: query {qi}: top hit {idx[0]} is not the planted exact copy")
+        sampler = ClockSampler(device_index)
+        torch.cuda.synchronize()
+        sampler.start()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        dev_ms, launches, rescored, per_query = 0.0, 0, 0, []
+        for _ in range(steps):
+            per_query = []
+            for q, (fi, fs) in zip(queries, first):
+                idx, sc, st = db.search(q, matrix, g, TOP_K)
+                if not ((idx == fi).all() and (sc == fs).all()):
+                    raise SystemExit(f"{name}: determinism_error in a single search")
+                dev_ms += st["ms_total"]
+                launches += st["kernel_launches"]
+                rescored += st["rescored_i32"]
+                per_query.append({"m": len(q), "gcups": len(q) * sdb.residues / (st["ms_total"] * 1e-3) / 1e9, "ms": st["ms_total"],
+                                  "rescored_i32": int(st["rescored_i32"])})
+        e1.record(stream)
+        batch_ms = 0.0
+        l0 = db.info()["kernel_launches_total"]
+        for _ in range(steps):
+            many, ms = db.search_many(queries, matrix, g, TOP_K)
+            batch_ms += float(ms.sum())
+            for (a, b), (c, e) in zip(many, first):
+                if not ((a == c).all() and (b == e).all()):
+                    raise SystemExit(f"{name}: determinism_error in the batched sweep")
+        e2.record(stream)
+        torch.cuda.synchronize()
+        batch_launches = db.info()["kernel_launches_total"] - l0
+        clocks = sampler.stop()
+    roof = p_dpx * 2.0 / 6.0
+    single = cells * steps / (dev_ms * 1e-3) / 1e9
+    batched = cells * steps / (batch_ms * 1e-3) / 1e9
+    return {"workload": name, "metric": "GCUPS", "value": max(single, batched), "unit": "GCUPS",
+            "single_query": {"value": single, "e2e": cells * steps / (e0.elapsed_time(e1) * 1e-3) / 1e9, "gpu_launches": launches,
+                             "per_query": per_query},
+            "batched": {"value": batched, "e2e": cells * steps / (e1.elapsed_time(e2) * 1e-3) / 1e9, "gpu_launches": batch_launches},
+            "steps": steps, "warmup": max(warmup, 1), "rescored_i32_per_sweep": rescored // max(steps, 1),
+            "roofline": {"bound": "dpx_alu", "peak": roof, "unit": "GCUPS", "frac": max(single, batched) / roof,
+                         "frac_single_query": single / roof, "peak_def": "P_dpx x 2 / 6, P_dpx measured live in this run"},
+            "db": {k: info[k] for k in ("n_total", "n_groups", "residues", "padded_residues", "n_short", "n_long")},
+            "clocks": clocks}
 
 
 # ------------------------------------------------------------------------------------------------------------
@@ -348,13 +412,25 @@ def main_native(args):
         scan_gcups = total_cells * steps / (scan_ms * 1e-3) / 1e9
         hbm_peak = peaks["hbm_gbs"] if peaks else 6650.0
         db_stream_gbs = sdb.residues * len(queries) * steps / (scan_ms * 1e-3) / 1e9
-        traffic = None
+        # DRAM bytes per launch come from an ncu --set full capture (profiles/traffic.json, written by
+        # tools/traffic_from_ncu.py), stamped with the hash of the kernel sources it was taken from: a capture of other
+        # kernels than the ones timed here is not quoted
+        traffic, traffic_note = None, "profiles/traffic.json missing"
         tfile = ROOT / "profiles" / "traffic.json"
         if tfile.exists():
+            from paper_2203_11100_b200.build import kernel_source_hash
             traffic = json.loads(tfile.read_text())
+            if traffic.get("kernel_source_sha256") != kernel_source_hash():
+                traffic_note = (f"stale: profiles/traffic.json was captured from kernel sources {str(traffic.get('kernel_source_sha256'))[:12]}, "
+                                f"this run's are {kernel_source_hash()[:12]}")
+                traffic = None
+            else:
+                traffic_note = "ncu capture of these kernel sources (hash matches)"
         single = {"value": value, "e2e": e2e, "unit": "GCUPS", "ms_per_step": e2e_ms / steps, "gpu_launches": launches,
                   "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                   "scan_kernel_gcups": scan_gcups,
+                  # host time per search that the device does not hide: (end-to-end - device) / searches
+                  "host_overhead_us_per_search": (e2e_ms - dev_ms) * 1e3 / (steps * len(queries)),
                   "api": "swb_search, one call per query (what swsearch::run_search forwards to)" +
                          ("" if world == 1 else " + one all-gather of k keys per search"),
                   "per_query": [{"m": m, "gcups": m * sdb.residues / (ms * 1e-3) / 1e9, "ms": ms, "scan_ms": sms,
@@ -418,7 +494,7 @@ def main_native(args):
                          "peak_executed_mix": p_dpx * 2.0 / (3.5 if batch else 4.5) * world,
                          "frac_executed_mix": head_value / (p_dpx * 2.0 / (3.5 if batch else 4.5) * world),
                          "p_dpx_ginst_per_s": p_dpx, "pipe_rates": rates,
-                         "traffic": traffic.get("dram_bytes") if traffic else None, "traffic_detail": traffic,
+                         "traffic": traffic.get("dram_bytes") if traffic else None, "traffic_detail": traffic, "traffic_note": traffic_note,
                          "hbm": {"bound": "hbm", "achieved": db_stream_gbs, "peak": hbm_peak, "unit": "GB/s",
                                  "frac": db_stream_gbs / hbm_peak,
                                  "peak_src": "MEASURED_PEAKS.json" if peaks else "fallback",
@@ -431,6 +507,19 @@ def main_native(args):
         if batch:
             line["batched_per_query_ms"] = [{"m": len(q), "ms": ms} for q, ms in zip(queries, batch["per_query_ms"])]
             line["single_query"]["clocks"] = clocks
+        if world == 1 and args.scale == 1.0 and not args.no_extra_workloads:
+            # BASELINE configs[2] and configs[4] (one GPU's share) next to the headline, same run, same clocks protocol
+            engine.close()
+            q3, db3, _ = synth.config3()
+            line["config3"] = measure_extra_workload(
+                "config3: long-sequence pool -- the 9 queries >= 3005 vs only the config-2 entries >= 3000 residues "
+                f"({db3.n} seqs, {db3.residues} residues), BLOSUM62 10/2", q3, db3, b62, GAPS, p_dpx, args.steps, args.warmup,
+                local_rank, stream)
+            q5, db5 = synth.config5_share()
+            line["config5_share"] = measure_extra_workload(
+                "config5_share: one GPU's 1/8 share of the TrEMBL-shaped DB (350,000 seqs, ~125M residues), BLOSUM50 12/2, "
+                "queries 144..9000 (planted copies of the two longest leave int16: int32 re-run)", q5, db5, synth.blosum50(),
+                (12, 2), p_dpx, args.steps, args.warmup, local_rank, stream)
         if world == 1 and not args.no_cpu_baseline:
             qs, sub = cpu_sample(queries, sdb)
             threads = os.cpu_count() or 1

@@ -13,7 +13,9 @@
  *                             (profile -> partition -> both kernels -> merge_results), i.e. the
  *                             region SPEC.md:403 times; traceback (scheduler.hpp:246-249) stays host C++
  *   swb_search_keys           the same, returning packed sort keys for the multi-GPU merge
+ *   swb_search_keys_device    the same, enqueued on the caller's stream, keys left in device memory
  *   swb_merge_keys            merge_results               scheduler.hpp:106-117  (across shards)
+ *   swb_db_merge_keys         the same on the handle's stream, from gathered device keys
  *   swb_score_all             "sequential scalar scan"    scheduler.hpp:179-183  (all N scores)
  *   swb_score_batch           sw_score_batch              align.hpp:91-159
  *   swb_score_pair            sw_score_wavefront          align.hpp:166-229
@@ -146,7 +148,8 @@ swb_status swb_db_info_get(const swb_db* db, swb_db_info* info);
 
 /* Use an externally owned cudaStream_t (passed as an integer/pointer value, e.g.
  * torch.cuda.current_stream().cuda_stream) for all work of this handle; 0 restores the
- * handle's own stream. */
+ * handle's own (non-blocking) stream.  The legacy default stream is named explicitly, as
+ * cudaStreamLegacy ((cudaStream_t)0x1). */
 swb_status swb_db_set_stream(swb_db* db, void* cuda_stream);
 
 /* Which kernel scans the database (results are identical; tests and tuning use this to exercise each path):
@@ -208,6 +211,21 @@ swb_status swb_search_keys(swb_db* db, const uint8_t* query, uint32_t query_len,
                            const int32_t* matrix, int32_t gap_open, int32_t gap_extend,
                            uint32_t top_k, uint64_t* host_keys, void** device_keys,
                            swb_stats* stats);
+
+/* The same search for a caller that owns the stream and does the exchange itself (one process per GPU under
+ * torch.distributed / NCCL): everything is ENQUEUED on the handle's stream (swb_db_set_stream) and the top_k packed
+ * keys, zero padded, are left in the caller's DEVICE buffer `device_keys_out` (top_k entries).  Returns without
+ * synchronising; the keys are valid for work enqueued on the same stream afterwards (an all-gather, then
+ * swb_db_merge_keys).  At most one such search is in flight per handle: the next call on the handle waits for it. */
+swb_status swb_search_keys_device(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
+                                  int32_t gap_open, int32_t gap_extend, uint32_t top_k, uint64_t* device_keys_out);
+
+/* The cross-shard merge on the handle's stream: top_k of n packed DEVICE keys (the gathered per-shard lists; zeros
+ * are ignored) -> hits on the host.  One device-to-host copy of top_k keys and the only synchronisation of a sharded
+ * search.  stats (optional) describes the search enqueued by the last swb_search_keys_device on this handle
+ * (query_len = its query length). */
+swb_status swb_db_merge_keys(swb_db* db, const uint64_t* device_keys, uint64_t n, uint32_t top_k, swb_hit* hits,
+                             uint32_t* n_hits, uint32_t query_len, swb_stats* stats);
 
 /* Top-k select over n packed keys on `device` (the cross-shard merge; zeros are ignored).
  * keys is a host pointer unless keys_on_device != 0. */

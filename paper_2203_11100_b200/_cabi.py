@@ -101,6 +101,9 @@ SIGNATURES = {
                                   C.POINTER(SwbHit), u32p, C.POINTER(C.c_float)]),
     "swb_search_keys": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32, u64p,
                                   C.POINTER(C.c_void_p), C.POINTER(SwbStats)]),
+    "swb_search_keys_device": (C.c_int, [C.c_void_p, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, C.c_uint32, C.c_void_p]),
+    "swb_db_merge_keys": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(SwbHit), u32p, C.c_uint32,
+                                    C.POINTER(SwbStats)]),
     "swb_score_many": (C.c_int, [C.c_void_p, C.POINTER(u8p), u32p, C.c_uint32, i32p, C.c_int32, C.c_int32, i32p, i32p, u32p]),
     "swb_score_all_duo": (C.c_int, [C.c_void_p, u8p, C.c_uint32, u8p, C.c_uint32, i32p, C.c_int32, C.c_int32, i32p, i32p,
                                     C.POINTER(SwbStats)]),

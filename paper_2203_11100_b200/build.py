@@ -26,6 +26,19 @@ NVCC_FLAGS = [
 ]
 
 
+KERNEL_SOURCES = ["kernels.cuh", "pipeline.cuh", "duo.cuh"]
+
+
+def kernel_source_hash() -> str:
+    """sha256 over the device code of the scan kernels: ncu-derived numbers that bench.py quotes (profiles/traffic.json)
+    are stamped with it and dropped when the kernels have changed since the capture."""
+    import hashlib
+    h = hashlib.sha256()
+    for name in KERNEL_SOURCES:
+        h.update((CSRC / name).read_bytes())
+    return h.hexdigest()
+
+
 def _nvcc() -> str:
     for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
         if cand and os.path.exists(cand):

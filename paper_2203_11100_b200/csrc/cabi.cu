@@ -26,10 +26,12 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -166,7 +168,10 @@ struct swb_db {
     size_t stage_base = 0;        // offset of the current query's staging area (swb_search_many pipelines several)
     std::vector<cudaEvent_t> many_events;   // per-query start/end events of swb_search_many
     uint32_t* h_counters = nullptr;   // pinned copy of d_counters
+    uint64_t* h_merge = nullptr;      // pinned: merged keys down (swb_db_merge_keys)
+    uint32_t merge_cap = 0;
     cudaEvent_t ev[EV_COUNT] = {};
+    bool async_pending = false;   // swb_search_keys_device: a search is enqueued whose inputs still sit in h_stage
     uint32_t launches = 0;        // of the current search
     uint32_t launches_total = 0;  // of all earlier ones
     uint32_t last_units = 0;
@@ -296,6 +301,7 @@ void swb_db_destroy(swb_db* db) {
             if (p) cudaFree(p);
         if (db->h_stage) cudaFreeHost(db->h_stage);
         if (db->h_counters) cudaFreeHost(db->h_counters);
+        if (db->h_merge) cudaFreeHost(db->h_merge);
         for (auto& ev : db->ev)
             if (ev) cudaEventDestroy(ev);
         for (auto& ev : db->many_events) cudaEventDestroy(ev);
@@ -373,6 +379,68 @@ swb_status swb_search_keys(swb_db* db, const uint8_t* query, uint32_t query_len,
         for (uint32_t i = k_eff; i < top_k; ++i) host_keys[i] = 0;
     }
     if (device_keys) *device_keys = (k_eff == top_k) ? const_cast<uint64_t*>(d_top) : nullptr;
+    fill_stats(db, query_len, stats);
+    return SWB_OK;
+}
+
+swb_status swb_search_keys_device(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
+                                  int32_t gap_open, int32_t gap_extend, uint32_t top_k, uint64_t* device_keys_out) {
+    if (!db) return fail(SWB_ERR_INVALID, "db is null");
+    if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
+    if (!device_keys_out) return fail(SWB_ERR_INVALID, "device_keys_out is null");
+    swb_status st = check_scoring_args(query, query_len, matrix, gap_open, gap_extend);
+    if (st != SWB_OK) return st;
+    std::lock_guard<std::mutex> lock(db->mu);
+    DeviceGuard guard(db->device);
+    const uint64_t n_keys = db->meta.n_local;
+    const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint64_t>(n_keys, 1)));
+    const uint64_t* d_top = nullptr;
+    st = search_keys_locked(db, query, query_len, matrix, gap_open, gap_extend, k_eff, &d_top);
+    if (st != SWB_OK) return st;
+    cudaStream_t s = db->stream;
+    if (k_eff < top_k) SWB_CUDA(cudaMemsetAsync(device_keys_out, 0, static_cast<size_t>(top_k) * sizeof(uint64_t), s));
+    SWB_CUDA(cudaMemcpyAsync(device_keys_out, d_top, static_cast<size_t>(k_eff) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    SWB_CUDA(cudaMemcpyAsync(db->h_counters, db->d_counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SWB_CUDA(cudaEventRecord(db->ev[EV_END], s));
+    db->async_pending = true;
+    return SWB_OK;
+}
+
+swb_status swb_db_merge_keys(swb_db* db, const uint64_t* device_keys, uint64_t n, uint32_t top_k, swb_hit* hits,
+                             uint32_t* n_hits, uint32_t query_len, swb_stats* stats) {
+    if (!db) return fail(SWB_ERR_INVALID, "db is null");
+    if (!hits || !n_hits) return fail(SWB_ERR_INVALID, "hits/n_hits are null");
+    if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
+    if (n && !device_keys) return fail(SWB_ERR_INVALID, "device_keys is null");
+    *n_hits = 0;
+    std::lock_guard<std::mutex> lock(db->mu);
+    DeviceGuard guard(db->device);
+    cudaStream_t s = db->stream;
+    const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, n));
+    // the keys come down next to, not over, the pending search's inputs: a second pinned buffer of their own
+    if (k_eff > db->merge_cap) {
+        if (db->h_merge) cudaFreeHost(db->h_merge);
+        db->h_merge = nullptr, db->merge_cap = 0;
+        SWB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&db->h_merge), static_cast<size_t>(k_eff) * 2 * sizeof(uint64_t)));
+        db->merge_cap = k_eff * 2;
+    }
+    if (k_eff) {
+        const uint64_t* d_top = nullptr;
+        const uint32_t launches_before = db->launches;
+        swb_status st = select_topk(db, device_keys, n, k_eff, &d_top);
+        if (st != SWB_OK) return st;
+        db->launches = launches_before;   // the merge's launches are not the search's
+        db->launches_total += 1;
+        SWB_CUDA(cudaMemcpyAsync(db->h_merge, d_top, static_cast<size_t>(k_eff) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    }
+    SWB_CUDA(cudaStreamSynchronize(s));
+    db->async_pending = false;
+    uint32_t cnt = 0;
+    for (uint32_t i = 0; i < k_eff && db->h_merge[i]; ++i, ++cnt) {
+        hits[cnt].db_index = 0xFFFFFFFFu - static_cast<uint32_t>(db->h_merge[i] & 0xFFFFFFFFu);
+        hits[cnt].score = static_cast<int32_t>(db->h_merge[i] >> 32);
+    }
+    *n_hits = cnt;
     fill_stats(db, query_len, stats);
     return SWB_OK;
 }

@@ -13,6 +13,7 @@ swb_status score_streams_core(swb_db* db, const uint8_t* const* queries, const u
                               std::vector<uint32_t>& code_off) {
     cudaStream_t s = db->stream;
     swb_status st;
+    if ((st = settle_async(db)) != SWB_OK) return st;
     const uint32_t n_tiles = std::max(scan.tiles_a, scan.tiles_b);
     const uint32_t n_groups = static_cast<uint32_t>(db->meta.groups.size());
     scan_queries.clear();

@@ -47,6 +47,60 @@ struct NcclApi {
 
 constexpr int kNcclUint64 = 5;   // ncclUint64 (nccl.h)
 
+// One persistent host thread per shard: a search hands every worker its shard's job and waits for all of them,
+// instead of creating and joining G threads per call (the reference does the latter, scheduler.hpp:218-229).
+class ShardPool {
+public:
+    explicit ShardPool(size_t n) : jobs_(n), busy_(n, false) {
+        for (size_t r = 0; r < n; ++r) threads_.emplace_back([this, r] { loop(r); });
+    }
+    ~ShardPool() {
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            stop_ = true;
+        }
+        wake_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+    // fn(r) on worker r for every r, concurrently; returns when all are done
+    void run(const std::function<void(size_t)>& fn) {
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            for (size_t r = 0; r < jobs_.size(); ++r) jobs_[r] = &fn, busy_[r] = true;
+            pending_ = jobs_.size();
+        }
+        wake_.notify_all();
+        std::unique_lock<std::mutex> lock(mu_);
+        done_.wait(lock, [this] { return pending_ == 0; });
+    }
+
+private:
+    void loop(size_t r) {
+        for (;;) {
+            const std::function<void(size_t)>* job = nullptr;
+            {
+                std::unique_lock<std::mutex> lock(mu_);
+                wake_.wait(lock, [&] { return stop_ || busy_[r]; });
+                if (stop_) return;
+                job = jobs_[r];
+            }
+            (*job)(r);
+            {
+                std::lock_guard<std::mutex> lock(mu_);
+                busy_[r] = false;
+                if (--pending_ == 0) done_.notify_all();
+            }
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable wake_, done_;
+    std::vector<const std::function<void(size_t)>*> jobs_;
+    std::vector<bool> busy_;
+    size_t pending_ = 0;
+    bool stop_ = false;
+    std::vector<std::thread> threads_;
+};
+
 }  // namespace
 
 struct swb_mdb {
@@ -58,6 +112,7 @@ struct swb_mdb {
     std::vector<uint64_t*> d_gather;   // per shard: G * k_cap keys on that shard's device
     std::vector<uint64_t*> d_send;     // per shard: k_cap keys
     uint32_t k_cap = 0;
+    std::unique_ptr<ShardPool> pool;   // one worker per shard, created with the first multi-shard search
     std::mutex mu;
 };
 
@@ -257,14 +312,12 @@ swb_status swb_mdb_search_many(swb_mdb* mdb, const uint8_t* const* queries, cons
     std::vector<std::vector<swb_hit>> shard_hits(G, std::vector<swb_hit>(static_cast<size_t>(n_queries) * top_k));
     std::vector<std::vector<uint32_t>> shard_counts(G, std::vector<uint32_t>(n_queries, 0));
     std::vector<std::vector<float>> shard_ms(G, std::vector<float>(n_queries, 0.f));
-    std::vector<std::thread> pool;
-    for (size_t r = 0; r < G; ++r)
-        pool.emplace_back([&, r] {
-            sts[r] = swb_search_many(mdb->shards[r], queries, query_lens, n_queries, matrix, gap_open, gap_extend, top_k,
-                                     shard_hits[r].data(), shard_counts[r].data(), shard_ms[r].data());
-            if (sts[r] != SWB_OK) errs[r] = g_error;
-        });
-    for (auto& t : pool) t.join();
+    if (!mdb->pool) mdb->pool.reset(new ShardPool(G));
+    mdb->pool->run([&](size_t r) {
+        sts[r] = swb_search_many(mdb->shards[r], queries, query_lens, n_queries, matrix, gap_open, gap_extend, top_k,
+                                 shard_hits[r].data(), shard_counts[r].data(), shard_ms[r].data());
+        if (sts[r] != SWB_OK) errs[r] = g_error;
+    });
     for (size_t r = 0; r < G; ++r)
         if (sts[r] != SWB_OK) return fail(sts[r], "shard " + std::to_string(r) + ": " + errs[r]);
     std::vector<uint64_t> keys;
@@ -313,37 +366,19 @@ swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len
     const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(top_k, std::max<uint32_t>(n_total, 1)));
     if ((st = mdb_ensure_buffers(mdb, k)) != SWB_OK) return st;
 
-    // 1. every shard scores and selects concurrently; its keys stay on its device
+    // 1. every shard enqueues its search on its own stream (one persistent worker per shard: the host-side preparation
+    //    runs side by side); the k keys land in d_send on the shard's device, nothing synchronises yet
     std::vector<swb_status> sts(G, SWB_OK);
     std::vector<std::string> errs(G);
-    std::vector<swb_stats> sstats(G);
-    std::vector<std::thread> pool;
-    for (size_t r = 0; r < G; ++r)
-        pool.emplace_back([&, r] {
-            swb_db* db = mdb->shards[r];
-            std::vector<uint64_t> host(k);
-            void* dkeys = nullptr;
-            sts[r] = swb_search_keys(db, query, query_len, matrix, gap_open, gap_extend, k, host.data(), &dkeys, &sstats[r]);
-            if (sts[r] != SWB_OK) {
-                errs[r] = g_error;
-                return;
-            }
-            DeviceGuard guard(db->device);
-            // the shard's keys are already on its device; only a shard holding fewer than k sequences goes
-            // through the zero-padded host copy
-            cudaError_t e = dkeys ? cudaMemcpyAsync(mdb->d_send[r], dkeys, k * sizeof(uint64_t), cudaMemcpyDeviceToDevice, db->stream)
-                                  : cudaMemcpyAsync(mdb->d_send[r], host.data(), k * sizeof(uint64_t), cudaMemcpyHostToDevice, db->stream);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(db->stream);
-            if (e != cudaSuccess) {
-                sts[r] = SWB_ERR_CUDA;
-                errs[r] = cudaGetErrorString(e);
-            }
-        });
-    for (auto& t : pool) t.join();
+    if (!mdb->pool) mdb->pool.reset(new ShardPool(G));
+    mdb->pool->run([&](size_t r) {
+        sts[r] = swb_search_keys_device(mdb->shards[r], query, query_len, matrix, gap_open, gap_extend, k, mdb->d_send[r]);
+        if (sts[r] != SWB_OK) errs[r] = g_error;
+    });
     for (size_t r = 0; r < G; ++r)
         if (sts[r] != SWB_OK) return fail(sts[r], errs[r]);
 
-    // 2. exchange: k keys per shard
+    // 2. exchange: k keys per shard, enqueued behind each shard's search on its stream
     if (mdb->distinct) {
         int rc = mdb->nccl.GroupStart();
         for (size_t r = 0; r < G && rc == 0; ++r) {
@@ -353,21 +388,30 @@ swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len
         const int rc_end = mdb->nccl.GroupEnd();
         if (rc == 0) rc = rc_end;
         if (rc != 0) return fail(SWB_ERR_NCCL, std::string("ncclAllGather: ") + mdb->nccl.GetErrorString(rc));
-        for (size_t r = 0; r < G; ++r) {
-            DeviceGuard guard(mdb->devices[r]);
-            SWB_CUDA(cudaStreamSynchronize(mdb->shards[r]->stream));
-        }
     } else {
+        // shards that share a device (tests on a one-GPU box): device-to-device copies on shard 0's stream, each
+        // behind the event that ends its shard's search
         DeviceGuard guard(mdb->devices[0]);
-        for (size_t r = 0; r < G; ++r)
+        for (size_t r = 0; r < G; ++r) {
+            if (r) SWB_CUDA(cudaStreamWaitEvent(mdb->shards[0]->stream, mdb->shards[r]->ev[EV_END], 0));
             SWB_CUDA(cudaMemcpyPeerAsync(mdb->d_gather[0] + r * k, mdb->devices[0], mdb->d_send[r], mdb->devices[r],
                                          k * sizeof(uint64_t), mdb->shards[0]->stream));
-        SWB_CUDA(cudaStreamSynchronize(mdb->shards[0]->stream));
+        }
     }
 
-    // 3. global select on shard 0's device
-    st = swb_merge_keys(mdb->d_gather[0], G * k, 1, mdb->devices[0], top_k, hits, n_hits);
+    // 3. global select on shard 0's stream: the one device-to-host copy (k hits) and, for shard 0, the one
+    //    synchronisation; the other shards only have to finish before their statistics are read
+    std::vector<swb_stats> sstats(G);
+    st = swb_db_merge_keys(mdb->shards[0], mdb->d_gather[0], G * k, top_k, hits, n_hits, query_len, &sstats[0]);
     if (st != SWB_OK) return st;
+    for (size_t r = 1; r < G; ++r) {
+        swb_db* db = mdb->shards[r];
+        std::lock_guard<std::mutex> shard_lock(db->mu);
+        DeviceGuard guard(db->device);
+        SWB_CUDA(cudaStreamSynchronize(db->stream));
+        db->async_pending = false;
+        fill_stats(db, query_len, &sstats[r]);
+    }
     if (stats) {
         std::memset(stats, 0, sizeof(*stats));
         for (size_t r = 0; r < G; ++r) {

@@ -108,9 +108,22 @@ swb_status launch_wavefront(swb_db* db, const WaveParams& wp, uint32_t grid, uin
 }
 
 // Scores every local sequence; results land in d_slot_scores.  Asynchronous on db->stream.
+// A search enqueued by swb_search_keys_device may still be reading its inputs from the pinned staging buffer.
+swb_status settle_async(swb_db* db) {
+    if (db->async_pending) {
+        SWB_CUDA(cudaStreamSynchronize(db->stream));
+        db->async_pending = false;
+    }
+    return SWB_OK;
+}
+
 swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_t* matrix, int32_t open,
                       int32_t ext) {
     cudaStream_t s = db->stream;
+    {
+        const swb_status settled = settle_async(db);
+        if (settled != SWB_OK) return settled;
+    }
     const QueryPlan pl = make_plan(db, m, matrix, open, ext);
     db->launches_total += db->launches;
     db->launches = 0;

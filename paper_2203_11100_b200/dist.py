@@ -4,6 +4,11 @@ all-gather of k packed 64-bit keys per rank (NCCL over NVLink on GPUs; gloo in t
 The data path has no other collective: every (query, subject) score is independent
 (align.hpp:80-82) and the (score desc, index asc) order is a strict total order
 (scheduler.hpp:111-114), so top-k of the union == top-k of the per-shard top-k's.
+
+A sharded search touches the host once: the library enqueues the shard's search on torch's current stream and
+leaves its k keys in a preallocated CUDA tensor (swb_search_keys_device), the all-gather runs on that tensor, the
+library selects the global top-k from the gathered tensor on the same stream (swb_db_merge_keys) and copies k hits
+down -- the one device-to-host copy and the one synchronisation of the search.
 """
 from __future__ import annotations
 
@@ -13,7 +18,8 @@ import torch.distributed as dist
 
 
 def exchange_keys(local_keys: np.ndarray, device: torch.device | None = None, group=None) -> np.ndarray:
-    """All-gather this rank's top_k packed keys (zero padded to a common length).
+    """All-gather this rank's top_k packed keys (zero padded to a common length), host in, host out: the flavour for
+    keys that are already on the host (the batched sweep's n_queries x k block; the CPU tests).
 
     Returns the concatenation over ranks, shape (world * k,).  uint64 keys travel as int64 bit
     patterns (NCCL/gloo have no uint64 tensor type in torch)."""
@@ -40,27 +46,44 @@ def merge_many(gathered: np.ndarray, world: int, n_queries: int, top_k: int):
 
 
 class ShardedSearch:
-    """This rank's shard of the database plus the cross-rank merge."""
+    """This rank's shard of the database plus the cross-rank merge.
 
-    def __init__(self, codes, offsets, length_threshold: int = 3000, device_index: int = 0, group=None):
+    device_path: route every search through the device-tensor path (keys stay on the GPU between the shard's select,
+    the all-gather and the global select) even when world == 1, where search() would otherwise call swb_search
+    directly -- what the one-GPU test of that path uses."""
+
+    def __init__(self, codes, offsets, length_threshold: int = 3000, device_index: int = 0, group=None, device_path: bool = False):
         from .search import Database
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.device_index = device_index
+        self.device_path = device_path
         self.db = Database(codes, offsets, length_threshold=length_threshold, device=device_index,
                            shard_rank=self.rank, shard_count=self.world)
+        self._send = self._recv = None   # CUDA int64 tensors of k and world x k keys, reused across searches
+
+    def _buffers(self, top_k: int):
+        if self._send is None or self._send.numel() != top_k:
+            device = torch.device("cuda", self.device_index)
+            self._send = torch.zeros(top_k, dtype=torch.int64, device=device)
+            self._recv = torch.zeros(self.world * top_k, dtype=torch.int64, device=device)
+        return self._send, self._recv
 
     def search(self, query, matrix, gaps, top_k: int = 10):
         """-> (db_index, score, local stats).  Every rank returns the same global list."""
-        from .search import decode_keys, merge_keys
-        keys, _, stats = self.db.search_keys(query, matrix, gaps, top_k)
-        if self.world == 1:
-            idx, sc = decode_keys(keys)
-            return idx, sc, stats
-        gathered = exchange_keys(keys, torch.device("cuda", self.device_index), self.group)
-        idx, sc = merge_keys(gathered, top_k, device=self.device_index)
-        return idx, sc, stats
+        if self.world == 1 and not self.device_path:
+            return self.db.search(query, matrix, gaps, top_k)
+        # the library's stream must be the one the collective orders itself against: torch's current stream
+        stream = torch.cuda.current_stream(torch.device("cuda", self.device_index))
+        self.db.set_stream(stream.cuda_stream)
+        send, recv = self._buffers(top_k)
+        self.db.search_keys_device(query, matrix, gaps, top_k, send.data_ptr())
+        if self.world > 1:
+            dist.all_gather_into_tensor(recv, send, group=self.group)
+        else:
+            recv = send
+        return self.db.merge_keys_device(recv.data_ptr(), recv.numel(), top_k, len(query))
 
     def search_many(self, queries, matrix, gaps, top_k: int = 10):
         """A batch of queries (swb_search_many on this rank's shard: shared scans where they apply), then ONE

@@ -143,8 +143,12 @@ class Database:
         """Which kernel scans the database (swb_scan_policy); results are identical."""
         _raise(self._lib, self._lib.swb_db_set_scan_policy(self._h, policy))
 
-    def set_stream(self, cuda_stream: int):
-        _raise(self._lib, self._lib.swb_db_set_stream(self._h, C.c_void_p(cuda_stream)))
+    def set_stream(self, cuda_stream: int | None):
+        """All work of this handle goes to `cuda_stream` (torch.cuda.current_stream().cuda_stream); None restores the
+        handle's own stream.  torch's default stream has the handle 0, which the C-ABI reads as "own stream": it is
+        passed as cudaStreamLegacy (0x1), the explicit name of the same stream."""
+        handle = 0 if cuda_stream is None else (cuda_stream or 1)
+        _raise(self._lib, self._lib.swb_db_set_stream(self._h, C.c_void_p(handle)))
 
     def search(self, query, matrix, gaps: GapModel, top_k: int = 10):
         """-> (db_index[uint32], score[int32], stats dict), at most top_k hits, final order."""
@@ -215,6 +219,26 @@ class Database:
                                        top_k, _ptr(keys, _u64p), C.byref(dptr), C.byref(st))
         _raise(self._lib, rc)
         return keys[:top_k], dptr.value, st.as_dict()
+
+    def search_keys_device(self, query, matrix, gaps: GapModel, top_k: int, device_keys_ptr: int):
+        """Enqueue the search on the handle's stream (set_stream) and leave its top_k packed keys, zero padded, at the
+        DEVICE address `device_keys_ptr` (top_k x 8 bytes).  Does not synchronise (swb_search_keys_device)."""
+        q, mat = _u8(query), _mat(matrix)
+        rc = self._lib.swb_search_keys_device(self._h, _ptr(q, _u8p), len(q), _ptr(mat, _i32p), gaps.open, gaps.extend,
+                                              top_k, C.c_void_p(device_keys_ptr))
+        _raise(self._lib, rc)
+
+    def merge_keys_device(self, device_keys_ptr: int, n: int, top_k: int, query_len: int):
+        """Top top_k of `n` packed DEVICE keys on the handle's stream (swb_db_merge_keys): the one device-to-host copy
+        and the one synchronisation of a sharded search.  -> (db_index, score, stats of the enqueued search)."""
+        hits = (_cabi.SwbHit * max(1, top_k))()
+        cnt = C.c_uint32(0)
+        st = _cabi.SwbStats()
+        rc = self._lib.swb_db_merge_keys(self._h, C.c_void_p(device_keys_ptr), n, top_k, hits, C.byref(cnt), query_len, C.byref(st))
+        _raise(self._lib, rc)
+        idx = np.array([hits[i].db_index for i in range(cnt.value)], dtype=np.uint32)
+        sc = np.array([hits[i].score for i in range(cnt.value)], dtype=np.int32)
+        return idx, sc, st.as_dict()
 
     def align_hits(self, query, matrix, gaps: GapModel, index, score, subject_lengths, memory_cap: int = 256 << 20):
         """Tracebacks of search hits straight from the resident database (swb_db_align_hits): a list of dicts

@@ -15,7 +15,7 @@ b62 = synth.blosum62()
 ok = True
 for seed, gaps in ((41, (10, 2)), (42, (11, 1)), (43, (4, 4)), (44, (0, 0))):
     rng = np.random.default_rng(seed)
-    seqs = [synth.random_residues(rng, int(rng.integers(0, 300))) for _ in range(int(rng.integers(100, 400)))]
+    seqs = [synth.random_residues(rng, int(rng.integers(0, 300))) for _ in range(int(rng.integers(200, 400)))]
     # tall groups: row counts around the chunk (8) and publish (32 rows) granules, one far taller than the rest
     for i, n in enumerate([2049, 2056, 2081, 4100, 9000, 2600] + [int(x) for x in rng.integers(2049, 3300, 180)]):
         seqs[i] = synth.random_residues(rng, n)
