@@ -340,11 +340,14 @@ typedef struct swb_scan_plan_info {
     uint32_t wavefront_groups;  /* groups the wavefront kernel scans (the tallest ones, or all)            */
     uint32_t wavefront_sms;     /* SMs the wavefront kernel runs on                                        */
     uint32_t wavefront_units;   /* its work units                                                          */
-    uint32_t split_groups, narrow_groups, rowblock_groups;   /* wavefront groups cut by tile / 8-column tile / rows */
+    uint32_t split_groups, narrow_groups, rowblock_groups;   /* wavefront groups cut by tile / narrow tile / rows  */
     uint32_t ring_chunks;       /* pipeline: chunks per shared-memory ring next to this query's profile    */
     int32_t chain_bound;        /* the longest group's chain of rows bounds the search                     */
-    int32_t reserved;
+    uint32_t narrow_tile;       /* columns of a narrow tile: 8, or 4 for the most chain-bound searches     */
     uint64_t pipeline_rows, wavefront_rows;   /* padded rows on either side                                */
+    uint32_t wavefront_threads; /* CTA size of the wavefront kernel (128: one warp per scheduler)          */
+    uint32_t reserved;
+    uint64_t narrow_link_bytes; /* link buffers of the narrow groups (8 B per row, lane and tile boundary) */
 } swb_scan_plan_info;
 swb_status swb_scan_plan(const uint32_t* lens, uint32_t n, uint64_t length_threshold, uint32_t shard_rank,
                          uint32_t shard_count, uint32_t query_len, uint32_t sm_count, int32_t policy,

@@ -59,7 +59,8 @@ class SwbScanPlanInfo(C.Structure):
         ("n_groups", C.c_uint32), ("n_tiles", C.c_uint32), ("pipeline_groups", C.c_uint32), ("wavefront_groups", C.c_uint32),
         ("wavefront_sms", C.c_uint32), ("wavefront_units", C.c_uint32), ("split_groups", C.c_uint32),
         ("narrow_groups", C.c_uint32), ("rowblock_groups", C.c_uint32), ("ring_chunks", C.c_uint32),
-        ("chain_bound", C.c_int32), ("reserved", C.c_int32), ("pipeline_rows", C.c_uint64), ("wavefront_rows", C.c_uint64),
+        ("chain_bound", C.c_int32), ("narrow_tile", C.c_uint32), ("pipeline_rows", C.c_uint64), ("wavefront_rows", C.c_uint64),
+        ("wavefront_threads", C.c_uint32), ("reserved", C.c_uint32), ("narrow_link_bytes", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -136,6 +136,8 @@ struct swb_db {
     size_t vstate_cap = 0;
     uint32_t* d_progress = nullptr;
     size_t progress_cap = 0;
+    uint8_t* d_nlinks = nullptr;   // narrow groups' link buffers (kernels.cuh: 256 B per row and tile boundary)
+    size_t nlinks_cap = 0;
     uint64_t* d_keys = nullptr;
     uint64_t* d_sel[2] = {nullptr, nullptr};
     size_t sel_cap = 0;
@@ -294,7 +296,7 @@ void swb_db_destroy(swb_db* db) {
         if (db->side_stream) cudaStreamSynchronize(db->side_stream);
         void* ptrs[] = {db->d_codes,      db->d_groups,   db->d_slot_index, db->d_slot_len,    db->d_border0,
                         db->d_border1,    db->d_iborder0, db->d_iborder1, db->d_multi_scores, db->d_multi_codes, db->d_duo_tiles, db->d_prof2, db->d_duo_progress,   db->d_slot_scores, db->d_flag_list,
-                        db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_vstate_off, db->d_vstate, db->d_progress, db->d_keys,        db->d_sel[0],
+                        db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_vstate_off, db->d_vstate, db->d_progress, db->d_nlinks, db->d_keys,        db->d_sel[0],
                         db->d_sel[1],     db->d_sort,     db->d_all_scores, db->d_query,       db->d_matrix,
                         db->d_prof8,      db->d_prof8i,   db->d_prof32i};
         for (void* p : ptrs)
@@ -765,7 +767,7 @@ swb_status swb_scan_plan(const uint32_t* lens, uint32_t n, uint64_t length_thres
     shape.n_groups = n_groups;
     shape.padded_rows = padded_rows;
     shape.n_tiles = (query_len + kInterTile - 1) / kInterTile;
-    shape.n_tiles_narrow = (query_len + kNarrowTile - 1) / kNarrowTile;
+    shape.query_len = query_len;
     shape.sm_count = sm_count;
     shape.warps_per_cta = kInterThreads / 32;
     shape.policy = policy;
@@ -784,6 +786,9 @@ swb_status swb_scan_plan(const uint32_t* lens, uint32_t n, uint64_t length_thres
     out->rowblock_groups = sp.n_rowblock;
     out->ring_chunks = shape.pipe_rings;
     out->chain_bound = sp.chain_bound ? 1 : 0;
+    out->narrow_tile = sp.narrow_tile;
+    out->wavefront_threads = sp.wave_threads;
+    out->narrow_link_bytes = sp.link_rows * 256;
     out->wavefront_rows = sp.wave_rows;
     out->pipeline_rows = padded_rows - sp.wave_rows;
     return SWB_OK;

@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "pack.hpp"
 #include "scan_plan.hpp"
 
@@ -37,6 +39,7 @@ constexpr int kProfRows = 25;        // 24 symbols + the pad row
 #endif
 constexpr int kInterTile = SWB_INTER_TILE;        // query columns held in registers per pass (multiple of 8)
 constexpr int kInterThreads = SWB_INTER_THREADS;  // persistent CTA: 16 warps, four per SMSP
+constexpr int kNarrowThreads = 128;               // wavefront CTAs of narrow units next to the pipeline: one warp per SMSP
 constexpr int kIntraDelta = 64;      // step offset between neighbouring warps of an intra-task CTA
 constexpr int kIntraRing = 128;      // rows of border ring buffer between neighbouring warps
 constexpr int kIntraMaxWarps = 8;
@@ -129,7 +132,7 @@ struct WaveParams {
     const uint32_t* vstate_off;   // [n_groups] first vstate slot of a kGroupRowBlock group (slots of one tile each)
     uint4* vstate;                // register-state hand-over between row blocks
     uint32_t n_units;
-    uint32_t n_tiles_narrow;      // ceil(m / 8): tiles of a kGroupNarrow group
+    uint32_t n_tiles_narrow;      // ceil(m / narrow_tile): tiles of a kGroupNarrow group
     const int8_t* prof8;
     uint32_t pstride;
     uint32_t n_tiles;             // ceil(m / T)
@@ -140,6 +143,12 @@ struct WaveParams {
     uint32_t* ticket;
     uint32_t neg_open2;           // (-open, -open) packed
     uint32_t neg_ext2;            // (-extend, -extend) packed
+    // narrow units only (behind the fields every variant reads: ptxas's allocation of the plain sweep proved sensitive
+    // even to the parameter layout)
+    uint32_t narrow_tile;         // 8 or 4 columns
+    uint32_t narrow_staged;       // 1: narrow units hand over through link buffers of their own (short queries);
+                                  // 0: through the border arrays like every other tile (deep wavefronts: many narrow tiles)
+    uint8_t* nlinks;              // link buffers of the narrow groups (vstate_off[g]: first row slot, 256 B each, of group g's links)
 };
 
 // A group is either one unit (all tiles, one warp) or n_tiles units (one tile each, a wavefront of
@@ -330,81 +339,167 @@ __device__ __forceinline__ uint32_t sweep_unit_s16(const WaveParams& p, const in
     return best;
 }
 
-// Narrow units (kGroupNarrow): one 8-column tile over all rows of a very tall group, for searches whose duration is
-// bounded by that group's chain of rows (short query, 35,213-residue sequence).  A block of 8 rows x 8 columns is swept
-// in ANTI-DIAGONAL order: cell (r, c) needs (r-1, c), (r, c-1) and (r-1, c-1), all on the two previous anti-diagonals, so
-// the eight cells of an anti-diagonal are independent and a block's dependent chain is 15 cell steps instead of 64
-// (the reference's intra-task schedule, align.hpp:194-226, inside one thread).  Everything is unrolled: Hm and F live
-// per column, E and the left neighbour's Hm per row, and d[r] holds the diagonal term of row r's next cell, formed from
-// Hm[c] = H(r-1, c) before cell (r, c) overwrites that register.  With the chain gone a warp is bound by its issue
-// slots (~60 clk per row instead of ~270), so such units want a scheduler of their own: wavefront_s16_kernel hands its
-// first round of units out statically, one per SM at a time.
-__device__ __forceinline__ uint32_t sweep_unit_narrow_s16(const WaveParams& p, const int8_t* prof, const GroupDesc& gd, uint32_t tile,
-                                                          uint32_t n_tiles, const uint32_t* dep, uint32_t* pub, uint32_t lane) {
-    constexpr int T = kNarrowTile, R = static_cast<int>(kRowsPerChunk), P = 4;
-    static_assert(T == 8 && R == 8, "the block sweep is written for 8 x 8");
-    const uint32_t NO = p.neg_open2, NE = p.neg_ext2;
-    const uint32_t n_chunks = gd.n_chunks, rows = n_chunks * kRowsPerChunk;
+// Narrow units (kGroupNarrow): one tile of T = 8 or 4 columns over all rows of a very tall group, for searches whose
+// duration is bounded by that group's chain of rows (short query, 35,213-residue sequence).  A block of 8 rows x T
+// columns is swept in ANTI-DIAGONAL order: cell (r, c) needs (r-1, c), (r, c-1) and (r-1, c-1), all on the two previous
+// anti-diagonals, so the cells of an anti-diagonal are independent and a block's dependent chain is 8 + T - 1 cell steps
+// instead of 8 T (the reference's intra-task schedule, align.hpp:194-226, inside one thread).  Everything is unrolled:
+// Hm and F live per column, E and the left neighbour's Hm per row, and d[r] holds the diagonal term of row r's next cell,
+// formed from Hm[c] = H(r-1, c) before cell (r, c) overwrites that register.  A warp alone on its scheduler then runs at
+// its issue rate (tools/lat_probe.cu: dependent DPX instructions issue 4 clk apart, independent ones 2 clk apart; 760 clk
+// per 8 x 8 block and 390 per 8 x 4 block, i.e. 95 / 49 clk per row against 365 for the 32-column sweep), so such units
+// want a scheduler of their own: wavefront_s16_kernel hands its first round of units out statically, one per SM at a
+// time, and the host gives it CTAs of 4 warps.
+//
+// Hand-off between neighbouring tiles (one warp each, usually on different SMs): the DATA IS THE FLAG.  Every (Hm, E)
+// border entry is one 8-byte word per lane and row in a link buffer of its own (one region per group and tile boundary,
+// written once and read once per search, laid out [block][row pair][lane][2 rows] so that a warp's access is 512
+// contiguous bytes), which holds kNarrowEmpty wherever nothing has been produced yet.  The producer stores a block's rows
+// with four st.relaxed.gpu.v2.u64; the consumer reads them with ld.relaxed.gpu.v2.u64 a block ahead of their use, asks
+// again while a word's Hm half still reads as empty, and stores kNarrowEmpty back once it has the value, which leaves the
+// buffer ready for the next search (the next writer of that word is a later kernel on the stream).  Every 64-bit element
+// of these accesses is a strong, naturally aligned operation at gpu scope on one location: single-copy atomic and
+// race-free under the PTX memory model, and nothing else is published through it, so the path needs no fence, no
+// progress counter and no L1 invalidate.  That is what makes it fast, not only clean: measured on the B200
+// (tools/lat_probe.cu, profiles/r02_summary.md) a membar.gpu behind st.release.gpu or a fence.proxy.async costs the
+// issuing warp 750-850 clk -- two blocks of a 4-column tile -- and slows the other warps of its SM as well (a variant
+// with TMA staging and one release / acquire per 8 blocks ran 960 clk per block alone and 1,600 with four warps per SM).
+// kNarrowEmpty cannot be a value: its halves are -32,640, below anything a trusted lane holds (>= -open - ext >= -254);
+// a lane that has wrapped (its score is already above the trust limit and will be re-run in int32) could produce the
+// pattern by accident, so the producer nudges exactly that Hm word by one -- garbage stays garbage.
+constexpr unsigned long long kNarrowEmpty = 0x8080808080808080ull;   // what cudaMemset(0x80) leaves
+constexpr uint32_t kNarrowEmptyWord = 0x80808080u;                    // the test looks at the Hm word (the low one)
+constexpr uint32_t kNarrowLagBlocks = 4;                              // a tile (re)starts this many blocks behind its producer
+
+static_assert(kNarrowChunkBytes == kRowsPerChunk * 32 * 8, "scan_plan.hpp and the packed layout disagree on the block of border rows");
+
+// Two rows of a lane (16 bytes) at a time: each 64-bit element is a strong relaxed access of its own.
+__device__ __forceinline__ void ld_link2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+__device__ __forceinline__ void st_link2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b));
+}
+__device__ __forceinline__ bool link_empty(unsigned long long v) { return static_cast<uint32_t>(v) == kNarrowEmptyWord; }
+
+// Per-warp state of the narrow units.
+struct NarrowWarp {
+    const uint32_t* consts;   // (neg_open2, neg_ext2) in shared memory
+};
+
+// kFirst / kLast (tile 0 / the last tile) are compile-time, so that a tile without an inbound or outbound link carries
+// none of its code and the block loop's body is straight-line code apart from the rare "a row has not arrived yet".
+template <int T, bool kFirst, bool kLast>
+__device__ __forceinline__ uint32_t sweep_narrow_tile_s16(const WaveParams& p, const int8_t* prof, const GroupDesc& gd, uint32_t tile,
+                                                          uint8_t* link_base, uint32_t lane, NarrowWarp& nw) {
+    constexpr int R = static_cast<int>(kRowsPerChunk);
+    static_assert((T == 8 || T == 4) && R == 8, "the block sweep is written for 8 rows x 8 or 4 columns");
+    using ProfWord = typename std::conditional<T == 8, uint2, uint32_t>::type;   // a row's T int8 entries
+    // The two packed constants are read back from shared memory (written by the kernel from its parameters): taken from the
+    // parameters directly ptxas keeps them as 16-bit halves in uniform registers and, in a loop under this register
+    // pressure, rebuilds the vector operand with a PRMT in front of every VIADDMNMX and VIADD that uses them (+47
+    // instructions per 8 x 4 block; a shuffle does not hide the uniformity, a load does).
+    const uint32_t NO = *reinterpret_cast<const volatile uint32_t*>(nw.consts), NE = *reinterpret_cast<const volatile uint32_t*>(nw.consts + 1);
+    const uint32_t n_chunks = gd.n_chunks;
     if (n_chunks == 0) return 0;
+    constexpr size_t kBlockWords = kNarrowChunkBytes / 8;
+    const size_t link_words = static_cast<size_t>(n_chunks) * kBlockWords;   // one link: every block of the group
     const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
-    const size_t brow0 = static_cast<size_t>(gd.chunk_base) * kRowsPerChunk * 32 + lane;
     const int8_t* ptile = prof + tile * T;
-    const bool first = tile == 0, last = tile + 1 == n_tiles;
-    const uint2* bin = ((tile & 1) ? p.border0 : p.border1) + brow0;
-    uint2* bout = ((tile & 1) ? p.border1 : p.border0) + brow0;
+    // link t: tile t -> tile t + 1; both pointers advance a block per iteration; a lane's rows 2i, 2i + 1 at [i][lane]
+    unsigned long long* const links = reinterpret_cast<unsigned long long*>(link_base);
+    const unsigned long long* lin = links + (static_cast<size_t>(tile) - (kFirst ? 0 : 1)) * link_words + lane * 2;
+    unsigned long long* lout = links + static_cast<size_t>(tile) * link_words + lane * 2;
+    const unsigned long long* const lin_end = lin + (static_cast<size_t>(n_chunks) - 1) * kBlockWords;   // the last block
+    auto next_block = [&](const unsigned long long* at) { return at < lin_end ? at + kBlockWords : lin_end; };
+    auto request = [&](unsigned long long(&q)[R], const unsigned long long* at) {
+#pragma unroll
+        for (int i = 0; i < R / 2; ++i) ld_link2(at + i * 64, q[2 * i], q[2 * i + 1]);
+    };
+    // wait until the producer is kNarrowLagBlocks ahead of block `at` (or done), so that from there on a request made a
+    // block ahead finds its rows: at the start, and again whenever the tile has caught up with its producer
+    auto fall_back = [&](const unsigned long long* at) {
+        const unsigned long long* probe = at;
+#pragma unroll
+        for (uint32_t i = 0; i < kNarrowLagBlocks; ++i) probe = next_block(probe);
+        unsigned long long a, b;
+        for (;;) {
+            ld_link2(probe + 3 * 64, a, b);
+            if (!link_empty(b)) break;   // the block's last row
+            __nanosleep(200);
+        }
+    };
 
     uint32_t Hm[T], F[T];
 #pragma unroll
     for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
     uint32_t diag_in = NO, best = 0;
-    uint32_t known = 0;   // producer progress (rows), as last acquired
-    uint4 cw = __ldg(gcodes);
-    uint2 q[R];           // inbound border rows of the chunk about to be computed, fetched one chunk ahead
+    // Inbound rows are requested at the start of the block BEFORE the one that uses them, into registers of their own, and
+    // take the place of the current ones at its end: a block (400+ clk) covers the L2 round trip (~310 clk), and the copy
+    // at the end never waits.  (Requests further ahead were tried: the values are then live across the loop's back edge in
+    // registers ptxas does not load into directly, and its copies wait for the load.)
+    unsigned long long q[R], qn[R];
+    const unsigned long long edge = (static_cast<unsigned long long>(NO) << 32) | NO;
 #pragma unroll
-    for (int i = 0; i < R; ++i) q[i] = make_uint2(NO, NO);
-    if (!first) {
-        if (dep != nullptr) {
-            if (lane == 0) known = wait_progress(dep, min(rows, 2u * kRowsPerChunk));
-            known = __shfl_sync(0xffffffffu, known, 0);
-        }
-#pragma unroll
-        for (int i = 0; i < R; ++i) q[i] = __ldcg(bin + static_cast<size_t>(i) * 32);
+    for (int i = 0; i < R; ++i) q[i] = qn[i] = edge;
+    if (!kFirst) {
+        fall_back(lin);
+        request(q, lin);
     }
-
-    for (uint32_t chunk = 0; chunk < n_chunks; ++chunk) {
-        const uint4 cur = cw;
-        if (chunk + 1 < n_chunks) cw = __ldg(gcodes + static_cast<size_t>(chunk + 1) * 32);
-        const size_t row0 = static_cast<size_t>(chunk) * kRowsPerChunk;
-        uint32_t E[R], hl[R], d[R];
-        uint2 pa[R], pb[R];
+    auto profile_rows = [&](const uint4& w, ProfWord* pa, ProfWord* pb) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const uint32_t a1 = ((r < 4 ? cur.x : cur.y) >> (8 * (r & 3))) & 0xffu;
-            const uint32_t a2 = ((r < 4 ? cur.z : cur.w) >> (8 * (r & 3))) & 0xffu;
-            pa[r] = *reinterpret_cast<const uint2*>(ptile + a1 * p.pstride);
-            pb[r] = *reinterpret_cast<const uint2*>(ptile + a2 * p.pstride);
+            // residue r of either sequence: one PRMT each (byte r & 3 of the word, zero-extended)
+            const uint32_t a1 = prmt(r < 4 ? w.x : w.y, 0, 0x4440u | (r & 3));
+            const uint32_t a2 = prmt(r < 4 ? w.z : w.w, 0, 0x4440u | (r & 3));
+            pa[r] = *reinterpret_cast<const ProfWord*>(ptile + a1 * p.pstride);
+            pb[r] = *reinterpret_cast<const ProfWord*>(ptile + a2 * p.pstride);
         }
+    };
+    auto codes_of = [&](uint32_t chunk) { return __ldg(gcodes + static_cast<size_t>(min(chunk, n_chunks - 1)) * 32); };
+    ProfWord na[R], nb[R];                       // the profile rows of the block about to be computed
+    profile_rows(codes_of(0), na, nb);
+    // the residues of the next odd / even block: loaded three blocks ahead into registers of their own (the loop is unrolled
+    // by two for that: rotating one set through another would wait for the load at the rotation)
+    uint4 cb = codes_of(1), ca = codes_of(2);
+
+    auto step = [&](uint4& cnext, uint32_t chunk) {
+        ProfWord pa[R], pb[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) pa[r] = na[r], pb[r] = nb[r];
         // substitution word of (row r, column c): the two sequences' int8 entries, sign-extended into the halves
         auto sub = [&](int r, int c) {
             const uint32_t sel = (c & 3) == 0 ? 0xC480u : (c & 3) == 1 ? 0xD591u : (c & 3) == 2 ? 0xE6A2u : 0xF7B3u;
-            return prmt(c < 4 ? pa[r].x : pa[r].y, c < 4 ? pb[r].x : pb[r].y, sel);
+            if constexpr (T == 8) return prmt(c < 4 ? pa[r].x : pa[r].y, c < 4 ? pb[r].x : pb[r].y, sel);
+            else return prmt(pa[r], pb[r], sel);
         };
+        if (!kFirst) {
+            request(qn, next_block(lin));   // the next block's rows (past the end: the last block's again, unused)
+            // this block's rows, requested a block ago.  A missing one means the tile has caught up with its producer:
+            // it falls back by kNarrowLagBlocks instead of trailing it row by row, then asks for both blocks again
+            bool missing = false;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            hl[r] = q[r].x, E[r] = q[r].y;
-            d[r] = __vadd2(r == 0 ? diag_in : q[r - 1].x, sub(r, 0));   // diagonal of column 0: the row above's inbound Hm
-        }
-        diag_in = q[R - 1].x;
-        // the next chunk's inbound rows travel while this one is computed
-        if (!first && chunk + 1 < n_chunks) {
-            const uint32_t need = min(rows, static_cast<uint32_t>(row0) + 3u * kRowsPerChunk);
-            if (dep != nullptr && known < need) {
-                if (lane == 0) known = wait_progress(dep, need);
-                known = __shfl_sync(0xffffffffu, known, 0);
+            for (int i = 0; i < R; ++i) missing |= link_empty(q[i]);
+            if (missing) {
+                fall_back(lin);
+                request(q, lin);
+                request(qn, next_block(lin));
             }
 #pragma unroll
-            for (int i = 0; i < R; ++i) q[i] = __ldcg(bin + (row0 + kRowsPerChunk + i) * 32);
+            for (int i = 0; i < R / 2; ++i) st_link2(const_cast<unsigned long long*>(lin) + i * 64, kNarrowEmpty, kNarrowEmpty);
         }
+        uint32_t E[R], hl[R], d[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            hl[r] = static_cast<uint32_t>(q[r]), E[r] = static_cast<uint32_t>(q[r] >> 32);
+            d[r] = __vadd2(r == 0 ? diag_in : static_cast<uint32_t>(q[r - 1]), sub(r, 0));   // diagonal of column 0: the row above's inbound Hm
+        }
+        diag_in = static_cast<uint32_t>(q[R - 1]);
+        // the next block's profile rows and the residues three blocks on travel while this one is computed (past the end:
+        // the last block's again, unused); tile 0 reads the residues from HBM for everyone behind it, well ahead
+        profile_rows(cnext, na, nb);
+        cnext = codes_of(chunk + 3);
+        if (kFirst) asm volatile("prefetch.global.L2 [%0];" ::"l"(gcodes + static_cast<size_t>(min(chunk + 32, n_chunks - 1)) * 32));
         uint32_t pend = 0;
         bool have = false;
 #pragma unroll
@@ -424,16 +519,38 @@ __device__ __forceinline__ uint32_t sweep_unit_narrow_s16(const WaveParams& p, c
                 else pend = dcur, have = true;
             }
         }
-        if (!last) {
+        if (!kLast) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) bout[(row0 + r) * 32] = make_uint2(hl[r], E[r]);
+            for (int i = 0; i < R / 2; ++i) {
+                // only a lane that has already wrapped can hold the "empty" pattern: nudge it, garbage stays garbage
+                const uint32_t h0 = hl[2 * i] == kNarrowEmptyWord ? kNarrowEmptyWord + 1 : hl[2 * i];
+                const uint32_t h1 = hl[2 * i + 1] == kNarrowEmptyWord ? kNarrowEmptyWord + 1 : hl[2 * i + 1];
+                st_link2(lout + i * 64, (static_cast<unsigned long long>(E[2 * i]) << 32) | h0,
+                         (static_cast<unsigned long long>(E[2 * i + 1]) << 32) | h1);
+            }
+            lout += kBlockWords;
         }
-        if (pub != nullptr && ((chunk + 1) % P == 0 || chunk + 1 == n_chunks)) {
-            __syncwarp();
-            if (lane == 0) st_release(pub, static_cast<uint32_t>(row0) + kRowsPerChunk);
+        if (!kFirst) {
+            lin = next_block(lin);
+#pragma unroll
+            for (int i = 0; i < R; ++i) q[i] = qn[i];
         }
+    };
+    for (uint32_t chunk = 0; chunk < n_chunks; chunk += 2) {
+        step(cb, chunk);
+        if (chunk + 1 < n_chunks) step(ca, chunk + 1);
     }
     return best;
+}
+
+template <int T>
+__device__ __forceinline__ uint32_t sweep_unit_narrow_s16(const WaveParams& p, const int8_t* prof, const GroupDesc& gd, uint32_t tile,
+                                                          uint32_t n_tiles, uint8_t* link_base, uint32_t lane, NarrowWarp& nw) {
+    const bool first = tile == 0, last = tile + 1 == n_tiles;
+    if (first) return last ? sweep_narrow_tile_s16<T, true, true>(p, prof, gd, tile, link_base, lane, nw)
+                           : sweep_narrow_tile_s16<T, true, false>(p, prof, gd, tile, link_base, lane, nw);
+    return last ? sweep_narrow_tile_s16<T, false, true>(p, prof, gd, tile, link_base, lane, nw)
+                : sweep_narrow_tile_s16<T, false, false>(p, prof, gd, tile, link_base, lane, nw);
 }
 
 // Group modes (GroupMode, kNarrowTile): scan_plan.hpp, where the host decides them per search.
@@ -443,6 +560,14 @@ __device__ __forceinline__ uint32_t sweep_unit_narrow_s16(const WaveParams& p, c
 template <bool kSmemProfile, int T, int kThreads, bool kNarrow, bool kRowBlocks>
 __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p) {
     extern __shared__ __align__(16) uint8_t smem_prof[];
+    struct NoNarrow {};
+    typename std::conditional<kNarrow, NarrowWarp, NoNarrow>::type nw{};
+    if constexpr (kNarrow) {
+        __shared__ uint32_t narrow_consts[2];   // sweep_narrow_tile_s16 reads its packed constants from here
+        if (threadIdx.x == 0) narrow_consts[0] = p.neg_open2, narrow_consts[1] = p.neg_ext2;
+        nw.consts = narrow_consts;
+        __syncthreads();
+    }
 
     const int8_t* prof;
     if (kSmemProfile) {
@@ -498,9 +623,21 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
             const uint32_t t1 = mode == kGroupSingle ? n_tiles : t0 + 1;
             const uint32_t* dep = t0 > 0 ? p.progress + (u - 1) : nullptr;
             uint32_t* pub = t1 < n_tiles ? p.progress + u : nullptr;
-            if (kNarrow && mode == kGroupNarrow)
-                best = sweep_unit_narrow_s16(p, prof, gd, t0, n_tiles, dep, pub, lane);
-            else
+            bool narrow_done = false;
+            if constexpr (kNarrow) {
+                if (mode == kGroupNarrow) {
+                    if (p.narrow_staged) {
+                        uint8_t* links = p.nlinks + static_cast<size_t>(p.vstate_off[g]) * 256;
+                        best = p.narrow_tile == 4 ? sweep_unit_narrow_s16<4>(p, prof, gd, t0, n_tiles, links, lane, nw)
+                                                  : sweep_unit_narrow_s16<8>(p, prof, gd, t0, n_tiles, links, lane, nw);
+                    } else {
+                        // a deep wavefront of 8-column tiles (long query): rows fetched 8 ahead, progress published every 4 chunks
+                        best = sweep_unit_s16<kNarrowTile, 8, 4, false>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane, 0, gd.n_chunks, nullptr);
+                    }
+                    narrow_done = true;
+                }
+            }
+            if (!narrow_done)
                 best = sweep_unit_s16<T, 2, 1, false>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane, 0, gd.n_chunks, nullptr);
         }
 

@@ -81,27 +81,38 @@ void report_pipe_stats(const char* what, const unsigned long long* d_stats, uint
 }
 #endif
 
+constexpr size_t kWaveStaticSmem = 1024;   // the wavefront kernel's own static shared memory, rounded up generously
+
 // The wavefront kernel.  The narrow-tile and row-block paths are only compiled into the variants that need them, so
 // that the plain 32-column sweep keeps its register allocation; a profile too large for shared memory is read from
 // global memory.
 swb_status launch_wavefront(swb_db* db, const WaveParams& wp, uint32_t grid, uint32_t threads, size_t smem, bool narrow,
                             bool rowblock, cudaStream_t s) {
-    const bool in_smem = smem <= db->smem_optin;
-#define SWB_LAUNCH_S16(NARROW, RB)                                                                                 \
+    constexpr size_t kStaticSmem = kWaveStaticSmem;
+    const bool in_smem = smem + kStaticSmem <= db->smem_optin;
+#define SWB_LAUNCH_S16(THREADS, NARROW, RB)                                                                        \
     {                                                                                                              \
         if (in_smem) {                                                                                             \
-            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB>,       \
+            SWB_CUDA(cudaFuncSetAttribute(wavefront_s16_kernel<true, kInterTile, THREADS, NARROW, RB>,             \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,                             \
-                                          static_cast<int>(db->smem_optin)));                                      \
-            wavefront_s16_kernel<true, kInterTile, kInterThreads, NARROW, RB><<<grid, threads, smem, s>>>(wp);      \
+                                          static_cast<int>(db->smem_optin - kStaticSmem)));                        \
+            wavefront_s16_kernel<true, kInterTile, THREADS, NARROW, RB><<<grid, threads, smem, s>>>(wp);            \
         } else {                                                                                                   \
-            wavefront_s16_kernel<false, kInterTile, kInterThreads, NARROW, RB><<<grid, threads, 0, s>>>(wp);        \
+            wavefront_s16_kernel<false, kInterTile, THREADS, NARROW, RB><<<grid, threads, 0, s>>>(wp);              \
         }                                                                                                          \
     }
-    if (narrow && rowblock) SWB_LAUNCH_S16(true, true)
-    else if (narrow) SWB_LAUNCH_S16(true, false)
-    else if (rowblock) SWB_LAUNCH_S16(false, true)
-    else SWB_LAUNCH_S16(false, false)
+    // CTAs of 4 or 8 warps (narrow units next to the pipeline, one or two warps per scheduler) get builds of their own,
+    // whose register budget is not the 128 of a 16-warp CTA
+    if (narrow && threads <= kNarrowThreads) {
+        if (rowblock) SWB_LAUNCH_S16(kNarrowThreads, true, true)
+        else SWB_LAUNCH_S16(kNarrowThreads, true, false)
+    } else if (narrow && threads <= 2 * kNarrowThreads) {
+        if (rowblock) SWB_LAUNCH_S16(2 * kNarrowThreads, true, true)
+        else SWB_LAUNCH_S16(2 * kNarrowThreads, true, false)
+    } else if (narrow && rowblock) SWB_LAUNCH_S16(kInterThreads, true, true)
+    else if (narrow) SWB_LAUNCH_S16(kInterThreads, true, false)
+    else if (rowblock) SWB_LAUNCH_S16(kInterThreads, false, true)
+    else SWB_LAUNCH_S16(kInterThreads, false, false)
 #undef SWB_LAUNCH_S16
     ++db->launches;
     return SWB_OK;
@@ -161,7 +172,8 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     std::memcpy(stage, matrix, off_query);
     std::memcpy(stage + off_query, query, m);
     const uint32_t n_tiles = (m + pl.tile - 1) / pl.tile;
-    const uint32_t n_tiles_narrow = (m + kNarrowTile - 1) / kNarrowTile;
+    uint32_t n_tiles_narrow = (m + kNarrowTile - 1) / kNarrowTile, narrow_tile = kNarrowTile;
+    bool narrow_staged = false;
     uint32_t n_units = 0;
     uint32_t pipe_first = n_groups;   // groups [pipe_first, n_groups) go through the on-chip pipeline
     uint32_t wave_sms = static_cast<uint32_t>(db->sm_count);   // SMs the wavefront kernel gets
@@ -179,7 +191,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         shape.n_groups = n_groups;
         shape.padded_rows = db->meta.padded_rows;
         shape.n_tiles = n_tiles;
-        shape.n_tiles_narrow = n_tiles_narrow;
+        shape.query_len = m;
         shape.sm_count = static_cast<uint32_t>(db->sm_count);
         shape.warps_per_cta = pl.threads / 32;
         shape.s16 = pl.main == kMainS16;
@@ -192,6 +204,15 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         n_units = sp.n_units;
         any_narrow = sp.any_narrow;
         any_rowblock = sp.any_rowblock;
+        n_tiles_narrow = sp.n_tiles_narrow;
+        narrow_tile = sp.narrow_tile;
+        narrow_staged = sp.narrow_staged;
+        if (any_narrow && narrow_staged && sp.link_rows * 256 > db->nlinks_cap) {
+            // link buffers of the narrow groups (256 B per row and tile boundary): every word holds kNarrowEmpty between
+            // searches -- the consumers give them back
+            if ((st = ensure_dev(&db->d_nlinks, &db->nlinks_cap, static_cast<size_t>(sp.link_rows) * 256, &db->device_bytes)) != SWB_OK) return st;
+            SWB_CUDA(cudaMemsetAsync(db->d_nlinks, 0x80, db->nlinks_cap, s));
+        }
         SWB_CUDA(cudaMemcpyAsync(db->d_unit_start, us, (static_cast<size_t>(n_groups) + 1) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, s));
         SWB_CUDA(cudaMemcpyAsync(db->d_group_mode, modes, std::max<size_t>(n_groups, 1), cudaMemcpyHostToDevice, s));
@@ -287,6 +308,9 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.vstate = db->d_vstate;
         wp.n_units = n_units;
         wp.n_tiles_narrow = n_tiles_narrow;
+        wp.narrow_tile = narrow_tile;
+        wp.nlinks = db->d_nlinks;
+        wp.narrow_staged = narrow_staged ? 1u : 0u;
         wp.prof8 = db->d_prof8;
         wp.pstride = pl.pstride;
         wp.n_tiles = n_tiles;

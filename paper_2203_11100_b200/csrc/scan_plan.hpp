@@ -50,7 +50,9 @@ enum GroupMode : uint8_t {
                         // efficient split when the query has many tiles and the group few rows (long queries,
                         // small per-GPU shards)
 };
-constexpr int kNarrowTile = 8;
+constexpr int kNarrowTile = 8;          // columns of a narrow tile ...
+constexpr int kNarrowTileFine = 4;      // ... or of a fine one, for the most chain-bound searches
+constexpr uint32_t kNarrowChunkBytes = 8 * 32 * 8;   // a block of border rows in a narrow link buffer: 8 rows x 32 lanes x 8 B
 
 enum ScanPolicy : int { kScanAuto = 0, kScanPipeline = 1, kScanWavefront = 2 };   // = swb_scan_policy
 
@@ -78,6 +80,12 @@ struct ScanKnobs {
     double duo_tall = 1.0;           // SWB200_DUO_TALL: ... and the tallest group's rows x SMs stay under this x the database's rows x 2
                                      // (a half-group is one CTA's item: it must fit that CTA's fair share of the scan)
     double duo_min_groups_per_sm = 2.0; // SWB200_DUO_MINGROUPS: ... and the database has at least this many groups per SM
+    double narrow_fine = 8.0;        // SWB200_NARROW_FINE: narrow tiles are 4 columns instead of 8 when the tallest group's rows exceed
+                                     // this x a warp's fair share of the search (an 8-column chain, ~95 clk per row, would still be
+                                     // about half the search)
+    double narrow_sms = 0.5;         // SWB200_NARROW_SMS: next to the pipeline, narrow units get a scheduler each (4 warps per SM) on at
+                                     // most this fraction of the SMs
+    uint64_t narrow_link_rows = 24u << 20; // SWB200_NARROW_LINKROWS: row slots (256 B each) of narrow link buffers at most (6 GiB)
     double wave_thin = 4.0;          // SWB200_WAVE_THIN: next to the pipeline, the wavefront kernel runs 8 warps per SM instead of
                                      // 16 when max_rows exceeds this x a warp's fair share of the search, and 4 warps beyond 1.5 x
                                      // this: its SMs then hold little besides the longest group's chain, which runs faster with
@@ -106,6 +114,9 @@ struct ScanKnobs {
         k.pipe_ring_cap = std::max<uint32_t>(2, static_cast<uint32_t>(num("SWB200_PIPE_RING", k.pipe_ring_cap)));
         k.pipe_lag_div = std::max<uint32_t>(1, static_cast<uint32_t>(num("SWB200_PIPE_LAGDIV", k.pipe_lag_div)));
         k.wave_thin = num("SWB200_WAVE_THIN", k.wave_thin);
+        k.narrow_fine = num("SWB200_NARROW_FINE", k.narrow_fine);
+        k.narrow_sms = num("SWB200_NARROW_SMS", k.narrow_sms);
+        k.narrow_link_rows = static_cast<uint64_t>(num("SWB200_NARROW_LINKROWS", static_cast<double>(k.narrow_link_rows)));
         k.duo_ratio = num("SWB200_DUO", k.duo_ratio);
         k.duo_stream_tiles = std::max<uint32_t>(16, static_cast<uint32_t>(num("SWB200_DUO_TILES", k.duo_stream_tiles)));
         k.duo_tall = num("SWB200_DUO_TALL", k.duo_tall);
@@ -120,7 +131,7 @@ struct ScanShape {
     uint32_t n_groups = 0;
     uint64_t padded_rows = 0;            // sum of the groups' padded rows
     uint32_t n_tiles = 0;                // ceil(m / 32)
-    uint32_t n_tiles_narrow = 0;         // ceil(m / 8)
+    uint32_t query_len = 0;              // m
     uint32_t sm_count = 0;
     uint32_t warps_per_cta = 16;
     bool s16 = true;                     // the packed int16 kernels scan (row blocks, narrow tiles, pipeline exist there only)
@@ -134,6 +145,10 @@ struct ScanPlan {
     uint32_t wave_threads = 512; // its CTA size
     uint32_t n_units = 0;      // wavefront units
     uint64_t vstate_slots = 0; // tiles of register state handed between row blocks
+    uint32_t narrow_tile = kNarrowTile;   // columns of a narrow tile (8 or 4)
+    uint32_t n_tiles_narrow = 0;          // ceil(m / narrow_tile)
+    uint64_t link_rows = 0;    // row slots of the narrow groups' link buffers (vstate_off[g]: a narrow group's first one)
+    bool narrow_staged = false;     // narrow units hand over through link buffers of their own (kernels.cuh: the data is the flag)
     bool any_narrow = false, any_rowblock = false, chain_bound = false;
     uint32_t n_split = 0, n_narrow = 0, n_rowblock = 0;   // groups per mode (the rest of [0, pipe_first) is single)
     uint64_t wave_rows = 0;    // padded rows of the wavefront kernel's groups
@@ -152,6 +167,19 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
     pl.wave_rows = in.padded_rows;
     const double fair_all = static_cast<double>(in.padded_rows) * n_tiles / (static_cast<double>(in.sm_count) * in.warps_per_cta);
     pl.chain_bound = static_cast<double>(max_rows) > k.pipe_chain * fair_all;
+    // Narrow units come in two forms.  With link buffers of their own (kernels.cuh: the data is the flag, no fences) a block
+    // costs half as much, but every tile runs kNarrowLagBlocks + 1 blocks behind its left neighbour and the links take
+    // 256 B per row and tile boundary: that form is for wavefronts that are shallow against the tallest group (short
+    // queries), in 4-column tiles for the most chain-bound searches.  Deep wavefronts (many 8-column tiles: long queries)
+    // keep the classic hand-over through the border arrays and progress counters.
+    pl.narrow_tile = static_cast<double>(max_rows) > k.narrow_fine * fair_all ? kNarrowTileFine : kNarrowTile;
+    pl.n_tiles_narrow = (in.query_len + pl.narrow_tile - 1) / pl.narrow_tile;
+    pl.narrow_staged = max_rows / kRowsPerChunk >= 32ull * pl.n_tiles_narrow;
+    if (!pl.narrow_staged && pl.narrow_tile != kNarrowTile) {
+        pl.narrow_tile = kNarrowTile;
+        pl.n_tiles_narrow = (in.query_len + pl.narrow_tile - 1) / pl.narrow_tile;
+        pl.narrow_staged = max_rows / kRowsPerChunk >= 32ull * pl.n_tiles_narrow;
+    }
     const bool can_pipe = in.s16 && in.pipe_rings >= 2 && n_groups > 0;
     if (can_pipe && in.policy == kScanPipeline) {
         pl.pipe_first = 0;
@@ -198,7 +226,8 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
     // that carries both extra paths spills registers in the common 32-column sweep (about 12 % slower), so a search
     // that needs narrow tiles cuts its other large groups by rows only if cutting them by tile instead would waste
     // more than that (small shards, long queries).
-    const bool narrow_needed = in.s16 && n_wave && in.n_tiles_narrow > 1 && rows_of(0) > narrow_rows;
+    const bool narrow_ok = in.s16 && pl.n_tiles_narrow > 1;
+    const bool narrow_needed = narrow_ok && n_wave && rows_of(0) > narrow_rows;
     bool row_blocks_ok = in.s16 && k.row_blocks;
     auto split_shape = [&](uint32_t g, double* eff_tiles, double* eff_rows) {   // -> row blocks of >= 2 chunks, ~budget row-tiles each
         const uint64_t chunks = in.groups[g].n_chunks, rows = rows_of(g), work = rows * n_tiles;
@@ -239,10 +268,14 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
                 took_vstate = true;
             }
         }
-        if (in.s16 && rows > narrow_rows && in.n_tiles_narrow > 1) {
+        const uint64_t links = pl.narrow_staged ? rows * (pl.n_tiles_narrow - 1) : 0;   // a link buffer per tile boundary
+        if (narrow_ok && rows > narrow_rows && pl.link_rows + links <= k.narrow_link_rows &&
+            pl.link_rows + links < (1ull << 32)) {
             if (took_vstate) pl.vstate_slots -= n_tiles;
             mode = kGroupNarrow;
-            units = in.n_tiles_narrow;
+            units = pl.n_tiles_narrow;
+            vstate_off[g] = static_cast<uint32_t>(pl.link_rows);
+            pl.link_rows += links;
         }
         modes[g] = mode;
         pl.n_split += mode == kGroupSplit;
@@ -252,6 +285,17 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
     }
     pl.any_narrow = pl.n_narrow > 0;
     pl.any_rowblock = pl.n_rowblock > 0;
+    if (pl.any_narrow && pl.narrow_staged && pl.pipe_first < n_groups && pl.narrow_tile == kNarrowTileFine) {
+        // The most chain-bound searches (those that take 4-column tiles): narrow units are bound by their own chain and run
+        // it fastest alone on a scheduler (tools/lat_probe.cu: 760 clk per 8 x 8 block with one warp per scheduler, 1,336
+        // with two): 4 warps per CTA, and SMs for the first round of units.  Where the chain is a smaller part of the
+        // search (a whole Swiss-Prot on one GPU, m = 144: 5 x a warp's fair share) the SMs are worth more to the pipeline.
+        pl.wave_threads = 128;   // = kNarrowThreads (kernels.cuh)
+        const uint32_t want = (pl.n_units + 3) / 4;
+        const uint32_t cap = std::max<uint32_t>(pl.wave_sms, static_cast<uint32_t>(k.narrow_sms * in.sm_count));
+        pl.wave_sms = std::max(pl.wave_sms, std::min(want, cap));
+        pl.wave_sms = std::max<uint32_t>(1, std::min<uint32_t>(pl.wave_sms, in.sm_count - 1));
+    }
     unit_start[n_wave] = pl.n_units;
     for (uint32_t g = n_wave + 1; g <= n_groups; ++g) unit_start[g] = pl.n_units;
     return pl;

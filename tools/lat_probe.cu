@@ -60,18 +60,113 @@ void run_chain(const char* name, int warps) {
     cudaFree(sink), cudaFree(clocks);
 }
 
+// What does a global store cost a lone warp?  Per iteration: 64 independent-ish DPX instructions (8 chains x 8) and
+// `kStores` stores of 8 bytes per lane (256 B per warp, coalesced), to addresses that advance like a link buffer's.
+enum StoreKind { kStWeak, kStStrong, kStCg, kStShared };
+template <int KIND, int kStores>
+__global__ void store_cost_kernel(unsigned long long* out, uint32_t* sink, long long* clocks, uint32_t a, uint32_t b, int iters) {
+    __shared__ unsigned long long sm[8 * 32];
+    uint32_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 2654435761u + i;
+    unsigned long long* o = out + threadIdx.x;
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = __viaddmax_s16x2(x[i], a, b);
+#pragma unroll
+        for (int r = 0; r < kStores; ++r) {
+            const unsigned long long v = (static_cast<unsigned long long>(x[r & 7]) << 32) | x[(r + 1) & 7];
+            if (KIND == kStWeak) o[r * 32] = v;
+            if (KIND == kStStrong) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(o + r * 32), "l"(v));
+            if (KIND == kStCg) asm volatile("st.global.cg.u64 [%0], %1;" ::"l"(o + r * 32), "l"(v));
+            if (KIND == kStShared) sm[r * 32 + threadIdx.x] = v;
+        }
+        o += 8 * 32;
+    }
+    const long long t1 = clock64();
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc ^= x[i];
+    if (acc == 0x12345678u) sink[0] = acc + static_cast<uint32_t>(sm[threadIdx.x]);
+    if (threadIdx.x == 0) clocks[0] = t1 - t0;
+}
+
+template <int KIND, int kStores>
+void run_store(const char* name, unsigned long long* buf) {
+    uint32_t* sink;
+    long long* clocks;
+    cudaMalloc(&sink, 64);
+    cudaMalloc(&clocks, 8);
+    const int iters = 4000;
+    for (int rep = 0; rep < 2; ++rep) store_cost_kernel<KIND, kStores><<<1, 32>>>(buf, sink, clocks, 0xfffefffeu, 0x00030003u, iters);
+    long long c = 0;
+    cudaMemcpy(&c, clocks, 8, cudaMemcpyDeviceToHost);
+    std::printf("64 DPX instr + %d %-22s stores per iteration: %7.1f clk per iteration\n", kStores, name, double(c) / iters);
+    cudaFree(sink), cudaFree(clocks);
+}
+
+// Latency of ld.relaxed.gpu on lines another SM has just written (a link buffer's situation): CTA 0 fills `n` words of 8
+// bytes per lane with st.relaxed.gpu and raises a flag; CTA 1 (another SM) then chases a dependent chain of loads
+// through them; for comparison CTA 0 afterwards chases through its own lines.
+__global__ void link_latency_kernel(unsigned long long* buf, uint32_t* flag, int n, long long* clocks) {
+    const uint32_t lane = threadIdx.x;
+    if (blockIdx.x == 0) {
+        for (int i = 0; i < n; ++i) {
+            const unsigned long long next = static_cast<unsigned long long>((i + 1) % n);
+            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(buf + static_cast<size_t>(i) * 32 + lane), "l"(next));
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicExch(flag, 1u);
+    }
+    if (lane == 0) while (atomicAdd(flag, 0u) == 0u) __nanosleep(100);
+    __syncwarp();
+    if (blockIdx.x == 1) __nanosleep(2000);
+    unsigned long long at = 0;
+    const long long t0 = clock64();
+    for (int i = 0; i < n; ++i) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(at) : "l"(buf + at * 32 + lane));
+    const long long t1 = clock64();
+    if (lane == 0) clocks[blockIdx.x] = (t1 - t0) + (at == 12345 ? 1 : 0);
+}
+
 // One warp (or `warps` warps, each its own copy) sweeps a narrow tile over n_chunks chunks: no producer, no consumer.
-__global__ void __launch_bounds__(512, 1) narrow_kernel(WaveParams p, long long* clocks) {
-    extern __shared__ __align__(16) uint8_t smem_prof[];
+template <int T>
+__global__ void __launch_bounds__(128, 1) narrow_kernel(WaveParams p, long long* clocks) {
+    extern __shared__ __align__(128) uint8_t smem_prof[];
     const uint32_t n16 = kProfRows * p.pstride / 16;
     for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) reinterpret_cast<uint4*>(smem_prof)[i] = reinterpret_cast<const uint4*>(p.prof8)[i];
+    __shared__ uint32_t consts[2];
+    if (threadIdx.x == 0) consts[0] = p.neg_open2, consts[1] = p.neg_ext2;
     __syncthreads();
+    NarrowWarp nw{consts};
     const GroupDesc gd = p.groups[0];
     const long long t0 = clock64();
-    const uint32_t best = sweep_unit_narrow_s16(p, reinterpret_cast<const int8_t*>(smem_prof), gd, 0, 1, nullptr, nullptr, threadIdx.x & 31);
+    const uint32_t best = sweep_unit_narrow_s16<T>(p, reinterpret_cast<const int8_t*>(smem_prof), gd, 0, 1, nullptr, threadIdx.x & 31, nw);
     const long long t1 = clock64();
     if (best == 0x12345678u) p.slot_scores[0] = best;
     if ((threadIdx.x & 31) == 0) clocks[threadIdx.x >> 5] = t1 - t0;
+}
+
+// A chain of n_tiles narrow tiles, one warp per CTA (= per SM), handing rows over through link buffers in global memory.
+template <int T>
+__global__ void __launch_bounds__(128, 1) narrow_chain_kernel(WaveParams p, uint8_t* links, uint32_t n_tiles, long long* clocks) {
+    extern __shared__ __align__(128) uint8_t smem_prof[];
+    const uint32_t n16 = kProfRows * p.pstride / 16;
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) reinterpret_cast<uint4*>(smem_prof)[i] = reinterpret_cast<const uint4*>(p.prof8)[i];
+    __shared__ uint32_t consts[2];
+    if (threadIdx.x == 0) consts[0] = p.neg_open2, consts[1] = p.neg_ext2;
+    __syncthreads();
+    NarrowWarp nw{consts};
+    const GroupDesc gd = p.groups[0];
+    const uint32_t tile = blockIdx.x;
+    const long long t0 = clock64();
+    const uint32_t best = sweep_unit_narrow_s16<T>(p, reinterpret_cast<const int8_t*>(smem_prof), gd, tile, n_tiles, links, threadIdx.x & 31, nw);
+    const long long t1 = clock64();
+    if (best == 0x12345678u) p.slot_scores[0] = best;
+    if ((threadIdx.x & 31) == 0) clocks[blockIdx.x] = t1 - t0;
 }
 
 __global__ void __launch_bounds__(512, 1) wide_kernel(WaveParams p, long long* clocks) {
@@ -105,6 +200,37 @@ int main() {
     run_chain<kAdd, 8>("VIADD.16x2", 1);
     run_chain<kAdd, 8>("VIADD.16x2", 4);
 
+    {
+        unsigned long long* buf;
+        cudaMalloc(&buf, 4000ull * 8 * 32 * 8 + 4096);
+        run_store<kStWeak, 0>("(none)", buf);
+        run_store<kStWeak, 1>("weak global", buf);
+        run_store<kStWeak, 4>("weak global", buf);
+        run_store<kStWeak, 8>("weak global", buf);
+        run_store<kStStrong, 8>("st.relaxed.gpu", buf);
+        run_store<kStCg, 8>("st.global.cg", buf);
+        run_store<kStShared, 8>("shared", buf);
+        cudaFree(buf);
+    }
+    {
+        unsigned long long* buf;
+        uint32_t* flag;
+        long long* d_c;
+        const int n = 4096;
+        cudaMalloc(&buf, static_cast<size_t>(n) * 32 * 8);
+        cudaMalloc(&flag, 4);
+        cudaMalloc(&d_c, 16 * 8);
+        cudaFuncSetAttribute(link_latency_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 << 10);
+        for (int grid : {2, 8, 75, 148}) {   // the reader is always CTA 1; more CTAs only spread the placement
+            cudaMemset(flag, 0, 4);
+            link_latency_kernel<<<grid, 32, 120 << 10>>>(buf, flag, n, d_c);
+            long long c[2] = {};
+            cudaMemcpy(c, d_c, sizeof(c), cudaMemcpyDeviceToHost);
+            std::printf("ld.relaxed.gpu latency (grid %3d): lines written by this SM %6.1f clk, by another SM %6.1f clk\n", grid, double(c[0]) / n,
+                        double(c[1]) / n);
+        }
+        cudaFree(buf), cudaFree(flag), cudaFree(d_c);
+    }
     // the narrow sweep
     const uint32_t n_chunks = 2000;
     std::vector<uint8_t> codes(static_cast<size_t>(n_chunks) * 512);
@@ -136,16 +262,46 @@ int main() {
     p.n_tiles = 1, p.n_tiles_narrow = 1;
     p.slot_scores = d_scores;
     p.neg_open2 = 0xfff6fff6u, p.neg_ext2 = 0xfffefffeu;
-    for (int warps : {1, 4, 8, 16}) {
+    for (int warps : {1, 4}) {
         long long c[16] = {};
-        for (int rep = 0; rep < 2; ++rep) narrow_kernel<<<1, 32 * warps, kProfRows * pstride>>>(p, d_clocks);
+        for (int rep = 0; rep < 2; ++rep) narrow_kernel<8><<<1, 32 * warps, kProfRows * pstride>>>(p, d_clocks);
         cudaMemcpy(c, d_clocks, sizeof(c), cudaMemcpyDeviceToHost);
         std::printf("narrow 8x8 block sweep, %2d warps on the SM: %7.1f clk per chunk (%.1f per row)\n", warps, double(c[0]) / n_chunks,
+                    double(c[0]) / n_chunks / 8);
+        for (int rep = 0; rep < 2; ++rep) narrow_kernel<4><<<1, 32 * warps, kProfRows * pstride>>>(p, d_clocks);
+        cudaMemcpy(c, d_clocks, sizeof(c), cudaMemcpyDeviceToHost);
+        std::printf("narrow 8x4 block sweep, %2d warps on the SM: %7.1f clk per chunk (%.1f per row)\n", warps, double(c[0]) / n_chunks,
                     double(c[0]) / n_chunks / 8);
         for (int rep = 0; rep < 2; ++rep) wide_kernel<<<1, 32 * warps, kProfRows * pstride>>>(p, d_clocks);
         cudaMemcpy(c, d_clocks, sizeof(c), cudaMemcpyDeviceToHost);
         std::printf("32-column sweep,        %2d warps on the SM: %7.1f clk per chunk (%.1f per row)\n", warps, double(c[0]) / n_chunks,
                     double(c[0]) / n_chunks / 8);
+    }
+    {
+        // chains of tiles over link buffers: tile 0 alone with its stores (nobody reads), then 2, 8 and 36 tiles
+        const uint32_t max_tiles = 36;
+        uint8_t* d_links;
+        const size_t link_bytes = static_cast<size_t>(max_tiles) * n_chunks * kNarrowChunkBytes;
+        cudaMalloc(&d_links, link_bytes);
+        long long* d_c;
+        cudaMalloc(&d_c, 64 * 8);
+        cudaFuncSetAttribute(narrow_chain_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 << 10);
+        cudaFuncSetAttribute(narrow_chain_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 << 10);
+        for (uint32_t tiles : {1u, 2u, 8u, 36u}) {
+            for (int t = 0; t < 2; ++t) {
+                long long c[64] = {};
+                cudaMemset(d_links, 0x80, link_bytes);
+                // tiles == 1: the producer writes into link 0 and nobody consumes (n_tiles = 2, grid 1); 120 KB of dynamic
+                // shared memory: one CTA per SM
+                const uint32_t n_tiles = tiles == 1 ? 2 : tiles, grid = tiles == 1 ? 1 : tiles;
+                if (t == 0) narrow_chain_kernel<8><<<grid, 32, 120 << 10>>>(p, d_links, n_tiles, d_c);
+                else narrow_chain_kernel<4><<<grid, 32, 120 << 10>>>(p, d_links, n_tiles, d_c);
+                cudaMemcpy(c, d_c, sizeof(c), cudaMemcpyDeviceToHost);
+                std::printf("chain of %2u narrow tiles (T=%d): clk per chunk of tile 0 %7.1f, tile 1 %7.1f, last tile %7.1f  %s\n", tiles, t == 0 ? 8 : 4,
+                            double(c[0]) / n_chunks, double(c[grid > 1 ? 1 : 0]) / n_chunks, double(c[grid - 1]) / n_chunks,
+                            cudaGetErrorString(cudaGetLastError()));
+            }
+        }
     }
     std::printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
     return 0;
