@@ -690,10 +690,17 @@ struct IntraParams {
     int32_t open, ext;
 };
 
+// A lane meets its subject's residues in order, one per step: they come as 8-byte words (8 consecutive rows of the
+// interleaved layout), requested four steps before the first of them is needed, and the int8 profile entries of the
+// lane's own columns (25 symbols x 8 B) are staged in shared memory once per pass -- without either, every step waited
+// for two dependent global loads (2,600 clk per step instead of ~200: the int32 re-run of three 8,000-residue hits cost
+// 47 ms next to a 160 ms scan).
 template <int T, typename PT>
 __global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraParams p) {
     __shared__ uint2 ring[kIntraMaxWarps][kIntraRing];
     __shared__ int32_t warp_best[kIntraMaxWarps];
+    extern __shared__ __align__(16) uint8_t intra_dyn[];   // int8 profile: [25][blockDim.x] uint2, this pass's columns
+    uint2* const sprof = reinterpret_cast<uint2*>(intra_dyn);
 
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int32_t NO = -p.open, NE = -p.ext;
@@ -708,8 +715,9 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraPar
         const int64_t n = p.slot_len[slot];
         const GroupDesc gd = p.groups[slot / kGroupSeqs];
         const uint32_t sl = slot % kGroupSeqs;
-        // residue r of this sequence: seq[(r / 8) * 512 + (r % 8)]
-        const uint8_t* seq = p.codes + (static_cast<size_t>(gd.chunk_base) * 32 + (sl & 31)) * 16 + (sl >> 5) * 8;
+        // residues 8w .. 8w + 7 of this sequence: the 8-byte word seq8[w * 64]
+        const uint2* seq8 = reinterpret_cast<const uint2*>(p.codes + (static_cast<size_t>(gd.chunk_base) * 32 + (sl & 31)) * 16 + (sl >> 5) * 8);
+        const int64_t n_words = gd.n_chunks;
 
         int32_t best = 0;
         const int64_t steps = n + 31 + static_cast<int64_t>(kIntraDelta) * (W - 1);
@@ -727,12 +735,31 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraPar
             for (int k = 0; k < T; ++k) Hm[k] = NO, F[k] = NO;
             int32_t diag_in = NO, out_h = NO, out_e = NO;
 
-            __syncthreads();   // ring and border rows are reused across passes and items
+            __syncthreads();   // ring, border rows and the profile slice are reused across passes and items
+            if (sizeof(PT) == 1) {
+                for (uint32_t sym = 0; sym < kProfRows; ++sym)
+                    sprof[sym * blockDim.x + threadIdx.x] = *reinterpret_cast<const uint2*>(ptile + static_cast<size_t>(sym) * row_words);
+                __syncthreads();
+            }
 
+            const int64_t r0 = -static_cast<int64_t>(w) * kIntraDelta - lane;   // this lane's row at step 0
+            uint2 cur8 = make_uint2(0, 0), nxt8 = __ldg(seq8);
+            // the previous pass's border rows (warp 0, lane 0 needs row d at step d): fetched 32 rows at a time by the whole
+            // warp, a batch ahead, and handed to lane 0 by shuffle -- a load per step would stall the leading warp, and with
+            // it the whole wavefront, for an L2 round trip at every step of every pass but the first
+            const bool from_pass = w == 0 && !first;
+            uint2 bq = make_uint2(0, 0), bq_next = make_uint2(0, 0);
+            if (from_pass && lane < n) bq_next = bin[lane];
             for (int64_t d = 0; d < steps; ++d) {
-                const int64_t r = d - static_cast<int64_t>(w) * kIntraDelta - lane;
+                const int64_t r = d + r0;
                 const bool in_range = r >= 0 && r < n;
-                const uint32_t a = (in_range && tile_valid) ? seq[(r >> 3) * 512 + (r & 7)] : kPadCode;
+                if ((r & 7) == 0) cur8 = nxt8;
+                if ((r & 7) == 4) {
+                    const int64_t wi = (r >> 3) + 1;
+                    if (wi >= 0 && wi < n_words) nxt8 = __ldg(seq8 + wi * 64);
+                }
+                const uint32_t byte = ((r & 4) ? cur8.y : cur8.x) >> (8 * (static_cast<uint32_t>(r) & 3u)) & 0xffu;
+                const uint32_t a = (in_range && tile_valid) ? byte : kPadCode;
 
                 // inbound border: from the left lane (previous step), the left warp's ring, the
                 // previous pass's global row, or the matrix edge
@@ -744,16 +771,23 @@ __global__ void __launch_bounds__(32 * kIntraMaxWarps) intra_s32_kernel(IntraPar
                         if (w > 0) {
                             const uint2 v = ring[w][r & (kIntraRing - 1)];
                             in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
-                        } else if (!first) {
-                            const uint2 v = bin[r];
-                            in_h = static_cast<int32_t>(v.x), in_e = static_cast<int32_t>(v.y);
                         }
                     }
+                }
+                if (from_pass) {
+                    if ((d & 31) == 0) {
+                        bq = bq_next;
+                        const int64_t ahead = d + 32 + lane;
+                        if (ahead < n) bq_next = bin[ahead];
+                    }
+                    const uint32_t vx = __shfl_sync(0xffffffffu, bq.x, static_cast<int>(d & 31));
+                    const uint32_t vy = __shfl_sync(0xffffffffu, bq.y, static_cast<int>(d & 31));
+                    if (lane == 0 && in_range) in_h = static_cast<int32_t>(vx), in_e = static_cast<int32_t>(vy);
                 }
 
                 int32_t sub[T];
                 if (sizeof(PT) == 1) {
-                    const uint2 v = *reinterpret_cast<const uint2*>(ptile + static_cast<size_t>(a) * row_words);
+                    const uint2 v = sprof[a * blockDim.x + threadIdx.x];
 #pragma unroll
                     for (int k = 0; k < T; ++k) {
                         const uint32_t word = k < 4 ? v.x : v.y;

@@ -3,7 +3,11 @@
 
 template <int T, typename PT>
 void launch_intra(const IntraParams& ip, uint32_t ctas, uint32_t warps, cudaStream_t s) {
-    intra_s32_kernel<T, PT><<<ctas, warps * 32, 0, s>>>(ip);
+    // the int8 flavour stages each lane's 25 profile words in shared memory: 200 B per thread, 50 KB for 8 warps
+    const size_t smem = sizeof(PT) == 1 ? static_cast<size_t>(kProfRows) * warps * 32 * sizeof(uint2) : 0;
+    if (smem > 48 * 1024)   // per device, so not remembered: the call is cheap
+        cudaFuncSetAttribute(intra_s32_kernel<T, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    intra_s32_kernel<T, PT><<<ctas, warps * 32, smem, s>>>(ip);
 }
 
 template <typename PT>

@@ -77,6 +77,8 @@ struct ScanKnobs {
     uint32_t duo_stream_tiles = 704; // SWB200_DUO_TILES: tiles per stream of a shared scan at most (a tall group's item must not outlast the scan)
     uint32_t duo_pass_items = 1;     // SWB200_DUO_PASS: shared scans hand out one pass (16 tiles) of a half-group per item:
                                      // 1 (default) where whole items do not fit, 2 always, 0 ("off") never
+    uint32_t duo_window_mb = 128;    // SWB200_DUO_WINDOW_MB: pass items are handed out pass-major within windows of half-groups whose
+                                     // border rows (256 B per database row) stay under this many MB, i.e. resident in L2
     double duo_tall = 1.0;           // SWB200_DUO_TALL: ... and the tallest group's rows x SMs stay under this x the database's rows x 2
                                      // (a half-group is one CTA's item: it must fit that CTA's fair share of the scan)
     double duo_min_groups_per_sm = 2.0; // SWB200_DUO_MINGROUPS: ... and the database has at least this many groups per SM
@@ -120,6 +122,7 @@ struct ScanKnobs {
         k.duo_ratio = num("SWB200_DUO", k.duo_ratio);
         k.duo_stream_tiles = std::max<uint32_t>(16, static_cast<uint32_t>(num("SWB200_DUO_TILES", k.duo_stream_tiles)));
         k.duo_tall = num("SWB200_DUO_TALL", k.duo_tall);
+        k.duo_window_mb = std::max<uint32_t>(1, static_cast<uint32_t>(num("SWB200_DUO_WINDOW_MB", k.duo_window_mb)));
         if (const char* e = std::getenv("SWB200_DUO_PASS")) k.duo_pass_items = std::string(e) == "off" ? 0u : static_cast<uint32_t>(std::atoi(e));
         k.duo_min_groups_per_sm = num("SWB200_DUO_MINGROUPS", k.duo_min_groups_per_sm);
         return k;

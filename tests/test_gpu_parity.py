@@ -499,15 +499,19 @@ def test_two_query_scan_against_the_oracle():
 
 
 def test_narrow_block_sweep_against_the_oracle():
-    """The wavefront kernel's narrow units (8 x 8 blocks in anti-diagonal order, for groups whose chain of rows bounds
-    the search) forced onto small databases: whole score vectors equal the oracle's (tests/_narrow_small.py)."""
+    """The wavefront kernel's narrow units (blocks of 8 rows x 8 or 4 columns in anti-diagonal order, handed from tile to
+    tile through link buffers whose data is the flag, for groups whose chain of rows bounds the search) forced onto small
+    databases, alone and next to the pipeline: whole score vectors equal the oracle's (tests/_narrow_small.py)."""
     import os, subprocess, sys
     from pathlib import Path
     root = Path(__file__).resolve().parent.parent
-    env = dict(os.environ, SWB200_NARROW="0.0001")
-    out = subprocess.run([sys.executable, str(root / "tests" / "_narrow_small.py")], cwd=root, env=env, capture_output=True,
-                         text=True, timeout=900)
-    assert out.returncode == 0 and "NARROW-SMALL-OK" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
+    for extra in ({}, {"SWB200_NARROW_FINE": "0.0001"}):      # 8-column tiles; 4-column tiles wherever the wavefront is shallow
+        env = dict(os.environ, SWB200_NARROW="0.0001", **extra)
+        out = subprocess.run([sys.executable, str(root / "tests" / "_narrow_small.py")], cwd=root, env=env, capture_output=True,
+                             text=True, timeout=900)
+        assert out.returncode == 0 and "NARROW-SMALL-OK" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
+        if extra:
+            assert "(4, 128, True)" in out.stdout, out.stdout[-1500:]     # 4-column tiles, CTAs of 4 warps, link buffers
 
 
 def test_large_random_batch_shares_scans_and_equals_single_searches(b62):

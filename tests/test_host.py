@@ -204,6 +204,25 @@ def test_scan_plan_divides_every_group_exactly_once(lib):
     assert search.scan_plan(lens, 1000)["ring_chunks"] == 4 and search.scan_plan(lens, 5478)["ring_chunks"] == 2
 
 
+def test_scan_plan_narrow_forms(lib):
+    """Narrow units (kernels.cuh): with link buffers of their own where the wavefront of narrow tiles is shallow against
+    the tallest group (short queries) -- in 4-column tiles and CTAs of 4 warps for the most chain-bound searches (a 1/8
+    shard, m = 144) -- and in the classic form through the border arrays for deep wavefronts (long queries)."""
+    lens = _swissprot_lengths()
+    whole = search.scan_plan(lens, 144)
+    assert whole["chain_bound"] == 1 and whole["narrow_groups"] > 0 and whole["narrow_tile"] == 8
+    assert whole["narrow_link_bytes"] > 0 and whole["wavefront_threads"] == 256
+    # links: 256 B per row of every narrow group and tile boundary (18 tiles of 8 columns: 17 boundaries)
+    assert whole["narrow_link_bytes"] % (256 * 17) == 0
+    shard = search.scan_plan(lens, 144, shard_rank=0, shard_count=8)
+    assert shard["narrow_tile"] == 4 and shard["wavefront_threads"] == 128 and shard["narrow_link_bytes"] > 0
+    assert shard["wavefront_units"] >= 36 * shard["narrow_groups"]                 # 36 tiles of 4 columns per narrow group
+    assert 4 * shard["wavefront_sms"] >= min(shard["wavefront_units"], 4 * 74)     # a scheduler per unit, on at most half the SMs
+    deep = search.scan_plan(lens, 3564, shard_rank=0, shard_count=8)
+    assert deep["narrow_groups"] > 0 and deep["narrow_tile"] == 8 and deep["narrow_link_bytes"] == 0   # 446 tiles: classic form
+    assert search.scan_plan(lens, 2005)["narrow_groups"] == 0 or search.scan_plan(lens, 2005)["narrow_link_bytes"] == 0
+
+
 def test_scan_plan_policies_and_small_databases(lib):
     lens = _swissprot_lengths()
     forced = search.scan_plan(lens, 2005, policy=search.Database.SCAN_PIPELINE)
