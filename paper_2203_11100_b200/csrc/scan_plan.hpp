@@ -88,6 +88,7 @@ struct ScanKnobs {
     double narrow_sms = 0.5;         // SWB200_NARROW_SMS: next to the pipeline, narrow units get a scheduler each (4 warps per SM) on at
                                      // most this fraction of the SMs
     uint64_t narrow_link_rows = 24u << 20; // SWB200_NARROW_LINKROWS: row slots (256 B each) of narrow link buffers at most (6 GiB)
+    uint32_t wave_threads = 0;       // SWB200_WAVE_THREADS: CTA size of the wavefront kernel (128, 256 or 512; 0: automatic)
     double wave_thin = 4.0;          // SWB200_WAVE_THIN: next to the pipeline, the wavefront kernel runs 8 warps per SM instead of
                                      // 16 when max_rows exceeds this x a warp's fair share of the search, and 4 warps beyond 1.5 x
                                      // this: its SMs then hold little besides the longest group's chain, which runs faster with
@@ -116,6 +117,7 @@ struct ScanKnobs {
         k.pipe_ring_cap = std::max<uint32_t>(2, static_cast<uint32_t>(num("SWB200_PIPE_RING", k.pipe_ring_cap)));
         k.pipe_lag_div = std::max<uint32_t>(1, static_cast<uint32_t>(num("SWB200_PIPE_LAGDIV", k.pipe_lag_div)));
         k.wave_thin = num("SWB200_WAVE_THIN", k.wave_thin);
+        k.wave_threads = static_cast<uint32_t>(num("SWB200_WAVE_THREADS", 0.0));
         k.narrow_fine = num("SWB200_NARROW_FINE", k.narrow_fine);
         k.narrow_sms = num("SWB200_NARROW_SMS", k.narrow_sms);
         k.narrow_link_rows = static_cast<uint64_t>(num("SWB200_NARROW_LINKROWS", static_cast<double>(k.narrow_link_rows)));
@@ -211,7 +213,9 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
     const uint32_t n_wave = pl.pipe_first;
     const uint64_t total_row_tiles = pl.wave_rows * n_tiles;
     pl.wave_threads = in.warps_per_cta * 32;
-    if (pl.pipe_first < n_groups && pl.pipe_first > 0) {
+    if (k.wave_threads) {
+        pl.wave_threads = k.wave_threads;   // tuning override
+    } else if (pl.pipe_first < n_groups && pl.pipe_first > 0) {
         const double chain = static_cast<double>(max_rows) / std::max(fair_all, 1.0);
         if (chain >= 1.5 * k.wave_thin) pl.wave_threads = std::min<uint32_t>(pl.wave_threads, 128);
         else if (chain >= k.wave_thin) pl.wave_threads = std::min<uint32_t>(pl.wave_threads, 256);
