@@ -768,6 +768,11 @@ swb_status swb_scan_plan(const uint32_t* lens, uint32_t n, uint64_t length_thres
     shape.padded_rows = padded_rows;
     shape.n_tiles = (query_len + kInterTile - 1) / kInterTile;
     shape.query_len = query_len;
+    {
+        const size_t prof_bytes = static_cast<size_t>(kProfRows) * profile_stride(query_len, kInterTile);
+        const size_t used = ((prof_bytes + 127) & ~size_t(127)) + 1024;
+        shape.narrow_room = used < kSmemOptinB200 ? kSmemOptinB200 - used : 0;
+    }
     shape.sm_count = sm_count;
     shape.warps_per_cta = kInterThreads / 32;
     shape.policy = policy;

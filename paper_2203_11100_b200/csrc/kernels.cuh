@@ -148,6 +148,9 @@ struct WaveParams {
     uint32_t narrow_tile;         // 8 or 4 columns
     uint32_t narrow_staged;       // 1: narrow units hand over through link buffers of their own (short queries);
                                   // 0: through the border arrays like every other tile (deep wavefronts: many narrow tiles)
+    uint32_t narrow_helpers;      // 1: CTAs of 8 warps, warps 0-3 take units, warps 4-7 carry their narrow units' blocks between the
+                                  // link buffers and rings in shared memory (narrow_stage_off: where those start)
+    uint32_t narrow_stage_off;
     uint8_t* nlinks;              // link buffers of the narrow groups (vstate_off[g]: first row slot, 256 B each, of group g's links)
 };
 
@@ -385,11 +388,130 @@ __device__ __forceinline__ bool link_empty(unsigned long long v) { return static
 // Per-warp state of the narrow units.
 struct NarrowWarp {
     const uint32_t* consts;   // (neg_open2, neg_ext2) in shared memory
+    uint32_t in_ring = 0;     // kRings: shared-memory address of the pair's inbound / outbound ring of blocks
+    uint32_t out_ring = 0;
+    uint32_t mailbox = 0;     // and of the mailbox through which the compute warp tells its helper what to carry
+    uint32_t posted = 0;      // commands posted so far
 };
+
+// With a helper warp (kRings): the compute warp of a narrow unit never touches global memory for its hand-off.  Its
+// partner on the same scheduler -- warp w + 4 of the CTA -- carries the blocks between the link buffers in global memory
+// (same strong relaxed accesses, same "data is the flag" protocol as above) and two rings of kNarrowRingSlots blocks in
+// shared memory, where the flag is again the data: a slot whose Hm words read kNarrowEmpty is free / not yet filled.  The
+// compute warp waits 30 clk for a shared-memory load instead of 310 for L2, packs and checks nothing for the far side, and
+// the helper's waiting costs its scheduler nothing but an occasional poll.
+constexpr uint32_t kNarrowRingSlots = 4;
+constexpr uint32_t kNarrowPairBytes = 2 * kNarrowRingSlots * kNarrowChunkBytes + 64;   // in ring, out ring, mailbox
+static_assert(kNarrowPairBytes == kNarrowPairBytesHost, "scan_plan.hpp and kernels.cuh disagree on a pair's shared memory");
+struct NarrowMail {           // compute warp -> helper
+    uint32_t cmd;             // incremented by the compute warp once the fields below describe a new unit (0: nothing yet)
+    uint32_t done;            // set to cmd by the helper when it has carried the unit's last block
+    uint32_t kind;            // 1: a narrow unit, 0: leave
+    uint32_t n_chunks, tile, n_tiles;
+    uint32_t link_lo, link_hi;   // the group's link buffers (64-bit address)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint4 lds128v(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128v(uint32_t a, uint4 v) {
+    asm volatile("st.volatile.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+}
+__device__ __forceinline__ uint32_t lds32v(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts32v(uint32_t a, uint32_t v) { asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
+
+// The helper's side of one narrow unit: blocks of the inbound link -> the in ring, blocks of the out ring -> the outbound
+// link, each as far as its source has them and its target has room; neither direction ever blocks the other.
+__device__ __forceinline__ void narrow_helper_unit(uint8_t* link_base, uint32_t n_chunks, uint32_t tile, uint32_t n_tiles, uint32_t lane,
+                                                   const NarrowWarp& nw) {
+    constexpr size_t kBlockWords = kNarrowChunkBytes / 8;
+    const size_t link_words = static_cast<size_t>(n_chunks) * kBlockWords;
+    unsigned long long* const links = reinterpret_cast<unsigned long long*>(link_base);
+    const bool has_in = tile > 0, has_out = tile + 1 < n_tiles;
+    unsigned long long* lin = links + (static_cast<size_t>(tile) - (has_in ? 1 : 0)) * link_words + lane * 2;
+    unsigned long long* lout = links + static_cast<size_t>(tile) * link_words + lane * 2;
+    const uint4 empty4 = make_uint4(kNarrowEmptyWord, kNarrowEmptyWord, kNarrowEmptyWord, kNarrowEmptyWord);
+    uint32_t bi = 0, bo = 0;
+    // outbound: a block the compute warp has completed -> the link buffer; false: nothing there yet
+    auto try_out = [&]() -> bool {
+        if (!has_out || bo >= n_chunks) return false;
+        const uint32_t slot = nw.out_ring + (bo % kNarrowRingSlots) * kNarrowChunkBytes + lane * 16;
+        uint4 v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = lds128v(slot + i * 512);
+        bool valid = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) valid &= v[i].x != kNarrowEmptyWord && v[i].z != kNarrowEmptyWord;
+        if (!__all_sync(0xffffffffu, valid)) return false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sts128v(slot + i * 512, empty4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            st_link2(lout + i * 64, (static_cast<unsigned long long>(v[i].y) << 32) | v[i].x, (static_cast<unsigned long long>(v[i].w) << 32) | v[i].z);
+        lout += kBlockWords;
+        ++bo;
+        return true;
+    };
+    // inbound: TWO blocks are on request at any time, each into registers of its own (ga: the block to move next, gb: the
+    // one after it, then the roles swap), so that an answer that came too early costs one more round trip for that block
+    // only, and the stream is not paced by one L2 round trip per block
+    unsigned long long ga[8], gb[8];
+    auto request = [&](unsigned long long(&g)[8], uint32_t block) {
+        const unsigned long long* at = lin + static_cast<size_t>(min(block, n_chunks - 1)) * kBlockWords;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ld_link2(at + i * 64, g[2 * i], g[2 * i + 1]);
+    };
+    // block bi is in g (or on its way): into the in ring if it is all there and the slot is free
+    auto try_in = [&](unsigned long long(&g)[8]) -> bool {
+        bool valid = true;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) valid &= !link_empty(g[i]);
+        if (!__all_sync(0xffffffffu, valid)) {
+            request(g, bi);   // not all there yet: ask again
+            return false;
+        }
+        const uint32_t slot = nw.in_ring + (bi % kNarrowRingSlots) * kNarrowChunkBytes + lane * 16;
+        if (!__all_sync(0xffffffffu, lds32v(slot + 3 * 512 + 8) == kNarrowEmptyWord)) return false;   // the slot's last word: not free yet
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            sts128v(slot + i * 512, make_uint4(static_cast<uint32_t>(g[2 * i]), static_cast<uint32_t>(g[2 * i] >> 32),
+                                               static_cast<uint32_t>(g[2 * i + 1]), static_cast<uint32_t>(g[2 * i + 1] >> 32)));
+        unsigned long long* at = lin + static_cast<size_t>(bi) * kBlockWords;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) st_link2(at + i * 64, kNarrowEmpty, kNarrowEmpty);
+        ++bi;
+        request(g, bi + 1);   // the other register set holds block bi now
+        return true;
+    };
+    if (has_in) {
+        request(ga, 0);
+        request(gb, 1);
+        while (bi < n_chunks) {
+            while (!try_in(ga))
+                if (!try_out()) __nanosleep(40);
+            try_out();
+            if (bi >= n_chunks) break;
+            while (!try_in(gb))
+                if (!try_out()) __nanosleep(40);
+            try_out();
+        }
+    }
+    // (a short back-off: spinning without it takes issue slots from the compute warp on the same scheduler -- 680 against 637
+    // clk per block for a tile that only sends)
+    while (has_out && bo < n_chunks)
+        if (!try_out()) __nanosleep(40);
+}
 
 // kFirst / kLast (tile 0 / the last tile) are compile-time, so that a tile without an inbound or outbound link carries
 // none of its code and the block loop's body is straight-line code apart from the rare "a row has not arrived yet".
-template <int T, bool kFirst, bool kLast>
+template <int T, bool kFirst, bool kLast, bool kRings>
 __device__ __forceinline__ uint32_t sweep_narrow_tile_s16(const WaveParams& p, const int8_t* prof, const GroupDesc& gd, uint32_t tile,
                                                           uint8_t* link_base, uint32_t lane, NarrowWarp& nw) {
     constexpr int R = static_cast<int>(kRowsPerChunk);
@@ -442,10 +564,11 @@ __device__ __forceinline__ uint32_t sweep_narrow_tile_s16(const WaveParams& p, c
     const unsigned long long edge = (static_cast<unsigned long long>(NO) << 32) | NO;
 #pragma unroll
     for (int i = 0; i < R; ++i) q[i] = qn[i] = edge;
-    if (!kFirst) {
+    if (!kFirst && !kRings) {
         fall_back(lin);
         request(q, lin);
     }
+    const uint4 empty4 = make_uint4(kNarrowEmptyWord, kNarrowEmptyWord, kNarrowEmptyWord, kNarrowEmptyWord);
     auto profile_rows = [&](const uint4& w, ProfWord* pa, ProfWord* pb) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -473,7 +596,27 @@ __device__ __forceinline__ uint32_t sweep_narrow_tile_s16(const WaveParams& p, c
             if constexpr (T == 8) return prmt(c < 4 ? pa[r].x : pa[r].y, c < 4 ? pb[r].x : pb[r].y, sel);
             else return prmt(pa[r], pb[r], sel);
         };
-        if (!kFirst) {
+        if (!kFirst && kRings) {
+            // this block's rows from the in ring (the helper warp brings them): wait until every word is there, take them,
+            // give the slot back
+            const uint32_t slot = nw.in_ring + (chunk % kNarrowRingSlots) * kNarrowChunkBytes + lane * 16;
+            uint4 v[R / 2];
+            for (;;) {
+#pragma unroll
+                for (int i = 0; i < R / 2; ++i) v[i] = lds128v(slot + i * 512);
+                bool valid = true;
+#pragma unroll
+                for (int i = 0; i < R / 2; ++i) valid &= v[i].x != kNarrowEmptyWord && v[i].z != kNarrowEmptyWord;
+                if (valid) break;
+                __nanosleep(20);
+            }
+#pragma unroll
+            for (int i = 0; i < R / 2; ++i) sts128v(slot + i * 512, empty4);
+#pragma unroll
+            for (int i = 0; i < R / 2; ++i)
+                q[2 * i] = (static_cast<unsigned long long>(v[i].y) << 32) | v[i].x, q[2 * i + 1] = (static_cast<unsigned long long>(v[i].w) << 32) | v[i].z;
+        }
+        if (!kFirst && !kRings) {
             request(qn, next_block(lin));   // the next block's rows (past the end: the last block's again, unused)
             // this block's rows, requested a block ago.  A missing one means the tile has caught up with its producer:
             // it falls back by kNarrowLagBlocks instead of trailing it row by row, then asks for both blocks again
@@ -519,7 +662,18 @@ __device__ __forceinline__ uint32_t sweep_narrow_tile_s16(const WaveParams& p, c
                 else pend = dcur, have = true;
             }
         }
-        if (!kLast) {
+        if (!kLast && kRings) {
+            // outbound: into the out ring once its slot is free (the helper warp takes it from there)
+            const uint32_t slot = nw.out_ring + (chunk % kNarrowRingSlots) * kNarrowChunkBytes + lane * 16;
+            while (lds32v(slot + 3 * 512 + 8) != kNarrowEmptyWord) __nanosleep(20);
+#pragma unroll
+            for (int i = 0; i < R / 2; ++i) {
+                const uint32_t h0 = hl[2 * i] == kNarrowEmptyWord ? kNarrowEmptyWord + 1 : hl[2 * i];
+                const uint32_t h1 = hl[2 * i + 1] == kNarrowEmptyWord ? kNarrowEmptyWord + 1 : hl[2 * i + 1];
+                sts128v(slot + i * 512, make_uint4(h0, E[2 * i], h1, E[2 * i + 1]));
+            }
+        }
+        if (!kLast && !kRings) {
 #pragma unroll
             for (int i = 0; i < R / 2; ++i) {
                 // only a lane that has already wrapped can hold the "empty" pattern: nudge it, garbage stays garbage
@@ -530,7 +684,7 @@ __device__ __forceinline__ uint32_t sweep_narrow_tile_s16(const WaveParams& p, c
             }
             lout += kBlockWords;
         }
-        if (!kFirst) {
+        if (!kFirst && !kRings) {
             lin = next_block(lin);
 #pragma unroll
             for (int i = 0; i < R; ++i) q[i] = qn[i];
@@ -543,14 +697,14 @@ __device__ __forceinline__ uint32_t sweep_narrow_tile_s16(const WaveParams& p, c
     return best;
 }
 
-template <int T>
+template <int T, bool kRings>
 __device__ __forceinline__ uint32_t sweep_unit_narrow_s16(const WaveParams& p, const int8_t* prof, const GroupDesc& gd, uint32_t tile,
                                                           uint32_t n_tiles, uint8_t* link_base, uint32_t lane, NarrowWarp& nw) {
     const bool first = tile == 0, last = tile + 1 == n_tiles;
-    if (first) return last ? sweep_narrow_tile_s16<T, true, true>(p, prof, gd, tile, link_base, lane, nw)
-                           : sweep_narrow_tile_s16<T, true, false>(p, prof, gd, tile, link_base, lane, nw);
-    return last ? sweep_narrow_tile_s16<T, false, true>(p, prof, gd, tile, link_base, lane, nw)
-                : sweep_narrow_tile_s16<T, false, false>(p, prof, gd, tile, link_base, lane, nw);
+    if (first) return last ? sweep_narrow_tile_s16<T, true, true, kRings>(p, prof, gd, tile, link_base, lane, nw)
+                           : sweep_narrow_tile_s16<T, true, false, kRings>(p, prof, gd, tile, link_base, lane, nw);
+    return last ? sweep_narrow_tile_s16<T, false, true, kRings>(p, prof, gd, tile, link_base, lane, nw)
+                : sweep_narrow_tile_s16<T, false, false, kRings>(p, prof, gd, tile, link_base, lane, nw);
 }
 
 // Group modes (GroupMode, kNarrowTile): scan_plan.hpp, where the host decides them per search.
@@ -566,6 +720,19 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
         __shared__ uint32_t narrow_consts[2];   // sweep_narrow_tile_s16 reads its packed constants from here
         if (threadIdx.x == 0) narrow_consts[0] = p.neg_open2, narrow_consts[1] = p.neg_ext2;
         nw.consts = narrow_consts;
+        if (p.narrow_helpers) {
+            // rings (all slots empty) and mailboxes of the four compute / helper pairs
+            const uint32_t stage = smem_u32(smem_prof) + p.narrow_stage_off;
+            for (uint32_t i = threadIdx.x; i < 4 * kNarrowPairBytes / 16; i += blockDim.x) {
+                const uint32_t off = i * 16, in_pair = off % kNarrowPairBytes;
+                const uint32_t fill = in_pair < kNarrowPairBytes - 64 ? kNarrowEmptyWord : 0u;
+                sts128v(stage + off, make_uint4(fill, fill, fill, fill));
+            }
+            const uint32_t base = stage + ((threadIdx.x >> 5) & 3) * kNarrowPairBytes;
+            nw.in_ring = base;
+            nw.out_ring = base + kNarrowRingSlots * kNarrowChunkBytes;
+            nw.mailbox = nw.out_ring + kNarrowRingSlots * kNarrowChunkBytes;
+        }
         __syncthreads();
     }
 
@@ -582,12 +749,31 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
     }
 
     const uint32_t lane = threadIdx.x & 31;
+    bool helpers = false;
+    if constexpr (kNarrow) {
+        helpers = p.narrow_helpers != 0;
+        if (helpers && (threadIdx.x >> 5) >= 4) {
+            // a helper warp: carries the blocks of whatever narrow unit its compute warp (warp - 4, same scheduler) posts
+            for (uint32_t seen = 0;;) {
+                uint32_t cmd;
+                while ((cmd = lds32v(nw.mailbox)) == seen) __nanosleep(100);
+                seen = cmd;
+                if (lds32v(nw.mailbox + 8) == 0) return;
+                const uint32_t n_chunks = lds32v(nw.mailbox + 12), tile = lds32v(nw.mailbox + 16), n_tiles = lds32v(nw.mailbox + 20);
+                const unsigned long long link = (static_cast<unsigned long long>(lds32v(nw.mailbox + 28)) << 32) | lds32v(nw.mailbox + 24);
+                narrow_helper_unit(reinterpret_cast<uint8_t*>(link), n_chunks, tile, n_tiles, lane, nw);
+                __syncwarp();
+                if (lane == 0) sts32v(nw.mailbox + 4, cmd);
+            }
+        }
+    }
+    const uint32_t n_compute = helpers ? 4u : blockDim.x >> 5;   // warps that take units
 
     // First round: static, unit (warp, CTA) -> warp x gridDim + CTA, so that consecutive units -- the tiles of the
     // tallest groups, whose warps are bound by their own chain -- start on different SMs instead of on the sixteen warps
     // of whichever CTA came up first.  After that, tickets.  Either way a unit's producer (the unit before it) is held
     // by a resident warp or was handed out earlier: waiting on it cannot deadlock (the grid never exceeds the SM count).
-    const uint32_t static_units = gridDim.x * (blockDim.x >> 5);
+    const uint32_t static_units = gridDim.x * n_compute;
     for (uint32_t round = 0;; ++round) {
         uint32_t u = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
         if (round > 0) {
@@ -626,10 +812,24 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
             bool narrow_done = false;
             if constexpr (kNarrow) {
                 if (mode == kGroupNarrow) {
-                    if (p.narrow_staged) {
+                    if (p.narrow_staged && helpers) {
+                        // tell the helper warp what to carry (once it is done with the unit before), then sweep on the rings
                         uint8_t* links = p.nlinks + static_cast<size_t>(p.vstate_off[g]) * 256;
-                        best = p.narrow_tile == 4 ? sweep_unit_narrow_s16<4>(p, prof, gd, t0, n_tiles, links, lane, nw)
-                                                  : sweep_unit_narrow_s16<8>(p, prof, gd, t0, n_tiles, links, lane, nw);
+                        while (lds32v(nw.mailbox + 4) != nw.posted) __nanosleep(40);
+                        ++nw.posted;
+                        if (lane == 0) {
+                            const unsigned long long link = reinterpret_cast<unsigned long long>(links);
+                            sts32v(nw.mailbox + 8, 1u), sts32v(nw.mailbox + 12, gd.n_chunks), sts32v(nw.mailbox + 16, t0);
+                            sts32v(nw.mailbox + 20, n_tiles), sts32v(nw.mailbox + 24, static_cast<uint32_t>(link));
+                            sts32v(nw.mailbox + 28, static_cast<uint32_t>(link >> 32));
+                            sts32v(nw.mailbox, nw.posted);
+                        }
+                        best = p.narrow_tile == 4 ? sweep_unit_narrow_s16<4, true>(p, prof, gd, t0, n_tiles, links, lane, nw)
+                                                  : sweep_unit_narrow_s16<8, true>(p, prof, gd, t0, n_tiles, links, lane, nw);
+                    } else if (p.narrow_staged) {
+                        uint8_t* links = p.nlinks + static_cast<size_t>(p.vstate_off[g]) * 256;
+                        best = p.narrow_tile == 4 ? sweep_unit_narrow_s16<4, false>(p, prof, gd, t0, n_tiles, links, lane, nw)
+                                                  : sweep_unit_narrow_s16<8, false>(p, prof, gd, t0, n_tiles, links, lane, nw);
                     } else {
                         // a deep wavefront of 8-column tiles (long query): rows fetched 8 ahead, progress published every 4 chunks
                         best = sweep_unit_s16<kNarrowTile, 8, 4, false>(p, prof, gd, t0, t1, n_tiles, dep, pub, lane, 0, gd.n_chunks, nullptr);
@@ -647,6 +847,12 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
         const uint32_t slot_a = gd.first_slot + lane;
         if (sa) atomicMax(p.slot_scores + slot_a, sa);
         if (sb) atomicMax(p.slot_scores + slot_a + 32, sb);
+    }
+    if constexpr (kNarrow) {
+        if (helpers) {   // send the helper warp home (once it is done with the last unit)
+            while (lds32v(nw.mailbox + 4) != nw.posted) __nanosleep(40);
+            if (lane == 0) sts32v(nw.mailbox + 8, 0u), sts32v(nw.mailbox, nw.posted + 1);
+        }
     }
 }
 

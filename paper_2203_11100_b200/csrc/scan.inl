@@ -177,7 +177,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     std::memcpy(stage + off_query, query, m);
     const uint32_t n_tiles = (m + pl.tile - 1) / pl.tile;
     uint32_t n_tiles_narrow = (m + kNarrowTile - 1) / kNarrowTile, narrow_tile = kNarrowTile;
-    bool narrow_staged = false;
+    bool narrow_staged = false, narrow_helpers = false;
     uint32_t n_units = 0;
     uint32_t pipe_first = n_groups;   // groups [pipe_first, n_groups) go through the on-chip pipeline
     uint32_t wave_sms = static_cast<uint32_t>(db->sm_count);   // SMs the wavefront kernel gets
@@ -201,6 +201,10 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         shape.s16 = pl.main == kMainS16;
         shape.policy = db->scan_policy;
         shape.pipe_rings = pipe_rings;
+        {
+            const size_t used = ((prof_elems + 127) & ~size_t(127)) + kWaveStaticSmem;
+            shape.narrow_room = used < db->smem_optin ? db->smem_optin - used : 0;
+        }
         const ScanPlan sp = plan_scan(shape, scan_knobs(), us, vso, modes);
         pipe_first = sp.pipe_first;
         wave_sms = sp.wave_sms;
@@ -211,6 +215,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         n_tiles_narrow = sp.n_tiles_narrow;
         narrow_tile = sp.narrow_tile;
         narrow_staged = sp.narrow_staged;
+        narrow_helpers = sp.narrow_helpers && sp.any_narrow;
         if (any_narrow && narrow_staged && sp.link_rows * 256 > db->nlinks_cap) {
             // link buffers of the narrow groups (256 B per row and tile boundary): every word holds kNarrowEmpty between
             // searches -- the consumers give them back
@@ -315,6 +320,8 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.narrow_tile = narrow_tile;
         wp.nlinks = db->d_nlinks;
         wp.narrow_staged = narrow_staged ? 1u : 0u;
+        wp.narrow_helpers = narrow_helpers ? 1u : 0u;
+        wp.narrow_stage_off = static_cast<uint32_t>((prof_elems + 127) & ~size_t(127));
         wp.prof8 = db->d_prof8;
         wp.pstride = pl.pstride;
         wp.n_tiles = n_tiles;
@@ -325,9 +332,10 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         wp.ticket = db->d_counters;
         wp.neg_open2 = pack16(-open);
         wp.neg_ext2 = pack16(-ext);
-        const uint32_t warps_per_cta = wave_threads / 32;
+        const uint32_t warps_per_cta = narrow_helpers ? 4 : wave_threads / 32;   // warps that take units
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(wave_sms, (n_units + warps_per_cta - 1) / warps_per_cta));
-        if ((st = launch_wavefront(db, wp, grid, wave_threads, prof_elems, any_narrow, any_rowblock, s)) != SWB_OK) return st;
+        const size_t wave_smem = narrow_helpers ? wp.narrow_stage_off + 4 * static_cast<size_t>(kNarrowPairBytes) : prof_elems;
+        if ((st = launch_wavefront(db, wp, grid, wave_threads, wave_smem, any_narrow, any_rowblock, s)) != SWB_OK) return st;
         if (n_pipe_items) {
             // the wavefront kernel's SMs are free now: let them help with whatever pipeline items are left
             pipeline_s16_kernel<kInterTile, kInterThreads><<<grid, kInterThreads, pipe_smem, s>>>(qp);

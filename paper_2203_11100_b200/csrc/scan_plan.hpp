@@ -53,6 +53,7 @@ enum GroupMode : uint8_t {
 constexpr int kNarrowTile = 8;          // columns of a narrow tile ...
 constexpr int kNarrowTileFine = 4;      // ... or of a fine one, for the most chain-bound searches
 constexpr uint32_t kNarrowChunkBytes = 8 * 32 * 8;   // a block of border rows in a narrow link buffer: 8 rows x 32 lanes x 8 B
+constexpr uint32_t kNarrowPairBytesHost = 2 * 4 * kNarrowChunkBytes + 64;   // = kNarrowPairBytes (kernels.cuh): a compute / helper pair's rings
 
 enum ScanPolicy : int { kScanAuto = 0, kScanPipeline = 1, kScanWavefront = 2 };   // = swb_scan_policy
 
@@ -85,6 +86,7 @@ struct ScanKnobs {
     double narrow_fine = 8.0;        // SWB200_NARROW_FINE: narrow tiles are 4 columns instead of 8 when the tallest group's rows exceed
                                      // this x a warp's fair share of the search (an 8-column chain, ~95 clk per row, would still be
                                      // about half the search)
+    bool narrow_helpers = true;      // SWB200_NARROW_HELPERS=0: narrow units without helper warps (link buffers read by the unit itself)
     double narrow_sms = 0.5;         // SWB200_NARROW_SMS: next to the pipeline, narrow units get a scheduler each (4 warps per SM) on at
                                      // most this fraction of the SMs
     uint64_t narrow_link_rows = 24u << 20; // SWB200_NARROW_LINKROWS: row slots (256 B each) of narrow link buffers at most (6 GiB)
@@ -119,6 +121,7 @@ struct ScanKnobs {
         k.wave_thin = num("SWB200_WAVE_THIN", k.wave_thin);
         k.wave_threads = static_cast<uint32_t>(num("SWB200_WAVE_THREADS", 0.0));
         k.narrow_fine = num("SWB200_NARROW_FINE", k.narrow_fine);
+        k.narrow_helpers = !off("SWB200_NARROW_HELPERS");
         k.narrow_sms = num("SWB200_NARROW_SMS", k.narrow_sms);
         k.narrow_link_rows = static_cast<uint64_t>(num("SWB200_NARROW_LINKROWS", static_cast<double>(k.narrow_link_rows)));
         k.duo_ratio = num("SWB200_DUO", k.duo_ratio);
@@ -142,6 +145,7 @@ struct ScanShape {
     bool s16 = true;                     // the packed int16 kernels scan (row blocks, narrow tiles, pipeline exist there only)
     int policy = kScanAuto;
     uint32_t pipe_rings = 0;             // chunks per ring that fit next to this query's profile (< 2: no pipeline)
+    size_t narrow_room = 0;              // shared memory left next to the profile for the helper warps' rings (wavefront kernel)
 };
 
 struct ScanPlan {
@@ -154,6 +158,7 @@ struct ScanPlan {
     uint32_t n_tiles_narrow = 0;          // ceil(m / narrow_tile)
     uint64_t link_rows = 0;    // row slots of the narrow groups' link buffers (vstate_off[g]: a narrow group's first one)
     bool narrow_staged = false;     // narrow units hand over through link buffers of their own (kernels.cuh: the data is the flag)
+    bool narrow_helpers = false;    // ... carried by helper warps through rings in shared memory (CTAs of 4 + 4 warps)
     bool any_narrow = false, any_rowblock = false, chain_bound = false;
     uint32_t n_split = 0, n_narrow = 0, n_rowblock = 0;   // groups per mode (the rest of [0, pipe_first) is single)
     uint64_t wave_rows = 0;    // padded rows of the wavefront kernel's groups
@@ -298,6 +303,12 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
         // with two): 4 warps per CTA, and SMs for the first round of units.  Where the chain is a smaller part of the
         // search (a whole Swiss-Prot on one GPU, m = 144: 5 x a warp's fair share) the SMs are worth more to the pipeline.
         pl.wave_threads = 128;   // = kNarrowThreads (kernels.cuh)
+        // ... and, where their rings fit next to the profile, a helper warp per unit on the same scheduler that carries its
+        // blocks between global and shared memory (4 + 4 warps per CTA): the unit itself then never waits for L2
+        if (k.narrow_helpers && in.narrow_room >= 4 * kNarrowPairBytesHost) {
+            pl.narrow_helpers = true;
+            pl.wave_threads = 256;
+        }
         const uint32_t want = (pl.n_units + 3) / 4;
         const uint32_t cap = std::max<uint32_t>(pl.wave_sms, static_cast<uint32_t>(k.narrow_sms * in.sm_count));
         pl.wave_sms = std::max(pl.wave_sms, std::min(want, cap));

@@ -511,7 +511,7 @@ def test_narrow_block_sweep_against_the_oracle():
                              text=True, timeout=900)
         assert out.returncode == 0 and "NARROW-SMALL-OK" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
         if extra:
-            assert "(4, 128, True)" in out.stdout, out.stdout[-1500:]     # 4-column tiles, CTAs of 4 warps, link buffers
+            assert "(4, 256, True)" in out.stdout, out.stdout[-1500:]     # 4-column tiles, CTAs of 4 + 4 warps (helpers), link buffers
 
 
 def test_large_random_batch_shares_scans_and_equals_single_searches(b62):

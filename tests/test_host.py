@@ -215,7 +215,7 @@ def test_scan_plan_narrow_forms(lib):
     # links: 256 B per row of every narrow group and tile boundary (18 tiles of 8 columns: 17 boundaries)
     assert whole["narrow_link_bytes"] % (256 * 17) == 0
     shard = search.scan_plan(lens, 144, shard_rank=0, shard_count=8)
-    assert shard["narrow_tile"] == 4 and shard["wavefront_threads"] == 128 and shard["narrow_link_bytes"] > 0
+    assert shard["narrow_tile"] == 4 and shard["wavefront_threads"] == 256 and shard["narrow_link_bytes"] > 0   # 4 + 4 helper warps
     assert shard["wavefront_units"] >= 36 * shard["narrow_groups"]                 # 36 tiles of 4 columns per narrow group
     assert 4 * shard["wavefront_sms"] >= min(shard["wavefront_units"], 4 * 74)     # a scheduler per unit, on at most half the SMs
     deep = search.scan_plan(lens, 3564, shard_rank=0, shard_count=8)

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(128, 1) narrow_kernel(WaveParams p, long long*
     NarrowWarp nw{consts};
     const GroupDesc gd = p.groups[0];
     const long long t0 = clock64();
-    const uint32_t best = sweep_unit_narrow_s16<T>(p, reinterpret_cast<const int8_t*>(smem_prof), gd, 0, 1, nullptr, threadIdx.x & 31, nw);
+    const uint32_t best = sweep_unit_narrow_s16<T, false>(p, reinterpret_cast<const int8_t*>(smem_prof), gd, 0, 1, nullptr, threadIdx.x & 31, nw);
     const long long t1 = clock64();
     if (best == 0x12345678u) p.slot_scores[0] = best;
     if ((threadIdx.x & 31) == 0) clocks[threadIdx.x >> 5] = t1 - t0;
@@ -163,10 +163,35 @@ __global__ void __launch_bounds__(128, 1) narrow_chain_kernel(WaveParams p, uint
     const GroupDesc gd = p.groups[0];
     const uint32_t tile = blockIdx.x;
     const long long t0 = clock64();
-    const uint32_t best = sweep_unit_narrow_s16<T>(p, reinterpret_cast<const int8_t*>(smem_prof), gd, tile, n_tiles, links, threadIdx.x & 31, nw);
+    const uint32_t best = sweep_unit_narrow_s16<T, false>(p, reinterpret_cast<const int8_t*>(smem_prof), gd, tile, n_tiles, links, threadIdx.x & 31, nw);
     const long long t1 = clock64();
     if (best == 0x12345678u) p.slot_scores[0] = best;
     if ((threadIdx.x & 31) == 0) clocks[blockIdx.x] = t1 - t0;
+}
+
+// The same chain with a helper warp per tile (warp 4, the compute warp's scheduler): rings in shared memory.
+template <int T>
+__global__ void __launch_bounds__(256, 1) narrow_helper_chain_kernel(WaveParams p, uint8_t* links, uint32_t n_tiles, long long* clocks) {
+    extern __shared__ __align__(128) uint8_t smem_prof[];
+    const uint32_t n16 = kProfRows * p.pstride / 16;
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) reinterpret_cast<uint4*>(smem_prof)[i] = reinterpret_cast<const uint4*>(p.prof8)[i];
+    __shared__ uint32_t consts[2];
+    if (threadIdx.x == 0) consts[0] = p.neg_open2, consts[1] = p.neg_ext2;
+    const uint32_t stage = smem_u32(smem_prof) + 4096;
+    for (uint32_t i = threadIdx.x; i < kNarrowPairBytes / 16; i += blockDim.x)
+        sts128v(stage + i * 16, make_uint4(kNarrowEmptyWord, kNarrowEmptyWord, kNarrowEmptyWord, kNarrowEmptyWord));
+    __syncthreads();
+    NarrowWarp nw{consts};
+    nw.in_ring = stage, nw.out_ring = stage + kNarrowRingSlots * kNarrowChunkBytes;
+    const GroupDesc gd = p.groups[0];
+    const uint32_t tile = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 4) narrow_helper_unit(links, gd.n_chunks, tile, n_tiles, lane, nw);
+    if (warp != 0) return;
+    const long long t0 = clock64();
+    const uint32_t best = sweep_unit_narrow_s16<T, true>(p, reinterpret_cast<const int8_t*>(smem_prof), gd, tile, n_tiles, links, lane, nw);
+    const long long t1 = clock64();
+    if (best == 0x12345678u) p.slot_scores[0] = best;
+    if (lane == 0) clocks[blockIdx.x] = t1 - t0;
 }
 
 __global__ void __launch_bounds__(512, 1) wide_kernel(WaveParams p, long long* clocks) {
@@ -298,6 +323,15 @@ int main() {
                 else narrow_chain_kernel<4><<<grid, 32, 120 << 10>>>(p, d_links, n_tiles, d_c);
                 cudaMemcpy(c, d_c, sizeof(c), cudaMemcpyDeviceToHost);
                 std::printf("chain of %2u narrow tiles (T=%d): clk per chunk of tile 0 %7.1f, tile 1 %7.1f, last tile %7.1f  %s\n", tiles, t == 0 ? 8 : 4,
+                            double(c[0]) / n_chunks, double(c[grid > 1 ? 1 : 0]) / n_chunks, double(c[grid - 1]) / n_chunks,
+                            cudaGetErrorString(cudaGetLastError()));
+                cudaMemset(d_links, 0x80, link_bytes);
+                cudaFuncSetAttribute(narrow_helper_chain_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 << 10);
+                cudaFuncSetAttribute(narrow_helper_chain_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 << 10);
+                if (t == 0) narrow_helper_chain_kernel<8><<<grid, 160, 120 << 10>>>(p, d_links, n_tiles, d_c);
+                else narrow_helper_chain_kernel<4><<<grid, 160, 120 << 10>>>(p, d_links, n_tiles, d_c);
+                cudaMemcpy(c, d_c, sizeof(c), cudaMemcpyDeviceToHost);
+                std::printf("   with helper warps             : clk per chunk of tile 0 %7.1f, tile 1 %7.1f, last tile %7.1f  %s\n",
                             double(c[0]) / n_chunks, double(c[grid > 1 ? 1 : 0]) / n_chunks, double(c[grid - 1]) / n_chunks,
                             cudaGetErrorString(cudaGetLastError()));
             }
