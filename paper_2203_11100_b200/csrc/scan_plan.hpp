@@ -67,6 +67,7 @@ struct ScanKnobs {
     double pipe_chain = 1.2;         // SWB200_PIPE_CHAIN: chain-bound when max_rows > this x a warp's fair share of the search
     double pipe_tall = 0.35;         // SWB200_PIPE_TALL: groups taller than this x a CTA's fair share of rows go to the wavefront kernel
     double wave_margin = 1.25;       // SWB200_PIPE_WAVE_MARGIN: wavefront SMs = its share of the rows x this ...
+    double wave_margin_near = 1.6;   // SWB200_PIPE_WAVE_MARGIN_NEAR: ... x this when the search is close to chain-bound ...
     double wave_margin_chain = 2.0;  // SWB200_PIPE_WAVE_MARGIN_CHAIN: ... or x this when chain-bound (its SMs are then
                                      // busy for the whole search whatever their number: +15 % at m = 375, -2 % at m = 1000)
     uint32_t pipe_ring_cap = 4;      // SWB200_PIPE_RING: chunks per shared-memory ring at most (power of two)
@@ -116,6 +117,7 @@ struct ScanKnobs {
         k.pipe_tall = num("SWB200_PIPE_TALL", k.pipe_tall);
         k.wave_margin = num("SWB200_PIPE_WAVE_MARGIN", k.wave_margin);
         k.wave_margin_chain = num("SWB200_PIPE_WAVE_MARGIN_CHAIN", k.wave_margin_chain);
+        k.wave_margin_near = num("SWB200_PIPE_WAVE_MARGIN_NEAR", k.wave_margin_near);
         k.pipe_ring_cap = std::max<uint32_t>(2, static_cast<uint32_t>(num("SWB200_PIPE_RING", k.pipe_ring_cap)));
         k.pipe_lag_div = std::max<uint32_t>(1, static_cast<uint32_t>(num("SWB200_PIPE_LAGDIV", k.pipe_lag_div)));
         k.wave_thin = num("SWB200_WAVE_THIN", k.wave_thin);
@@ -208,7 +210,11 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
             pl.wave_sms = 0;
         } else {
             const double share = static_cast<double>(rows_wave) / static_cast<double>(in.padded_rows);
-            const double margin = pl.chain_bound ? k.wave_margin_chain : k.wave_margin;
+            // chain-bound searches give the wavefront kernel twice its share; searches close to it (the tallest group's rows
+            // above 1.0 x a warp's fair share: long queries on a 1/8 shard) 1.6 x -- m = 5478 on 1/8 Swiss-Prot 29.7 -> 27.4 ms
+            // (long queries only: at 23 tiles, m = 729 on the whole database, the same ratio loses 2 % with the larger share)
+            const double near_chain = static_cast<double>(max_rows) > 1.0 * fair_all && n_tiles >= 64 ? k.wave_margin_near : k.wave_margin;
+            const double margin = pl.chain_bound ? k.wave_margin_chain : near_chain;
             pl.wave_sms = static_cast<uint32_t>(std::ceil(share * margin * in.sm_count));
             pl.wave_sms = std::max<uint32_t>(1, std::min<uint32_t>(pl.wave_sms, in.sm_count - 1));
         }
