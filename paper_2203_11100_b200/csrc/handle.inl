@@ -103,18 +103,22 @@ swb_status create_from(const SeqSource& src, uint64_t threshold, int32_t device,
         return fail(bad ? SWB_ERR_RANGE : SWB_ERR_INVALID, err);
     }
     DeviceGuard guard(device);
-    cudaDeviceProp prop{};
-    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    // three attributes, not cudaGetDeviceProperties: that call costs milliseconds, and the pair / batch entry points
+    // build a handle per call
+    int major = 0, sms = 0, smem_optin = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e != cudaSuccess) {
         delete db;
         return fail(SWB_ERR_CUDA, cudaGetErrorString(e));
     }
-    if (prop.major < 10) {
+    if (major < 10) {
         delete db;
         return fail(SWB_ERR_CUDA, "device is not sm_100-class; this library is built for sm_100a only");
     }
-    db->sm_count = prop.multiProcessorCount;
-    db->smem_optin = prop.sharedMemPerBlockOptin;
+    db->sm_count = sms;
+    db->smem_optin = static_cast<size_t>(smem_optin);
     swb_status st = init_handle_resources(db);
     if (st == SWB_OK) st = upload_db(db);
     if (st != SWB_OK) {

@@ -42,6 +42,17 @@ def test_no_cpu_fallback_without_gpu(lib):
         search.score_batch(A, [A], 4, synth.blosum62(), search.GapModel(10, 2))
 
 
+def test_device_key_entry_points_validate_before_cuda(lib):
+    """swb_search_keys_device / swb_db_merge_keys (the per-rank sharded search): a null handle or buffer is an argument
+    error with a message, never a crash and never a CUDA call."""
+    import ctypes as C
+    from paper_2203_11100_b200 import _cabi
+    hits = (_cabi.SwbHit * 4)()
+    n = C.c_uint32(7)
+    assert lib.swb_search_keys_device(None, None, 0, None, 10, 2, 4, None) != 0 and b"db is null" in lib.swb_last_error()
+    assert lib.swb_db_merge_keys(None, None, 0, 4, hits, C.byref(n), 0, None) != 0 and b"db is null" in lib.swb_last_error()
+
+
 def test_validation_before_cuda(lib, b62):
     A = enc("AAA")
     g = search.GapModel(10, 2)
