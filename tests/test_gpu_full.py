@@ -202,3 +202,33 @@ def test_sharded_full_database(full, b62):
     i2, s2, st = mdb.search(q, b62, GapModel(10, 2), 50)
     mdb.close()
     assert (i1 == i2).all() and (s1 == s2).all()
+
+
+def test_shard_of_eight_short_queries_against_the_oracle(lib, port, b62):
+    """One GPU's 1/8 share of the config-2 database (what BASELINE config 4 gives every rank at N = 8): the short queries
+    are chain-bound there and take the wavefront kernel's narrow units in their fastest form -- 4-column tiles, CTAs of
+    4 + 4 warps (helper warps carry the blocks), link buffers whose data is the flag -- next to the pipeline.  Score
+    vectors of the shard's sequences against the oracle on a seeded sample that includes every sequence of the tall
+    groups' head; repeated, because the link buffers must come back empty from every search."""
+    from paper_2203_11100_b200 import scan_plan, shard_assignment
+    queries, sdb = synth.config2()
+    lens = sdb.lengths()
+    mine = np.nonzero(shard_assignment(lens, 3000, 8) == 0)[0]
+    rng = np.random.default_rng(8)
+    longest = mine[np.argsort(lens[mine])[-80:]]
+    sample = np.unique(np.concatenate([rng.choice(mine, 1500, replace=False), longest]))
+    sub = po.FlatDb.from_list([sdb.seq(int(i)) for i in sample])
+    g = GapModel(10, 2)
+    with Database(sdb.codes, sdb.offsets, shard_rank=0, shard_count=8) as db:
+        for rep in range(2):
+            for qi in (0, 1, 2, 3):                                    # m = 144, 189, 222, 375
+                q = queries[qi]
+                plan = scan_plan(lens, len(q), shard_rank=0, shard_count=8)
+                assert plan["narrow_groups"] > 0 and plan["narrow_link_bytes"] > 0 and plan["pipeline_groups"] > 0
+                if qi == 0:
+                    assert plan["narrow_tile"] == 4 and plan["wavefront_threads"] == 256
+                got = np.full(sdb.n, -1, dtype=np.int32)
+                got, st = db.score_all(q, b62, g, out=got)
+                exp = port.score_all(q, sub, b62, 10, 2)
+                assert (got[sample] == exp).all(), f"m={len(q)} rep={rep}"
+                assert (got[mine] >= 0).all() and st["cells"] == len(q) * int(lens[mine].sum())
