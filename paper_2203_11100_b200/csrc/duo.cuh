@@ -24,22 +24,11 @@
 
 namespace swb {
 
-#ifndef SWB_DUO_LDS64
-#define SWB_DUO_LDS64 0
-#endif
-#if SWB_DUO_LDS64
-// Slice layout for 8-byte loads: [column pair 0..15][symbol 0..25] x 2 words.  A lane reads (pair, its residue) with one
-// LDS.64; a half-warp's 16 requests then fall on bank pair (10 pair + residue) mod 16, so only residues 16 apart collide
-// (20 common residues over 16 bank pairs: ~1.3 wavefronts per half-warp), against ~2.1 per quarter-warp for 16-byte loads
-// of [symbol][36 words] rows, where 20 residues share 8 bank groups: 42 instead of 67 wavefronts per row of 32 columns on
-// the LSU data pipe, which the 16-byte layout kept 92 % busy (profiles/r01k_ncu_duo_sweep_raw.csv).
-constexpr uint32_t kDuoPairSyms = 26;                             // 25 symbols + 1 filler: pair blocks 208 B apart
-constexpr uint32_t kDuoSliceWords = (kInterTile / 2) * kDuoPairSyms * 2;   // 832 words
-__host__ __device__ constexpr uint32_t duo_slice_word(uint32_t s, uint32_t c) { return ((c >> 1) * kDuoPairSyms + s) * 2 + (c & 1); }
-#else
+// (An 8-byte layout, [column pair][symbol] x 2 words read with LDS.64, was built and measured: 42 instead of 67 shared-memory
+// wavefronts per row of 32 columns, bit-exact, and 3 % slower -- 7,239 against 7,455 GCUPS on the sweep: the 8 extra issue
+// slots per row cost more than the wavefronts saved; profiles/r02_summary.md.)
 constexpr uint32_t kDuoRowWords = kInterTile + 4;                 // 36 words = 144 B: rows 16 B apart modulo 128
 constexpr uint32_t kDuoSliceWords = kProfRows * kDuoRowWords;     // one tile's profile slice: 900 words
-#endif
 constexpr uint32_t kDuoSliceBytes = (kDuoSliceWords * 4 + 255) & ~255u;
 
 constexpr uint32_t kDuoNone = 0xFFFFFFFFu;
@@ -68,11 +57,7 @@ __global__ void build_duo_profile_kernel(DuoProfileParams p) {
     const uint32_t total = p.n_tiles * kDuoSliceWords;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const uint32_t tile = i / kDuoSliceWords, rem = i % kDuoSliceWords;
-#if SWB_DUO_LDS64
-        const uint32_t s = (rem >> 1) % kDuoPairSyms, c = ((rem >> 1) / kDuoPairSyms) * 2 + (rem & 1);
-#else
         const uint32_t s = rem / kDuoRowWords, c = rem % kDuoRowWords;
-#endif
         const DuoTile td = p.tiles[tile];
         int32_t va = p.shift, vb = p.shift;
         if (s < kAlphabet && c < kInterTile) {
@@ -258,13 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
             for (int rp = 0; rp < static_cast<int>(kRowsPerChunk); rp += 2) {
                 const uint32_t aA = ((rp < 4 ? r_lo : r_hi) >> (8 * (rp & 3))) & 0xffu;
                 const uint32_t aB = ((rp + 1 < 4 ? r_lo : r_hi) >> (8 * ((rp + 1) & 3))) & 0xffu;
-#if SWB_DUO_LDS64
-                const uint2* prowA = reinterpret_cast<const uint2*>(slice) + aA;   // pair block p: + p * kDuoPairSyms
-                const uint2* prowB = reinterpret_cast<const uint2*>(slice) + aB;
-#else
                 const uint4* prowA = reinterpret_cast<const uint4*>(slice + aA * kDuoRowWords);
                 const uint4* prowB = reinterpret_cast<const uint4*>(slice + aB * kDuoRowWords);
-#endif
                 uint2 biA = make_uint2(NO, NO), biB = make_uint2(NO, NO);
                 if (!first) {
                     biA = bin[rp * 32], biB = bin[(rp + 1) * 32];
@@ -272,53 +252,6 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
                     biB.x = (biB.x & keep) | edge, biB.y = (biB.y & keep) | edge;
                 }
                 uint32_t hlA = biA.x, EA = biA.y, hlB = biB.x, EB = biB.y;
-#if SWB_DUO_LDS64
-                uint2 swA = prowA[0], swB = prowB[0];
-                uint32_t dA = __vadd2(diag_in, swA.x);   // (row A, column 0): diagonal = the previous row's inbound Hm
-                uint32_t dB = __vadd2(hlA, swB.x);       // (row B, column 0): diagonal = row A's inbound Hm
-                diag_in = hlB;
-                uint32_t seenA = 0;
-#pragma unroll
-                for (int k = 0; k <= T; ++k) {
-                    // row A, column k
-                    if (k < T) {
-                        EA = __viaddmax_s16x2(EA, NE, hlA);
-                        F[k] = __viaddmax_s16x2(F[k], NE, Hm[k]);
-                        const uint32_t dcur = dA;
-                        if (k & 1) {                       // column k + 1 opens the next pair
-                            if (k + 1 < T) {
-                                swA = prowA[((k + 1) / 2) * kDuoPairSyms];
-                                dA = __vadd2(Hm[k], swA.x);
-                            }
-                        } else {
-                            dA = __vadd2(Hm[k], swA.y);
-                        }
-                        hlA = __vadd2(__vimax3_s16x2_relu(dcur, EA, F[k]), NO);
-                        Hm[k] = hlA;
-                        if (k == 0) best = __vmaxs2(best, dcur);
-                        else seenA = dcur;
-                    }
-                    // row B, column k - 1
-                    if (k >= 1) {
-                        const int c = k - 1;
-                        EB = __viaddmax_s16x2(EB, NE, hlB);
-                        F[c] = __viaddmax_s16x2(F[c], NE, Hm[c]);
-                        const uint32_t dcur = dB;
-                        if (c & 1) {
-                            if (c + 1 < T) {
-                                swB = prowB[((c + 1) / 2) * kDuoPairSyms];
-                                dB = __vadd2(Hm[c], swB.x);
-                            }
-                        } else {
-                            dB = __vadd2(Hm[c], swB.y);
-                        }
-                        hlB = __vadd2(__vimax3_s16x2_relu(dcur, EB, F[c]), NO);
-                        Hm[c] = hlB;
-                        // the running maximum over the diagonal terms (exact, see sweep_unit_s16): one VIMNMX3 per two cells
-                        best = k < T ? __vimax3_s16x2(best, seenA, dcur) : __vmaxs2(best, dcur);
-                    }
-                }
-#else
                 uint4 swA = prowA[0], swB = prowB[0];
                 uint32_t dA = __vadd2(diag_in, swA.x);   // (row A, column 0): diagonal = the previous row's inbound Hm
                 uint32_t dB = __vadd2(hlA, swB.x);       // (row B, column 0): diagonal = row A's inbound Hm
@@ -366,7 +299,6 @@ __global__ void __launch_bounds__(kThreads, 1) duo_pipeline_kernel(DuoParams p) 
                         best = k < T ? __vimax3_s16x2(best, seenA, dcur) : __vmaxs2(best, dcur);
                     }
                 }
-#endif
                 if (!last) {
                     *reinterpret_cast<uint2*>(bout + rp * 256) = make_uint2(hlA, EA);
                     *reinterpret_cast<uint2*>(bout + (rp + 1) * 256) = make_uint2(hlB, EB);
