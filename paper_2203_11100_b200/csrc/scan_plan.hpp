@@ -66,7 +66,7 @@ struct ScanKnobs {
     uint32_t pipe_min_tiles = 9;     // SWB200_PIPE_MINTILES: fewer tiles -> wavefront kernel only, unless chain-bound
     double pipe_chain = 1.2;         // SWB200_PIPE_CHAIN: chain-bound when max_rows > this x a warp's fair share of the search
     double pipe_tall = 0.35;         // SWB200_PIPE_TALL: groups taller than this x a CTA's fair share of rows go to the wavefront kernel
-    double pipe_tall_small = 0.6;    // SWB200_PIPE_TALL_SMALL: ... x this on databases of fewer than 40 groups per SM (shards)
+    double pipe_tall_small = 0.6;    // SWB200_PIPE_TALL_SMALL: ... x this on databases of fewer than 32 groups per SM (shards)
     double wave_margin = 1.25;       // SWB200_PIPE_WAVE_MARGIN: wavefront SMs = its share of the rows x this ...
     double wave_margin_near = 1.6;   // SWB200_PIPE_WAVE_MARGIN_NEAR: ... x this when the search is close to chain-bound ...
     double wave_margin_chain = 2.0;  // SWB200_PIPE_WAVE_MARGIN_CHAIN: ... or x this when chain-bound (its SMs are then
@@ -203,8 +203,8 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
                n_groups >= 2 * in.sm_count) {
         const uint64_t fair_cta = in.padded_rows / in.sm_count;   // rows per CTA
         // (a smaller shard has fewer groups per CTA to balance with, but its wavefront share grows with every group that is
-        // called tall: 0.6 of a CTA's share below 40 groups per SM -- 1/8 Swiss-Prot, m = 3564: 18.1 -> 16.9 ms)
-        const double tall_fraction = n_groups < 40 * in.sm_count ? k.pipe_tall_small : k.pipe_tall;
+        // called tall: 0.6 of a CTA's share below 32 groups per SM -- 1/8 Swiss-Prot, m = 3564: 18.1 -> 16.9 ms)
+        const double tall_fraction = n_groups < 32 * in.sm_count ? k.pipe_tall_small : k.pipe_tall;
         const uint64_t tall = std::max<uint64_t>(256, static_cast<uint64_t>(tall_fraction * static_cast<double>(fair_cta)));
         uint32_t g = 0;
         uint64_t rows_wave = 0;
