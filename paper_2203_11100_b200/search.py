@@ -43,6 +43,9 @@ def _ptr(arr, typ):
     return arr.ctypes.data_as(typ)
 
 
+_HIT_DTYPE = np.dtype([("db_index", np.uint32), ("score", np.int32)])   # = swb_hit (include/swb200.h)
+
+
 @dataclass
 class SearchConfig:
     """scheduler.hpp:20-36.  worker_count / lane_width / chunk_width / cpu_pool_threads are
@@ -153,15 +156,13 @@ class Database:
     def search(self, query, matrix, gaps: GapModel, top_k: int = 10):
         """-> (db_index[uint32], score[int32], stats dict), at most top_k hits, final order."""
         q, mat = _u8(query), _mat(matrix)
-        hits = (_cabi.SwbHit * max(1, top_k))()
+        hits = np.empty(max(1, top_k), dtype=_HIT_DTYPE)      # swb_hit records: (db_index, score)
         n = C.c_uint32(0)
         st = _cabi.SwbStats()
         rc = self._lib.swb_search(self._h, _ptr(q, _u8p), len(q), _ptr(mat, _i32p), gaps.open, gaps.extend,
-                                  top_k, hits, C.byref(n), C.byref(st))
+                                  top_k, hits.ctypes.data_as(C.POINTER(_cabi.SwbHit)), C.byref(n), C.byref(st))
         _raise(self._lib, rc)
-        idx = np.array([hits[i].db_index for i in range(n.value)], dtype=np.uint32)
-        sc = np.array([hits[i].score for i in range(n.value)], dtype=np.int32)
-        return idx, sc, st.as_dict()
+        return hits["db_index"][:n.value].copy(), hits["score"][:n.value].copy(), st.as_dict()
 
     def search_many(self, queries, matrix, gaps: GapModel, top_k: int = 10):
         """Pipelined searches (swb_search_many): -> list of (db_index, score) per query, and the per-query device ms."""
