@@ -148,7 +148,13 @@ swb_status mdb_build(const SeqSource& src, uint64_t threshold, const int32_t* de
             return fail(st, msg);
         }
 
-    if (n_devices > 1 && mdb->distinct) {
+    // SWB200_FORCE_NCCL=1: a communicator even for one device, so that the NCCL branch (dlopen, ncclCommInitAll, the grouped
+    // all-gather on the shards' streams) can be exercised on a box with a single GPU
+    static const bool force_nccl = [] {
+        const char* e = std::getenv("SWB200_FORCE_NCCL");
+        return e && *e == '1';
+    }();
+    if ((n_devices > 1 || force_nccl) && mdb->distinct) {
         std::string why;
         if (!mdb->nccl.load(&why)) {
             swb_mdb_destroy(mdb);
@@ -356,7 +362,8 @@ swb_status swb_mdb_search(swb_mdb* mdb, const uint8_t* query, uint32_t query_len
     if (!hits || !n_hits) return fail(SWB_ERR_INVALID, "hits/n_hits are null");
     if (top_k < 1) return fail(SWB_ERR_INVALID, "top_k must be >= 1");
     const size_t G = mdb->shards.size();
-    if (G == 1) return swb_search(mdb->shards[0], query, query_len, matrix, gap_open, gap_extend, top_k, hits, n_hits, stats);
+    if (G == 1 && mdb->comms.empty())
+        return swb_search(mdb->shards[0], query, query_len, matrix, gap_open, gap_extend, top_k, hits, n_hits, stats);
     swb_status st = check_scoring_args(query, query_len, matrix, gap_open, gap_extend);
     if (st != SWB_OK) return st;
 

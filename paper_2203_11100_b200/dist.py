@@ -79,7 +79,7 @@ class ShardedSearch:
         self.db.set_stream(stream.cuda_stream)
         send, recv = self._buffers(top_k)
         self.db.search_keys_device(query, matrix, gaps, top_k, send.data_ptr())
-        if self.world > 1:
+        if dist.is_initialized():     # also with world = 1: the same collective on the same stream
             dist.all_gather_into_tensor(recv, send, group=self.group)
         else:
             recv = send

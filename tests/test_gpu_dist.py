@@ -71,3 +71,29 @@ def test_device_keys_of_shards_merge_to_the_single_list(lib, b62):
         ref_i, ref_s, _ = db.search(qs[0][:40], b62, g, 8)
         assert len(idx) == 3 and (idx == ref_i).all() and (sc == ref_s).all()
         assert (buf[3:].cpu().numpy() == 0).all()
+
+
+def test_nccl_all_gather_on_the_search_stream_world1(lib):
+    """The NCCL flavour of the per-rank path as far as one GPU can run it: process group "nccl" with one rank, the search
+    enqueued on torch's current stream, all_gather_into_tensor on the tensor the library filled, the global select on the
+    gathered tensor (tests/_nccl_world1.py, in a process of its own because it owns a process group)."""
+    import os, socket, subprocess, sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port_no = s.getsockname()[1]
+    s.close()
+    out = subprocess.run([sys.executable, str(root / "tests" / "_nccl_world1.py"), str(port_no)], cwd=root, capture_output=True, text=True,
+                         timeout=600, env=dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no)))
+    assert out.returncode == 0 and "NCCL-WORLD1-OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
+
+
+def test_in_process_nccl_branch_on_one_gpu(lib):
+    """swb_mdb_search's NCCL branch (dlopen of libnccl, ncclCommInitAll, grouped ncclAllGather on the shard's stream, device
+    select) with a communicator of one device: tests/_nccl_inprocess.py under SWB200_FORCE_NCCL=1."""
+    import subprocess, sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    out = subprocess.run([sys.executable, str(root / "tests" / "_nccl_inprocess.py")], cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "NCCL-INPROCESS-OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
