@@ -122,6 +122,21 @@ swb_status swb_score_pair(const uint8_t* query, uint32_t query_len, const uint8_
     return SWB_OK;
 }
 
+// Direction matrices of all hits of one call live on the device at once: memory_cap bounds each pair (align.hpp:262-267), this
+// bounds their sum -- beyond it the hits are traced back in several rounds (large top_k with long query and subjects).
+static uint64_t traceback_round_bytes() {   // SWB200_TRACEBACK_ROUND_KB (tests: a tiny value forces several rounds)
+    static const uint64_t bytes = [] {
+        const char* e = std::getenv("SWB200_TRACEBACK_ROUND_KB");
+        const long long kb = e ? std::atoll(e) : 0;
+        return kb > 0 ? static_cast<uint64_t>(kb) << 10 : 6ull << 30;
+    }();
+    return bytes;
+}
+
+static swb_status align_hits_locked(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix, int32_t gap_open,
+                                    int32_t gap_extend, const swb_hit* hits, uint32_t n_hits, uint64_t memory_cap, swb_alignment* out,
+                                    uint8_t* ops, const uint64_t* ops_offset);
+
 swb_status swb_db_align_hits(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix,
                              int32_t gap_open, int32_t gap_extend, const swb_hit* hits, uint32_t n_hits,
                              uint64_t memory_cap, swb_alignment* out, uint8_t* ops, const uint64_t* ops_offset) {
@@ -131,6 +146,13 @@ swb_status swb_db_align_hits(swb_db* db, const uint8_t* query, uint32_t query_le
     if (st != SWB_OK) return st;
     std::lock_guard<std::mutex> lock(db->mu);
     DeviceGuard guard(db->device);
+    return align_hits_locked(db, query, query_len, matrix, gap_open, gap_extend, hits, n_hits, memory_cap, out, ops, ops_offset);
+}
+
+static swb_status align_hits_locked(swb_db* db, const uint8_t* query, uint32_t query_len, const int32_t* matrix, int32_t gap_open,
+                                    int32_t gap_extend, const swb_hit* hits, uint32_t n_hits, uint64_t memory_cap, swb_alignment* out,
+                                    uint8_t* ops, const uint64_t* ops_offset) {
+    swb_status st = SWB_OK;
     cudaStream_t s = db->stream;
 
     if (db->slot_of.empty() && db->meta.n_total) {      // db_index -> slot, built on first use
@@ -174,6 +196,14 @@ swb_status swb_db_align_hits(swb_db* db, const uint8_t* query, uint32_t query_le
         job_hit.push_back(i);
     }
     if (jobs.empty()) return SWB_OK;
+    if (dir_bytes > traceback_round_bytes() && n_hits > 1) {
+        // too much for one round: the two halves of the hit list one after the other (ops_offset holds absolute offsets)
+        const uint32_t half = n_hits / 2;
+        st = align_hits_locked(db, query, query_len, matrix, gap_open, gap_extend, hits, half, memory_cap, out, ops, ops_offset);
+        if (st != SWB_OK) return st;
+        return align_hits_locked(db, query, query_len, matrix, gap_open, gap_extend, hits + half, n_hits - half, memory_cap, out + half, ops,
+                                 ops_offset + half);
+    }
 
     const QueryPlan pl = make_plan(db, query_len, matrix, gap_open, gap_extend);
     const uint32_t n_lane_tiles = (query_len + 7) / 8;

@@ -558,3 +558,14 @@ def test_search_many_edge_cases(port, b62):
         for q, (idx, sc) in zip([q1[:80], q2[:90]], out):
             ei, es, _ = port.run_search(q, fdb, wide, 400, 80, top_k=6)
             assert (idx == ei).all() and (sc == es).all()
+
+
+def test_traceback_in_several_rounds():
+    """The direction matrices of a call's hits are bounded in sum (pairs.inl): with SWB200_TRACEBACK_ROUND_KB=64 the twelve
+    hits of test_batched_traceback_of_search_hits are traced back in several rounds and must give the same edit scripts."""
+    import os, subprocess, sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    out = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-q", "-x", "-k", "traceback and not several_rounds"], cwd=root,
+                         env=dict(os.environ, SWB200_TRACEBACK_ROUND_KB="64"), capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and " passed" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
