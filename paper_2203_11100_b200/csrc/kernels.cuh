@@ -812,7 +812,9 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
             bool narrow_done = false;
             if constexpr (kNarrow) {
                 if (mode == kGroupNarrow) {
-                    if (p.narrow_staged && helpers) {
+                    // (the link-buffer forms are only compiled where the host can choose them: profile in shared memory, and the
+                    // helper form only into the build for CTAs of 4 + 4 warps -- each form is eight instantiations of the sweep)
+                    if (kSmemProfile && kThreads == 2 * kNarrowThreads && p.narrow_staged && helpers) {
                         // tell the helper warp what to carry (once it is done with the unit before), then sweep on the rings
                         uint8_t* links = p.nlinks + static_cast<size_t>(p.vstate_off[g]) * 256;
                         while (lds32v(nw.mailbox + 4) != nw.posted) __nanosleep(40);
@@ -826,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) wavefront_s16_kernel(WaveParams p
                         }
                         best = p.narrow_tile == 4 ? sweep_unit_narrow_s16<4, true>(p, prof, gd, t0, n_tiles, links, lane, nw)
                                                   : sweep_unit_narrow_s16<8, true>(p, prof, gd, t0, n_tiles, links, lane, nw);
-                    } else if (p.narrow_staged) {
+                    } else if (kSmemProfile && p.narrow_staged) {
                         uint8_t* links = p.nlinks + static_cast<size_t>(p.vstate_off[g]) * 256;
                         best = p.narrow_tile == 4 ? sweep_unit_narrow_s16<4, false>(p, prof, gd, t0, n_tiles, links, lane, nw)
                                                   : sweep_unit_narrow_s16<8, false>(p, prof, gd, t0, n_tiles, links, lane, nw);

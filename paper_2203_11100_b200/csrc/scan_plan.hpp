@@ -188,11 +188,12 @@ inline ScanPlan plan_scan(const ScanShape& in, const ScanKnobs& k, uint32_t* uni
     // keep the classic hand-over through the border arrays and progress counters.
     pl.narrow_tile = static_cast<double>(max_rows) > k.narrow_fine * fair_all ? kNarrowTileFine : kNarrowTile;
     pl.n_tiles_narrow = (in.query_len + pl.narrow_tile - 1) / pl.narrow_tile;
-    pl.narrow_staged = max_rows / kRowsPerChunk >= 32ull * pl.n_tiles_narrow;
+    // (narrow_room > 0: the profile is in shared memory -- the kernel builds for a profile in global memory carry the classic form only)
+    pl.narrow_staged = in.narrow_room > 0 && max_rows / kRowsPerChunk >= 32ull * pl.n_tiles_narrow;
     if (!pl.narrow_staged && pl.narrow_tile != kNarrowTile) {
         pl.narrow_tile = kNarrowTile;
         pl.n_tiles_narrow = (in.query_len + pl.narrow_tile - 1) / pl.narrow_tile;
-        pl.narrow_staged = max_rows / kRowsPerChunk >= 32ull * pl.n_tiles_narrow;
+        pl.narrow_staged = in.narrow_room > 0 && max_rows / kRowsPerChunk >= 32ull * pl.n_tiles_narrow;
     }
     const bool can_pipe = in.s16 && in.pipe_rings >= 2 && n_groups > 0;
     if (can_pipe && in.policy == kScanPipeline) {
