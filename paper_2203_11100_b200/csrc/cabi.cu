@@ -36,6 +36,7 @@
 #include <new>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/swb200.h"
@@ -67,11 +68,130 @@ swb_status fail(swb_status st, const std::string& msg) {
             return fail(SWB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__));      \
     } while (0)
 
+// ---- block cache of the ad-hoc entry points ------------------------------------------------------------------------
+// swb_score_pair / swb_score_batch / swb_align_traceback / swb_merge_keys build a handle per call (the reference's
+// sw_score_scalar, sw_score_batch, sw_align_traceback take plain sequences, align.hpp:42,91,166,262): some thirty
+// cudaMalloc / cudaFree and three cudaMallocHost per call cost milliseconds, the kernels microseconds.  While such a call
+// runs (BlockCacheScope on its thread) device and pinned blocks up to kCacheBlockMax come out of size classes (powers of two)
+// kept per device and go back there instead of to the driver, up to kCacheBytesMax per device.  Handles of resident
+// databases (swb_db_create & co.) do not use it.  A block is only handed back after the device went idle (release_block
+// synchronises unless the caller just did), so reuse needs no stream ordering.
+constexpr size_t kCacheBlockMax = 8u << 20;
+constexpr size_t kCacheBytesMax = 256u << 20;
+
+struct BlockCache {
+    struct Class {
+        std::vector<void*> dev, host;
+    };
+    std::mutex mu;
+    std::unordered_map<void*, uint32_t> owned;          // block -> (device << 8) | (host ? 0x80 : 0) | log2(size)
+    std::unordered_map<uint32_t, Class> classes;        // (device << 8) | log2(size)
+    std::unordered_map<int, size_t> cached_bytes;       // per device, blocks lying in `classes`
+};
+
+BlockCache& block_cache() {   // leaked on purpose: no CUDA call from a static destructor
+    static BlockCache* c = new BlockCache();
+    return *c;
+}
+
+thread_local int t_cache_scope = 0;
+
+struct BlockCacheScope {
+    BlockCacheScope() { ++t_cache_scope; }
+    ~BlockCacheScope() { --t_cache_scope; }
+    BlockCacheScope(const BlockCacheScope&) = delete;
+    BlockCacheScope& operator=(const BlockCacheScope&) = delete;
+};
+
+inline uint32_t size_class(size_t bytes) {
+    uint32_t lg = 9;   // 512 B: the smallest class
+    while ((size_t(1) << lg) < bytes) ++lg;
+    return lg;
+}
+
+// nullptr: not served from the cache (scope not active, block too large, nothing cached and the driver refused)
+void* cached_block(size_t bytes, bool host) {
+    static const bool off = std::getenv("SWB200_NO_BLOCK_CACHE") != nullptr;   // measurement: every block from the driver
+    if (!t_cache_scope || off || bytes > kCacheBlockMax) return nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    const uint32_t lg = size_class(bytes);
+    const uint32_t key = (static_cast<uint32_t>(dev) << 8) | lg;
+    BlockCache& c = block_cache();
+    {
+        std::lock_guard<std::mutex> lock(c.mu);
+        auto it = c.classes.find(key);
+        if (it != c.classes.end()) {
+            auto& list = host ? it->second.host : it->second.dev;
+            if (!list.empty()) {
+                void* p = list.back();
+                list.pop_back();
+                c.cached_bytes[dev] -= size_t(1) << lg;
+                return p;
+            }
+        }
+    }
+    void* p = nullptr;
+    const cudaError_t e = host ? cudaMallocHost(&p, size_t(1) << lg) : cudaMalloc(&p, size_t(1) << lg);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lock(c.mu);
+    c.owned[p] = key | (host ? 0x80u : 0u);
+    return p;
+}
+
+// Blocks of the cache go back to their class, others to the driver.  idle: the caller has synchronised every stream that
+// touched the block (cudaFree would have waited for the device by itself).
+void release_block(void* p, bool host, bool idle = false) {
+    if (!p) return;
+    BlockCache& c = block_cache();
+    uint32_t tag = 0;
+    bool ours = false;
+    {
+        std::lock_guard<std::mutex> lock(c.mu);
+        auto it = c.owned.find(p);
+        if (it != c.owned.end()) ours = true, tag = it->second;
+    }
+    if (!ours) {
+        if (host) cudaFreeHost(p);
+        else cudaFree(p);
+        return;
+    }
+    if (!idle) cudaDeviceSynchronize();
+    const int dev = static_cast<int>(tag >> 8);
+    const size_t bytes = size_t(1) << (tag & 0x7fu);
+    {
+        std::lock_guard<std::mutex> lock(c.mu);
+        size_t& cached = c.cached_bytes[dev];
+        if (cached + bytes <= kCacheBytesMax) {
+            auto& cl = c.classes[tag & ~0x80u];
+            (host ? cl.host : cl.dev).push_back(p);
+            cached += bytes;
+            return;
+        }
+        c.owned.erase(p);
+    }
+    if (host) cudaFreeHost(p);
+    else cudaFree(p);
+}
+
+inline void dev_free(void* p, bool idle = false) { release_block(p, false, idle); }
+inline void host_free(void* p, bool idle = false) { release_block(p, true, idle); }
+
+swb_status host_alloc(void** ptr, size_t bytes) {
+    if ((*ptr = cached_block(bytes, true)) != nullptr) return SWB_OK;
+    SWB_CUDA(cudaMallocHost(ptr, bytes));
+    return SWB_OK;
+}
+
 template <class T>
 swb_status dev_alloc(T** ptr, size_t count, uint64_t* tally) {
     *ptr = nullptr;
     const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
-    SWB_CUDA(cudaMalloc(reinterpret_cast<void**>(ptr), bytes));
+    if ((*ptr = static_cast<T*>(cached_block(bytes, false))) == nullptr)
+        SWB_CUDA(cudaMalloc(reinterpret_cast<void**>(ptr), bytes));
     if (tally) *tally += bytes;
     return SWB_OK;
 }
@@ -197,11 +317,12 @@ struct DeviceGuard {
 
 swb_status ensure_stage(swb_db* db, size_t bytes) {
     if (bytes <= db->stage_cap) return SWB_OK;
-    if (db->h_stage) cudaFreeHost(db->h_stage);
+    if (db->h_stage) host_free(db->h_stage);
     db->h_stage = nullptr;
     db->stage_cap = 0;
     const size_t cap = std::max<size_t>(bytes * 2, 1 << 16);
-    SWB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&db->h_stage), cap));
+    swb_status st = host_alloc(reinterpret_cast<void**>(&db->h_stage), cap);
+    if (st != SWB_OK) return st;
     db->stage_cap = cap;
     return SWB_OK;
 }
@@ -210,7 +331,7 @@ template <class T>
 swb_status ensure_dev(T** ptr, size_t* cap, size_t need, uint64_t* tally) {
     if (need <= *cap) return SWB_OK;
     if (*ptr) {
-        cudaFree(*ptr);
+        dev_free(*ptr);
         *tally -= *cap * sizeof(T);
     }
     *ptr = nullptr;
@@ -299,11 +420,12 @@ void swb_db_destroy(swb_db* db) {
                         db->d_counters,   db->d_unit_start, db->d_group_mode, db->d_vstate_off, db->d_vstate, db->d_progress, db->d_nlinks, db->d_keys,        db->d_sel[0],
                         db->d_sel[1],     db->d_sort,     db->d_all_scores, db->d_query,       db->d_matrix,
                         db->d_prof8,      db->d_prof8i,   db->d_prof32i};
+        // (both streams are idle: blocks of the ad-hoc entry points' cache can go straight back to it)
         for (void* p : ptrs)
-            if (p) cudaFree(p);
-        if (db->h_stage) cudaFreeHost(db->h_stage);
-        if (db->h_counters) cudaFreeHost(db->h_counters);
-        if (db->h_merge) cudaFreeHost(db->h_merge);
+            if (p) dev_free(p, true);
+        host_free(db->h_stage, true);
+        host_free(db->h_counters, true);
+        host_free(db->h_merge, true);
         for (auto& ev : db->ev)
             if (ev) cudaEventDestroy(ev);
         for (auto& ev : db->many_events) cudaEventDestroy(ev);
@@ -421,9 +543,10 @@ swb_status swb_db_merge_keys(swb_db* db, const uint64_t* device_keys, uint64_t n
     const uint32_t k_eff = static_cast<uint32_t>(std::min<uint64_t>(top_k, n));
     // the keys come down next to, not over, the pending search's inputs: a second pinned buffer of their own
     if (k_eff > db->merge_cap) {
-        if (db->h_merge) cudaFreeHost(db->h_merge);
+        host_free(db->h_merge);
         db->h_merge = nullptr, db->merge_cap = 0;
-        SWB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&db->h_merge), static_cast<size_t>(k_eff) * 2 * sizeof(uint64_t)));
+        swb_status hst = host_alloc(reinterpret_cast<void**>(&db->h_merge), static_cast<size_t>(k_eff) * 2 * sizeof(uint64_t));
+        if (hst != SWB_OK) return hst;
         db->merge_cap = k_eff * 2;
     }
     if (k_eff) {

@@ -80,7 +80,7 @@ swb_status init_handle_resources(swb_db* db) {
         return fail(SWB_ERR_CUDA, "cudaEventCreate failed");
     for (auto& ev : db->ev)
         if (cudaEventCreate(&ev) != cudaSuccess) return fail(SWB_ERR_CUDA, "cudaEventCreate failed");
-    if (cudaMallocHost(reinterpret_cast<void**>(&db->h_counters), 4 * sizeof(uint32_t)) != cudaSuccess)
+    if (host_alloc(reinterpret_cast<void**>(&db->h_counters), 4 * sizeof(uint32_t)) != SWB_OK)
         return fail(SWB_ERR_CUDA, "cudaMallocHost failed");
     std::memset(db->h_counters, 0, 4 * sizeof(uint32_t));
     return SWB_OK;

@@ -13,6 +13,7 @@ swb_status swb_merge_keys(const uint64_t* keys, uint64_t n, int32_t keys_on_devi
         return fail(SWB_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
     if (device < 0 || device >= ndev) return fail(SWB_ERR_INVALID, "device index out of range");
     DeviceGuard guard(device);
+    BlockCacheScope cache;
     // a scratch handle gives select_topk its buffers and stream
     swb_db tmp;
     tmp.device = device;
@@ -41,10 +42,10 @@ swb_status swb_merge_keys(const uint64_t* keys, uint64_t n, int32_t keys_on_devi
             break;
         }
     } while (false);
-    if (d_in) cudaFree(d_in);
-    for (auto& p : tmp.d_sel)
-        if (p) cudaFree(p);
-    if (tmp.d_sort) cudaFree(tmp.d_sort);
+    cudaStreamSynchronize(tmp.own_stream);
+    dev_free(d_in, true);
+    for (auto& p : tmp.d_sel) dev_free(p, true);
+    dev_free(tmp.d_sort, true);
     cudaStreamDestroy(tmp.own_stream);
     tmp.own_stream = nullptr;
     if (st != SWB_OK) return st;
@@ -79,6 +80,7 @@ swb_status swb_score_batch(const uint8_t* query, uint32_t query_len, const uint8
         ls[i] = subjects[i] ? lens[i] : 0;
     }
     if (count == 0 || query_len == 0) return SWB_OK;
+    BlockCacheScope cache;
     swb_db* db = nullptr;
     // threshold = infinity: every lane goes through the inter-task kernel, whatever its length
     st = swb_db_create(ptrs.data(), ls.data(), count, ~0ull, device, 0, 1, &db);
@@ -104,6 +106,7 @@ swb_status swb_score_pair(const uint8_t* query, uint32_t query_len, const uint8_
     if (st != SWB_OK) return st;
     *score = 0;
     if (query_len == 0 || subject_len == 0) return SWB_OK;
+    BlockCacheScope cache;
     swb_db* db = nullptr;
     const uint8_t* ptrs[1] = {subject};
     const uint32_t ls[1] = {subject_len};
@@ -271,10 +274,11 @@ static swb_status align_hits_locked(swb_db* db, const uint8_t* query, uint32_t q
         SWB_CUDA(cudaGetLastError());
         return SWB_OK;
     }();
+    cudaStreamSynchronize(s);   // (after an error the stream may still be busy with these blocks)
     for (void* ptr : {static_cast<void*>(d_dir), static_cast<void*>(d_ops), static_cast<void*>(d_result),
                       static_cast<void*>(d_b0), static_cast<void*>(d_b1), static_cast<void*>(d_prof8),
                       static_cast<void*>(d_prof32), static_cast<void*>(d_query), static_cast<void*>(d_jobs)})
-        if (ptr) cudaFree(ptr);
+        dev_free(ptr, true);
     if (st != SWB_OK) return st;
 
     for (size_t j = 0; j < jobs.size(); ++j) {
@@ -316,6 +320,7 @@ swb_status swb_align_traceback(const uint8_t* query, uint32_t query_len, const u
         out->capped = 1;
         return SWB_OK;
     }
+    BlockCacheScope cache;
     swb_db* db = nullptr;
     const uint8_t* ptrs[1] = {subject};
     const uint32_t ls[1] = {subject_len};

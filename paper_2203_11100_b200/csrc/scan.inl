@@ -167,7 +167,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     if (st != SWB_OK) return st;
     uint8_t* const stage = db->h_stage + db->stage_base;
     if (m > db->query_cap) {
-        if (db->d_query) cudaFree(db->d_query);
+        if (db->d_query) dev_free(db->d_query);
         db->d_query = nullptr;
         st = dev_alloc(&db->d_query, static_cast<size_t>(m) * 2, &db->device_bytes);
         if (st != SWB_OK) return st;
@@ -373,7 +373,7 @@ swb_status select_topk(swb_db* db, const uint64_t* d_in, uint64_t n, uint32_t k,
         const size_t need = static_cast<size_t>(first_blocks) * k;
         if (need > db->sel_cap) {
             for (auto& p : db->d_sel) {
-                if (p) cudaFree(p);
+                if (p) dev_free(p);
                 p = nullptr;
             }
             for (auto& p : db->d_sel)
@@ -398,7 +398,7 @@ swb_status select_topk(swb_db* db, const uint64_t* d_in, uint64_t n, uint32_t k,
     uint64_t pow2 = 2;
     while (pow2 < n) pow2 <<= 1;
     if (pow2 > db->sort_cap) {
-        if (db->d_sort) cudaFree(db->d_sort);
+        if (db->d_sort) dev_free(db->d_sort);
         db->d_sort = nullptr;
         if ((st = dev_alloc(&db->d_sort, pow2, &db->device_bytes)) != SWB_OK) return st;
         db->sort_cap = pow2;

@@ -569,3 +569,54 @@ def test_traceback_in_several_rounds():
     out = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-q", "-x", "-k", "traceback and not several_rounds"], cwd=root,
                          env=dict(os.environ, SWB200_TRACEBACK_ROUND_KB="64"), capture_output=True, text=True, timeout=900)
     assert out.returncode == 0 and " passed" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
+
+
+def test_adhoc_entry_points_from_many_threads(port, b62):
+    """sw_score_scalar / sw_score_batch / sw_score_wavefront / merge_results take plain sequences (align.hpp:42,91,166,
+    scheduler.hpp:106): each call builds a handle from the library's block cache (cabi.cu: BlockCacheScope).  Six threads
+    mix the four entry points with shapes that change from call to call (blocks move between size classes and
+    threads), next to a resident database whose blocks never enter the cache; every result against the oracle."""
+    import threading
+    from paper_2203_11100_b200 import encode_keys
+    qs, sdb = synth.config1()
+    g = GapModel(10, 2)
+    errors = []
+
+    def worker(seed):
+        rng = np.random.default_rng(seed)
+        try:
+            for it in range(25):
+                q = synth.random_residues(rng, int(rng.integers(1, 700)))
+                kind = (seed + it) % 4
+                if kind == 0:
+                    s = synth.random_residues(rng, int(rng.integers(1, 3000)))
+                    assert score_wavefront(q, s, b62, g, 64) == port.score_scalar(q, s, b62, 10, 2)
+                elif kind == 1:
+                    subs = [synth.random_residues(rng, int(rng.integers(1, 900))) for _ in range(int(rng.integers(1, 70)))]
+                    got = score_batch(q, subs, len(subs), b62, g)
+                    assert got.tolist() == [port.score_scalar(q, s, b62, 10, 2) for s in subs]
+                elif kind == 2:
+                    n = int(rng.integers(1, 30000))
+                    index = rng.permutation(n).astype(np.uint32)
+                    score = rng.integers(0, 50, n).astype(np.int32)
+                    k = int(rng.integers(1, 40))
+                    idx, sc = merge_keys(encode_keys(index, score), k)
+                    order = np.lexsort((index, -score.astype(np.int64)))[:k]
+                    assert idx.tolist() == index[order].tolist() and sc.tolist() == score[order].tolist()
+                else:
+                    seqs = [synth.random_residues(rng, int(rng.integers(1, 400))) for _ in range(70)]
+                    with Database.from_sequences(seqs) as small:     # a resident handle: driver blocks, not the cache
+                        idx, sc, _ = small.search(q, b62, g, 5)
+                    ei, es, _ = port.run_search(q, po.FlatDb.from_list(seqs), b62, 10, 2, top_k=5)
+                    assert idx.tolist() == list(ei) and sc.tolist() == list(es)
+        except Exception as e:   # noqa: BLE001 -- reported by the main thread
+            errors.append((seed, repr(e)))
+
+    with Database(sdb.codes, sdb.offsets) as db:
+        before = db.search(qs[0], b62, g, 10)[:2]
+        threads = [threading.Thread(target=worker, args=(100 + i,)) for i in range(6)]
+        [t.start() for t in threads]
+        [t.join() for t in threads]
+        after = db.search(qs[0], b62, g, 10)[:2]
+    assert not errors, errors
+    assert (before[0] == after[0]).all() and (before[1] == after[1]).all()
