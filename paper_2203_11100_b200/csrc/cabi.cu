@@ -899,8 +899,8 @@ swb_status swb_scan_plan(const uint32_t* lens, uint32_t n, uint64_t length_thres
     shape.sm_count = sm_count;
     shape.warps_per_cta = kInterThreads / 32;
     shape.policy = policy;
-    shape.pipe_rings = ring_chunks_for(static_cast<size_t>(kProfRows) * profile_stride(query_len, kInterTile), kSmemOptinB200,
-                                       sizeof(PipeCtl), static_cast<size_t>(kPipeWarps) * kPipeChunkBytes, scan_knobs().pipe_ring_cap);
+    shape.pipe_rings = pipe_rings_for(static_cast<size_t>(kProfRows) * profile_stride(query_len, kInterTile), kSmemOptinB200,
+                                      sizeof(PipeCtl), static_cast<size_t>(kPipeWarps) * kPipeChunkBytes, scan_knobs().pipe_ring_cap).chunks;
     std::vector<uint32_t> us(static_cast<size_t>(n_groups) + 1), vso(n_groups);
     std::vector<uint8_t> modes(n_groups);
     const ScanPlan sp = plan_scan(shape, scan_knobs(), us.data(), vso.data(), modes.data());

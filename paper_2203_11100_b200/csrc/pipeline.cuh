@@ -129,20 +129,27 @@ __device__ __forceinline__ uint32_t pipe_item(uint32_t* ticket, uint32_t n_items
     return __shfl_sync(0xffffffffu, g, 0);
 }
 
-template <int T, int kThreads>
+// kSlice: the query's profile does not fit shared memory next to the rings (m beyond ~6,500): every warp keeps the 25 x 32 B
+// slice of its current tile only (rows kPipeSliceStride apart) and reloads it from the profile in global memory at every slot
+// start, as the two-stream kernel does (scan_plan.hpp: pipe_rings_for).  prof_bytes is then the 16 slices' size.
+template <int T, int kThreads, bool kSlice>
 __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p) {
     static_assert(T % 16 == 0, "tile width must be a multiple of 16 columns");
+    static_assert(!kSlice || T == 32, "the slice layout assumes 32-column tiles");
     static_assert(kThreads == kPipeWarps * 32, "CTA shape");
+    static_assert(kPipeWarps == kPipeWarpsHost && kProfRows * kPipeSliceStride <= kPipeSliceBytes, "slice geometry");
     extern __shared__ __align__(256) uint8_t smem[];
     int8_t* prof = reinterpret_cast<int8_t*>(smem);
     PipeCtl* ctl = reinterpret_cast<PipeCtl*>(smem + p.prof_bytes);
     uint8_t* rings = smem + p.prof_bytes + sizeof(PipeCtl);
 
     {
-        const uint32_t n16 = kProfRows * p.pstride / 16;
-        const uint4* src = reinterpret_cast<const uint4*>(p.prof8);
-        uint4* dst = reinterpret_cast<uint4*>(smem);
-        for (uint32_t i = threadIdx.x; i < n16; i += kThreads) dst[i] = src[i];
+        if (!kSlice) {
+            const uint32_t n16 = kProfRows * p.pstride / 16;
+            const uint4* src = reinterpret_cast<const uint4*>(p.prof8);
+            uint4* dst = reinterpret_cast<uint4*>(smem);
+            for (uint32_t i = threadIdx.x; i < n16; i += kThreads) dst[i] = src[i];
+        }
         uint32_t* c = reinterpret_cast<uint32_t*>(ctl);
         for (uint32_t i = threadIdx.x; i < sizeof(PipeCtl) / 4; i += kThreads) c[i] = 0;
         __syncthreads();
@@ -182,7 +189,18 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
         if (lane == 0) ctl->warp_item[warp] = item;
         const GroupDesc gd = p.groups[g];
         const bool first = tile == 0, last = tile + 1 == p.n_tiles;
-        const int8_t* ptile = prof + tile * T;
+        const int8_t* ptile = kSlice ? prof + (threadIdx.x >> 5) * kPipeSliceBytes : prof + tile * T;
+        const uint32_t pstr = kSlice ? kPipeSliceStride : p.pstride;
+        if (kSlice) {
+            // this tile's 25 rows x 32 B -> the warp's own slice (50 loads of 16 B over the warp)
+            __syncwarp();
+            for (uint32_t i = lane; i < kProfRows * 2; i += 32) {
+                const uint32_t row = i >> 1, part = i & 1;
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.prof8 + static_cast<size_t>(row) * p.pstride + tile * T) + part);
+                reinterpret_cast<uint4*>(const_cast<int8_t*>(ptile) + row * kPipeSliceStride)[part] = v;
+            }
+            __syncwarp();
+        }
         const uint4* gcodes = p.codes + gd.chunk_base * 32 + lane;
         uint8_t* gborder = reinterpret_cast<uint8_t*>(p.border + gd.chunk_base * kRowsPerChunk * 32 + lane);
         const uint8_t* gstage = reinterpret_cast<const uint8_t*>(p.border + gd.chunk_base * kRowsPerChunk * 32) + lane * 16;
@@ -236,8 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
             uint2 bnext = make_uint2(NO, NO);
             if (!first) bnext = bin[0];
             // the first 16 columns' profile bytes of a row are loaded while the previous row is computed
-            const int8_t* pa_next = ptile + (cur.x & 0xffu) * p.pstride;
-            const int8_t* pb_next = ptile + (cur.z & 0xffu) * p.pstride;
+            const int8_t* pa_next = ptile + (cur.x & 0xffu) * pstr;
+            const int8_t* pb_next = ptile + (cur.z & 0xffu) * pstr;
             uint4 va_next = *reinterpret_cast<const uint4*>(pa_next), vb_next = *reinterpret_cast<const uint4*>(pb_next);
 #pragma unroll
             for (int r = 0; r < static_cast<int>(kRowsPerChunk); ++r) {
@@ -255,8 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1) pipeline_s16_kernel(PipeParams p)
                 if (r + 1 < static_cast<int>(kRowsPerChunk)) {
                     const uint32_t wa = r + 1 < 4 ? cur.x : cur.y;
                     const uint32_t wb = r + 1 < 4 ? cur.z : cur.w;
-                    pa_next = ptile + ((wa >> (8 * ((r + 1) & 3))) & 0xffu) * p.pstride;
-                    pb_next = ptile + ((wb >> (8 * ((r + 1) & 3))) & 0xffu) * p.pstride;
+                    pa_next = ptile + ((wa >> (8 * ((r + 1) & 3))) & 0xffu) * pstr;
+                    pb_next = ptile + ((wb >> (8 * ((r + 1) & 3))) & 0xffu) * pstr;
                     va_next = *reinterpret_cast<const uint4*>(pa_next);
                     vb_next = *reinterpret_cast<const uint4*>(pb_next);
                 }

@@ -9,9 +9,9 @@ const ScanKnobs& scan_knobs() {
 }
 
 // Capacity of each border ring of the pipeline kernel next to a profile of `prof_elems` bytes; < 2: it cannot run.
-uint32_t pipe_ring_chunks(const swb_db* db, size_t prof_elems) {
-    return ring_chunks_for(prof_elems, db->smem_optin, sizeof(PipeCtl), static_cast<size_t>(kPipeWarps) * kPipeChunkBytes,
-                           scan_knobs().pipe_ring_cap);
+PipeRings pipe_ring_chunks(const swb_db* db, size_t prof_elems) {
+    return pipe_rings_for(prof_elems, db->smem_optin, sizeof(PipeCtl), static_cast<size_t>(kPipeWarps) * kPipeChunkBytes,
+                          scan_knobs().pipe_ring_cap);
 }
 
 QueryPlan make_plan(const swb_db* db, uint32_t m, const int32_t* matrix, int32_t open, int32_t ext) {

@@ -1,6 +1,11 @@
 // scan.inl -- one search on one shard: upload, profile, unit table, packed scan, int32 re-run, top-k select.
 // Included by cabi.cu inside its anonymous namespace.
 
+void launch_pipeline(const PipeParams& qp, bool slices, uint32_t grid, size_t smem, cudaStream_t s) {
+    if (slices) pipeline_s16_kernel<kInterTile, kInterThreads, true><<<grid, kInterThreads, smem, s>>>(qp);
+    else pipeline_s16_kernel<kInterTile, kInterThreads, false><<<grid, kInterThreads, smem, s>>>(qp);
+}
+
 template <int T, typename PT>
 void launch_intra(const IntraParams& ip, uint32_t ctas, uint32_t warps, cudaStream_t s) {
     // the int8 flavour stages each lane's 25 profile words in shared memory: 200 B per thread, 50 KB for 8 warps
@@ -183,7 +188,8 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
     uint32_t wave_sms = static_cast<uint32_t>(db->sm_count);   // SMs the wavefront kernel gets
     uint32_t wave_threads = kInterThreads;                      // and its CTA size
     const size_t prof_elems = static_cast<size_t>(kProfRows) * pl.pstride;
-    const uint32_t pipe_rings = pipe_ring_chunks(db, prof_elems);
+    const PipeRings pipe_ring_plan = pipe_ring_chunks(db, prof_elems);
+    const uint32_t pipe_rings = pipe_ring_plan.chunks;
     bool any_narrow = false, any_rowblock = false;
     if (packed) {
         // which kernel scans which groups, and the wavefront kernel's units: scan_plan.hpp
@@ -276,7 +282,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         qp.n_items = n_pipe_items;
         qp.prof8 = db->d_prof8;
         qp.pstride = pl.pstride;
-        qp.prof_bytes = static_cast<uint32_t>((prof_elems + 255) & ~size_t(255));
+        qp.prof_bytes = static_cast<uint32_t>(pipe_ring_plan.prof_bytes);   // the whole profile, or 16 tile slices
         qp.n_tiles = n_tiles;
         qp.ring_chunks = pipe_rings;
         qp.lag_div = scan_knobs().pipe_lag_div;
@@ -287,7 +293,9 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         qp.neg_ext2 = pack16(-ext);
         pipe_smem = qp.prof_bytes + sizeof(PipeCtl) + static_cast<size_t>(kPipeWarps) * qp.ring_chunks * kPipeChunkBytes;
         if (!db->pipe_attr_set) {
-            SWB_CUDA(cudaFuncSetAttribute(pipeline_s16_kernel<kInterTile, kInterThreads>,
+            SWB_CUDA(cudaFuncSetAttribute(pipeline_s16_kernel<kInterTile, kInterThreads, false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(db->smem_optin)));
+            SWB_CUDA(cudaFuncSetAttribute(pipeline_s16_kernel<kInterTile, kInterThreads, true>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(db->smem_optin)));
             db->pipe_attr_set = true;
         }
@@ -299,10 +307,10 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         if (wave_grid) {
             SWB_CUDA(cudaEventRecord(db->ev_fork, s));
             SWB_CUDA(cudaStreamWaitEvent(db->side_stream, db->ev_fork, 0));
-            pipeline_s16_kernel<kInterTile, kInterThreads><<<side_grid, kInterThreads, pipe_smem, db->side_stream>>>(qp);
+            launch_pipeline(qp, pipe_ring_plan.slices, side_grid, pipe_smem, db->side_stream);
             SWB_CUDA(cudaEventRecord(db->ev_join, db->side_stream));
         } else {
-            pipeline_s16_kernel<kInterTile, kInterThreads><<<side_grid, kInterThreads, pipe_smem, s>>>(qp);
+            launch_pipeline(qp, pipe_ring_plan.slices, side_grid, pipe_smem, s);
         }
         ++db->launches;
     }
@@ -338,7 +346,7 @@ swb_status score_core(swb_db* db, const uint8_t* query, uint32_t m, const int32_
         if ((st = launch_wavefront(db, wp, grid, wave_threads, wave_smem, any_narrow, any_rowblock, s)) != SWB_OK) return st;
         if (n_pipe_items) {
             // the wavefront kernel's SMs are free now: let them help with whatever pipeline items are left
-            pipeline_s16_kernel<kInterTile, kInterThreads><<<grid, kInterThreads, pipe_smem, s>>>(qp);
+            launch_pipeline(qp, pipe_ring_plan.slices, grid, pipe_smem, s);
             ++db->launches;
             SWB_CUDA(cudaStreamWaitEvent(s, db->ev_join, 0));
         }

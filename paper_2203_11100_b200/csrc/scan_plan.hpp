@@ -458,6 +458,35 @@ inline uint32_t ring_chunks_for(size_t prof_bytes, size_t smem_optin, size_t fix
     return c;
 }
 
+// The pipeline kernel keeps the query's whole int8 profile in shared memory while at least two chunks per ring fit next to
+// it (m up to ~6,500); beyond that each warp keeps only the slice of its current tile (25 rows x 32 B, kPipeSliceStride apart,
+// reloaded at every slot start), the rings get their full capacity and shared memory no longer depends on m.
+// SWB200_PIPE_SLICES=1 takes the slice form for every query (measurement).
+constexpr uint32_t kPipeSliceStride = 48;     // bytes between the rows of a warp's slice: 16-byte groups 3 apart modulo 8
+constexpr uint32_t kPipeSliceBytes = 1280;    // 25 rows x 48 B, rounded up to 256
+constexpr uint32_t kPipeWarpsHost = 16;
+struct PipeRings {
+    uint32_t chunks = 0;      // capacity of each ring; < 2: the pipeline cannot run
+    bool slices = false;      // per-warp tile slices instead of the whole profile
+    size_t prof_bytes = 0;    // shared memory in front of the control block
+};
+inline PipeRings pipe_rings_for(size_t prof_bytes, size_t smem_optin, size_t fixed_bytes, size_t ring_chunk_bytes_all_warps,
+                                uint32_t cap) {
+    static const bool force = [] {
+        const char* e = std::getenv("SWB200_PIPE_SLICES");
+        return e != nullptr && *e == '1';
+    }();
+    PipeRings r;
+    r.prof_bytes = (prof_bytes + 255) & ~size_t(255);
+    r.chunks = ring_chunks_for(prof_bytes, smem_optin, fixed_bytes, ring_chunk_bytes_all_warps, cap);
+    if (r.chunks < 2 || force) {
+        r.slices = true;
+        r.prof_bytes = static_cast<size_t>(kPipeWarpsHost) * kPipeSliceBytes;
+        r.chunks = ring_chunks_for(r.prof_bytes, smem_optin, fixed_bytes, ring_chunk_bytes_all_warps, cap);
+    }
+    return r;
+}
+
 // Row stride of the int8 profile: columns padded to whole 32-column tiles, then to 16 (mod 128) bytes so that the
 // 25 rows spread over the shared-memory banks.
 inline uint32_t profile_stride(uint32_t m, uint32_t tile) {

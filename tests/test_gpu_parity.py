@@ -514,6 +514,21 @@ def test_narrow_block_sweep_against_the_oracle():
             assert "(4, 256, True)" in out.stdout, out.stdout[-1500:]     # 4-column tiles, CTAs of 4 + 4 warps (helpers), link buffers
 
 
+def test_pipeline_tile_slices_against_the_oracle():
+    """The pipeline kernel with per-warp tile slices instead of the whole profile in shared memory (queries beyond ~6,500
+    residues): forced for every query length (SWB200_PIPE_SLICES=1), and by itself for 6,600- and 7,000-residue queries;
+    whole score vectors equal the oracle's (tests/_slice_small.py)."""
+    import os, subprocess, sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    for extra in ({"SWB200_PIPE_SLICES": "1"}, {}):
+        env = dict(os.environ, **extra)
+        env.pop("SWB200_PIPE_SLICES", None) if not extra else None
+        out = subprocess.run([sys.executable, str(root / "tests" / "_slice_small.py")], cwd=root, env=env, capture_output=True,
+                             text=True, timeout=900)
+        assert out.returncode == 0 and "SLICE-SMALL-OK" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
+
+
 def test_large_random_batch_shares_scans_and_equals_single_searches(b62):
     """A batch of 60 queries of random lengths (with duplicates, an empty one and a one-residue one) on a database
     where shared scans apply: swb_search_many's ranked lists equal swb_search's, query by query, and the plan it
