@@ -244,9 +244,11 @@ def test_scan_plan_policies_and_small_databases(lib):
     assert short["chain_bound"] == 0 and short["pipeline_groups"] == 0 and short["wavefront_sms"] == 148   # wavefront kernel only
     small = search.scan_plan(lens[:10_000], 2005)                      # 157 groups < 2 per SM
     assert small["pipeline_groups"] == 0
-    huge = search.scan_plan(lens, 9000)                                # the profile leaves no room for the rings
-    assert huge["ring_chunks"] < 2 and huge["pipeline_groups"] == 0
-    assert search.scan_plan(lens, 9000, policy=search.Database.SCAN_PIPELINE)["pipeline_groups"] == 0
+    huge = search.scan_plan(lens, 9000)                                # the whole profile leaves no room for the rings:
+    assert huge["ring_chunks"] == 4 and huge["pipeline_groups"] > 0        # per-warp tile slices, rings at full capacity
+    edge = search.scan_plan(lens, 6000)                                    # whole profile (150 KB) + rings of 2 chunks
+    assert edge["ring_chunks"] == 2 and edge["pipeline_groups"] > 0
+    assert search.scan_plan(lens, 9000, policy=search.Database.SCAN_PIPELINE)["pipeline_groups"] == 8843
     shard = search.scan_plan(lens, 2005, shard_rank=3, shard_count=8)  # 1/8 of the database: still hybrid
     assert shard["n_groups"] in (1105, 1106) and shard["pipeline_groups"] > 0.9 * shard["n_groups"]
     empty = search.scan_plan(np.zeros(0, np.uint32), 100)
