@@ -29,5 +29,7 @@ cap duo_sweep duo_pipeline_kernel 1 python tests/manual/duo_profile.py sweep 2
 cap pipeline_m2005 pipeline_s16_kernel 1 python tests/manual/pipe_profile.py 2005 2
 cap wavefront_narrow_shard8_m144 wavefront_s16_kernel 2 python tools/chain_probe2.py 8 0 3
 SWB_PROFILE_SHARD=5/8 cap duo_pass_items_shard8 duo_pipeline_kernel 1 python tests/manual/duo_profile.py sweep 2
-rm -f $o/${tag}_ncu_*.ncu-rep.tmp
-ls -la $o | tail -40
+# the reports themselves (20 MB each) would push gpurun_out/ past what travels back: keep the exported pages only
+rm -f $o/${tag}_ncu_*.ncu-rep $o/${tag}_ncu_*.ncu-rep.tmp
+tail -3 $o/${tag}_gputests.log; tail -2 $o/${tag}_smoke.log; cat $o/${tag}_scaling_probe.txt $o/${tag}_scaling_probe_batched.txt $o/${tag}_slice_probe.txt | tail -40
+du -sh $o
