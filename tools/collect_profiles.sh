@@ -5,7 +5,8 @@
 set -e
 tag=$1
 cd "$(dirname "$0")/.."
-for f in bench.json bench_reference_arm.json bench_launches.csv rehearsal_n2.json sanitize_memcheck.log scaling_probe.txt pair_call_cost.txt slice_probe.txt \
+for f in bench.json bench_reference_arm.json bench_launches.csv rehearsal_n2.json sanitize_memcheck.log scaling_probe.txt scaling_probe_batched.txt pair_call_cost.txt slice_probe.txt gputests.log \
+         ncu_duo_pass_items_shard8_raw.csv ncu_duo_pass_items_shard8_details.txt \
          ncu_duo_sweep_raw.csv ncu_duo_sweep_details.txt ncu_pipeline_m2005_raw.csv ncu_pipeline_m2005_details.txt \
          ncu_wavefront_narrow_shard8_m144_raw.csv ncu_wavefront_narrow_shard8_m144_details.txt; do
   [ -f gpurun_out/${tag}_$f ] && cp gpurun_out/${tag}_$f profiles/
@@ -14,8 +15,10 @@ done
 python tools/launch_shares.py profiles/${tag}_bench_launches.csv \
   "bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-extra-workloads under ncu --metrics gpu__time_duration.sum --clock-control none (${tag})" \
   > profiles/${tag}_bench_launch_shares.csv
+pass_items=profiles/${tag}_ncu_duo_pass_items_shard8_raw.csv
+[ -f $pass_items ] || pass_items=profiles/r02r_ncu_duo_pass_items_shard8_raw.csv
 python tools/traffic_from_ncu.py profiles/${tag}_ncu_duo_sweep_raw.csv duo_pipeline \
   "the whole 20-query sweep as one shared scan (two streams of 653 tiles)" 4087906000 \
   "pipeline_s16_kernel=profiles/${tag}_ncu_pipeline_m2005_raw.csv:pipeline_s16:2005" \
-  "duo_pipeline_kernel (pass items, shard 5 of 8; captured before the last kernel clean-up)=profiles/r02r_ncu_duo_pass_items_shard8_raw.csv:duo_pipeline:sweep" \
+  "duo_pipeline_kernel (pass items, shard 5 of 8)=$pass_items:duo_pipeline:sweep" \
   "wavefront_s16_kernel (narrow units, shard 0 of 8)=profiles/${tag}_ncu_wavefront_narrow_shard8_m144_raw.csv:wavefront_s16:144"
